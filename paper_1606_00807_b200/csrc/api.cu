@@ -1,0 +1,385 @@
+// Device side of the C-ABI (include/enkf_mc.h): map upload, workspace, stage launchers and
+// the host-buffer entry point that assimilate_parallel binds (driver.py:159-253).
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+#include "plan.h"
+
+#define CK(expr)                                                                          \
+    do {                                                                                  \
+        cudaError_t _e = (expr);                                                          \
+        if (_e != cudaSuccess) {                                                          \
+            enkfmc_set_error(std::string("CUDA error: ") + cudaGetErrorString(_e) + " at " #expr); \
+            return ENKFMC_E_CUDA;                                                         \
+        }                                                                                 \
+    } while (0)
+
+struct DeviceState {
+    int device = -1, sm_count = 0;
+    size_t smem_limit = 0;
+    // maps
+    int64_t *tile_ptr = nullptr, *row_ptr = nullptr, *csc_ptr = nullptr, *csc_src = nullptr;
+    int32_t *col_idx = nullptr, *csc_row = nullptr, *phys = nullptr, *iphys = nullptr, *bw = nullptr,
+            *state_row = nullptr, *pred_state = nullptr, *work_order = nullptr, *tile_order = nullptr;
+    uint8_t *is_interior = nullptr;
+    int32_t *obs_slot = nullptr, *tile_nobs = nullptr;
+    bool obs_current = false;
+    // workspace
+    int64_t ws_nens = 0;
+    double *U = nullptr, *T = nullptr, *D = nullptr, *scratch = nullptr;
+    int32_t *flags = nullptr, *status = nullptr;
+    unsigned int *counters = nullptr;
+    SolveParams solve_layout{};
+    int solve_grid = 0;
+    // host-path staging
+    double *dX = nullptr, *dXa = nullptr, *dR = nullptr, *dYs = nullptr;
+    int64_t stage_nens = 0, stage_nobs = -1;
+    cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    cudaStream_t stream = nullptr;
+};
+
+namespace {
+
+template <class T>
+int upload(T *&dst, const std::vector<T> &src) {
+    if (dst) { cudaFree(dst); dst = nullptr; }
+    const size_t bytes = std::max<size_t>(src.size(), 1) * sizeof(T);
+    CK(cudaMalloc(&dst, bytes));
+    if (!src.empty()) CK(cudaMemcpy(dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return ENKFMC_OK;
+}
+
+template <class T>
+void release(T *&p) { if (p) { cudaFree(p); p = nullptr; } }
+
+int ensure_device(enkfmc_plan *p) {
+    if (p->dev) return ENKFMC_OK;
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0) {
+        enkfmc_set_error(std::string("no CUDA device available (") + cudaGetErrorString(e) +
+                         "); libenkfmc has no CPU fallback");
+        return ENKFMC_E_CUDA;
+    }
+    auto *d = new DeviceState();
+    CK(cudaGetDevice(&d->device));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, d->device));
+    if (prop.major < 10) {
+        enkfmc_set_error("libenkfmc is built for sm_100a only; found sm_" + std::to_string(prop.major) +
+                         std::to_string(prop.minor));
+        delete d;
+        return ENKFMC_E_CUDA;
+    }
+    d->sm_count = prop.multiProcessorCount;
+    d->smem_limit = prop.sharedMemPerBlockOptin;
+    p->dev = d;
+    int rc;
+    if ((rc = upload(d->tile_ptr, p->tile_ptr))) return rc;
+    if ((rc = upload(d->row_ptr, p->row_ptr))) return rc;
+    if ((rc = upload(d->csc_ptr, p->csc_ptr))) return rc;
+    if ((rc = upload(d->csc_src, p->csc_src))) return rc;
+    if ((rc = upload(d->col_idx, p->col_idx))) return rc;
+    if ((rc = upload(d->csc_row, p->csc_row))) return rc;
+    if ((rc = upload(d->phys, p->phys))) return rc;
+    if ((rc = upload(d->iphys, p->iphys))) return rc;
+    if ((rc = upload(d->bw, p->bw))) return rc;
+    if ((rc = upload(d->state_row, p->state_row))) return rc;
+    if ((rc = upload(d->pred_state, p->pred_state))) return rc;
+    if ((rc = upload(d->work_order, p->work_order))) return rc;
+    if ((rc = upload(d->tile_order, p->tile_order))) return rc;
+    if ((rc = upload(d->is_interior, p->is_interior))) return rc;
+    CK(cudaMalloc(&d->counters, 4 * sizeof(unsigned int)));
+    CK(cudaMemset(d->counters, 0, 4 * sizeof(unsigned int)));
+    for (auto &ev : d->ev) CK(cudaEventCreate(&ev));
+    CK(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
+    return ENKFMC_OK;
+}
+
+int ensure_obs(enkfmc_plan *p) {
+    DeviceState *d = p->dev;
+    if (d->obs_current) return ENKFMC_OK;
+    if (!p->have_obs) { enkfmc_set_error("observations not set on this plan"); return ENKFMC_E_VALUE; }
+    int rc;
+    if ((rc = upload(d->obs_slot, p->obs_slot))) return rc;
+    if ((rc = upload(d->tile_nobs, p->tile_nobs))) return rc;
+    d->obs_current = true;
+    return ENKFMC_OK;
+}
+
+int check_nens(int64_t nens) {
+    if (nens < 2) {
+        enkfmc_set_error("ensemble size must be at least 2, got " + std::to_string(nens));
+        return ENKFMC_E_CONFIG;
+    }
+    if (nens > ENKFMC_MAX_NENS) {
+        enkfmc_set_error("ensemble size " + std::to_string(nens) + " exceeds the kernel cap " +
+                         std::to_string(ENKFMC_MAX_NENS));
+        return ENKFMC_E_CAPACITY;
+    }
+    return ENKFMC_OK;
+}
+
+// Solve-stage layout (scratch, window placement) for a given ensemble size.
+int ensure_solve_layout(enkfmc_plan *p, int64_t nens) {
+    DeviceState *d = p->dev;
+    if (d->scratch && d->solve_layout.N == (int)nens) return ENKFMC_OK;
+    release(d->scratch);
+    SolveParams &L = d->solve_layout;
+    L = SolveParams{};
+    L.N = (int)nens;
+    L.bmax = (int)p->max_bw;
+    int64_t band = 1;
+    for (int64_t t = 0; t < p->ntiles; ++t)
+        band = std::max(band, (p->tile_ptr[t + 1] - p->tile_ptr[t]) * (int64_t)(p->bw[t] + 1));
+    L.nfields = (int)p->nfields;
+    L.ntiles = (int)p->ntiles;
+    const int64_t stride = solve_plan_scratch(L, band, std::max<int64_t>(p->max_nlocal, 1), d->smem_limit);
+    d->solve_grid = solve_grid_size(d->sm_count, L, d->smem_limit);
+    CK(cudaMalloc(&d->scratch, (size_t)stride * d->solve_grid * sizeof(double)));
+    return ENKFMC_OK;
+}
+
+int ensure_workspace(enkfmc_plan *p, int64_t nens) {
+    DeviceState *d = p->dev;
+    if (d->ws_nens == nens && d->U) return ENKFMC_OK;
+    release(d->U); release(d->T); release(d->D); release(d->flags); release(d->status);
+    const int64_t nstate = p->nstate2d * p->nfields;
+    CK(cudaMalloc(&d->U, std::max<size_t>(1, (size_t)nstate * nens) * sizeof(double)));
+    CK(cudaMalloc(&d->T, std::max<size_t>(1, (size_t)p->nnz() * p->nfields) * sizeof(double)));
+    CK(cudaMalloc(&d->D, std::max<size_t>(1, (size_t)p->sum_nlocal() * p->nfields) * sizeof(double)));
+    CK(cudaMalloc(&d->flags, std::max<size_t>(1, (size_t)p->sum_nlocal() * p->nfields) * sizeof(int32_t)));
+    CK(cudaMalloc(&d->status, std::max<size_t>(1, (size_t)p->ntiles * p->nfields) * sizeof(int32_t)));
+    d->ws_nens = nens;
+    return ENKFMC_OK;
+}
+
+int do_regress(enkfmc_plan *p, const double *d_U, int64_t nens, double rank_tol, double floor_, double *d_T,
+               double *d_D, int32_t *d_flags, cudaStream_t s) {
+    DeviceState *d = p->dev;
+    RegressParams R{};
+    R.U = d_U; R.N = (int)nens; R.ld = (int)nens | 1; R.pmax = (int)std::max<int64_t>(p->max_pred, 1);
+    R.nfields = (int)p->nfields; R.nloc = p->sum_nlocal(); R.nnz = p->nnz(); R.nstate2d = p->nstate2d;
+    R.nwork = R.nloc * p->nfields;
+    R.row_ptr = d->row_ptr; R.pred_state = d->pred_state; R.state_row = d->state_row; R.work_order = d->work_order;
+    R.rank_tol = rank_tol; R.variance_floor = floor_; R.fast_ratio = 1e-6;
+    R.T = d_T; R.D = d_D; R.flags = d_flags; R.counter = d->counters;
+    if (R.nwork > 0xfffffff0LL) { enkfmc_set_error("too many regressions for one launch"); return ENKFMC_E_CAPACITY; }
+    cudaError_t e = launch_regress(R, d->sm_count, d->smem_limit, s);
+    if (e == cudaErrorInvalidConfiguration) {
+        enkfmc_set_error("regression workspace (nens=" + std::to_string(nens) + ", predecessors=" +
+                         std::to_string(p->max_pred) + ") exceeds shared memory");
+        return ENKFMC_E_CAPACITY;
+    }
+    CK(e);
+    p->counters[0] += 1;
+    return ENKFMC_OK;
+}
+
+int do_solve(enkfmc_plan *p, const double *d_X, const double *d_T, const double *d_D, const double *d_r,
+             const double *d_Ys, int64_t nens, double *d_Xa, int32_t *d_status, cudaStream_t s) {
+    DeviceState *d = p->dev;
+    int rc = ensure_obs(p);
+    if (rc) return rc;
+    if ((rc = ensure_solve_layout(p, nens))) return rc;
+    SolveParams S = d->solve_layout;
+    S.X = d_X; S.T = d_T; S.D = d_D; S.rdiag = d_r; S.Ys = d_Ys; S.Xa = d_Xa;
+    S.nloc = p->sum_nlocal(); S.nnz = p->nnz(); S.nstate2d = p->nstate2d;
+    S.tile_ptr = d->tile_ptr; S.row_ptr = d->row_ptr; S.csc_ptr = d->csc_ptr; S.csc_src = d->csc_src;
+    S.col_idx = d->col_idx; S.csc_row = d->csc_row; S.phys = d->phys; S.iphys = d->iphys; S.bw = d->bw;
+    S.state_row = d->state_row; S.obs_slot = d->obs_slot; S.tile_nobs = d->tile_nobs; S.tile_order = d->tile_order;
+    S.is_interior = d->is_interior; S.scratch = d->scratch; S.status = d_status; S.counter = d->counters + 1;
+    cudaError_t e = launch_local_solve(S, d->solve_grid, d->smem_limit, s);
+    if (e == cudaErrorInvalidConfiguration) {
+        enkfmc_set_error("local-solve window (half-bandwidth " + std::to_string(p->max_bw) + ") exceeds shared memory");
+        return ENKFMC_E_CAPACITY;
+    }
+    CK(e);
+    p->counters[0] += 1;
+    return ENKFMC_OK;
+}
+
+}  // namespace
+
+void enkfmc_device_invalidate_obs(enkfmc_plan *p) { if (p->dev) p->dev->obs_current = false; }
+
+void enkfmc_device_release(enkfmc_plan *p) {
+    DeviceState *d = p->dev;
+    if (!d) return;
+    release(d->tile_ptr); release(d->row_ptr); release(d->csc_ptr); release(d->csc_src); release(d->col_idx);
+    release(d->csc_row); release(d->phys); release(d->iphys); release(d->bw); release(d->state_row);
+    release(d->pred_state); release(d->work_order); release(d->tile_order); release(d->is_interior);
+    release(d->obs_slot); release(d->tile_nobs); release(d->U); release(d->T); release(d->D); release(d->scratch);
+    release(d->flags); release(d->status); release(d->counters); release(d->dX); release(d->dXa); release(d->dR);
+    release(d->dYs);
+    for (auto &ev : d->ev) if (ev) cudaEventDestroy(ev);
+    if (d->stream) cudaStreamDestroy(d->stream);
+    delete d;
+    p->dev = nullptr;
+}
+
+extern "C" int enkfmc_center_rows(const double *d_X, double *d_U, int64_t nrows, int64_t nens, void *stream) {
+    int rc = check_nens(nens);
+    if (rc) return rc;
+    CK(launch_center_rows(d_X, d_U, nrows, (int)nens, (cudaStream_t)stream));
+    return ENKFMC_OK;
+}
+
+extern "C" int enkfmc_regress(enkfmc_plan *p, const double *d_U, int64_t nens, double rank_tol, double floor_,
+                              double *d_T, double *d_D, int32_t *d_flags, void *stream) {
+    int rc = check_nens(nens);
+    if (rc) return rc;
+    if ((rc = ensure_device(p))) return rc;
+    return do_regress(p, d_U, nens, rank_tol, floor_, d_T, d_D, d_flags, (cudaStream_t)stream);
+}
+
+extern "C" int enkfmc_local_solve(enkfmc_plan *p, const double *d_X, const double *d_T, const double *d_D,
+                                  const double *d_r, const double *d_Ys, int64_t nens, double *d_Xa,
+                                  int32_t *d_status, void *stream) {
+    int rc = check_nens(nens);
+    if (rc) return rc;
+    if ((rc = ensure_device(p))) return rc;
+    return do_solve(p, d_X, d_T, d_D, d_r, d_Ys, nens, d_Xa, d_status, (cudaStream_t)stream);
+}
+
+extern "C" int enkfmc_analysis_device(enkfmc_plan *p, const double *d_X, const double *d_r, const double *d_Ys,
+                                      int64_t nens, double rank_tol, double floor_, double *d_Xa, void *stream) {
+    int rc = check_nens(nens);
+    if (rc) return rc;
+    if ((rc = ensure_device(p))) return rc;
+    if ((rc = ensure_workspace(p, nens))) return rc;
+    DeviceState *d = p->dev;
+    cudaStream_t s = (cudaStream_t)stream;
+    CK(launch_center_rows(d_X, d->U, p->nstate2d * p->nfields, (int)nens, s));
+    p->counters[0] += 1;
+    if ((rc = do_regress(p, d->U, nens, rank_tol, floor_, d->T, d->D, d->flags, s))) return rc;
+    return do_solve(p, d_X, d->T, d->D, d_r, d_Ys, nens, d_Xa, d->status, s);
+}
+
+extern "C" int enkfmc_analysis_host(enkfmc_plan *p, const double *X, const double *r_diag, const double *Ys,
+                                    int64_t nens, double rank_tol, double floor_, double *Xa, double *timings_ms) {
+    int rc = check_nens(nens);
+    if (rc) return rc;
+    if ((rc = ensure_device(p))) return rc;
+    if ((rc = ensure_workspace(p, nens))) return rc;
+    DeviceState *d = p->dev;
+    const int64_t nstate = p->nstate2d * p->nfields;
+    const size_t xbytes = (size_t)nstate * nens * sizeof(double);
+    if (d->stage_nens != nens || !d->dX) {
+        release(d->dX); release(d->dXa);
+        CK(cudaMalloc(&d->dX, std::max<size_t>(xbytes, 8)));
+        CK(cudaMalloc(&d->dXa, std::max<size_t>(xbytes, 8)));
+        d->stage_nens = nens;
+        d->stage_nobs = -1;
+    }
+    if (d->stage_nobs != p->nobs) {
+        release(d->dR); release(d->dYs);
+        CK(cudaMalloc(&d->dR, std::max<size_t>((size_t)p->nobs, 1) * sizeof(double)));
+        CK(cudaMalloc(&d->dYs, std::max<size_t>((size_t)p->nobs * nens, 1) * sizeof(double)));
+        d->stage_nobs = p->nobs;
+    }
+    cudaStream_t s = d->stream;
+    CK(cudaEventRecord(d->ev[0], s));
+    CK(cudaMemcpyAsync(d->dX, X, xbytes, cudaMemcpyHostToDevice, s));
+    if (p->nobs) {
+        CK(cudaMemcpyAsync(d->dR, r_diag, (size_t)p->nobs * sizeof(double), cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(d->dYs, Ys, (size_t)p->nobs * nens * sizeof(double), cudaMemcpyHostToDevice, s));
+    }
+    CK(cudaEventRecord(d->ev[1], s));
+    CK(launch_center_rows(d->dX, d->U, nstate, (int)nens, s));
+    p->counters[0] += 1;
+    if ((rc = do_regress(p, d->U, nens, rank_tol, floor_, d->T, d->D, d->flags, s))) return rc;
+    CK(cudaEventRecord(d->ev[2], s));
+    if ((rc = do_solve(p, d->dX, d->T, d->D, d->dR, d->dYs, nens, d->dXa, d->status, s))) return rc;
+    CK(cudaEventRecord(d->ev[3], s));
+    CK(cudaMemcpyAsync(Xa, d->dXa, xbytes, cudaMemcpyDeviceToHost, s));
+    CK(cudaEventRecord(d->ev[4], s));
+    CK(cudaStreamSynchronize(s));
+    if (timings_ms) {
+        for (int k = 0; k < 4; ++k) {
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, d->ev[k], d->ev[k + 1]));
+            timings_ms[k] = ms;
+        }
+    }
+    // per-tile status -> NumericalError naming the sub-domain
+    std::vector<int32_t> st((size_t)(p->ntiles * p->nfields));
+    if (!st.empty()) CK(cudaMemcpy(st.data(), d->status, st.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    p->counters[4] = -1;
+    for (size_t it = 0; it < st.size(); ++it) {
+        if (st[it] != 0) {
+            const int64_t f = (int64_t)it / p->ntiles, t = (int64_t)it % p->ntiles;
+            p->counters[4] = (int64_t)it;
+            enkfmc_set_error("primal analysis solve failed in subdomain " + std::to_string(t) + " (field " +
+                             std::to_string(f) + "): " +
+                             (st[it] == 1 ? "matrix not positive definite" : "non-finite pivot"));
+            return ENKFMC_E_NUMERIC;
+        }
+    }
+    return ENKFMC_OK;
+}
+
+extern "C" int64_t enkfmc_plan_counter(const enkfmc_plan *p, int what) {
+    if (what < 0 || what >= 8) return -1;
+    return p->counters[what];
+}
+
+extern "C" void *enkfmc_plan_device_buffer(const enkfmc_plan *p, int what) {
+    if (!p->dev) return nullptr;
+    switch (what) {
+        case 0: return p->dev->U;
+        case 1: return p->dev->T;
+        case 2: return p->dev->D;
+        case 3: return p->dev->flags;
+        case 4: return p->dev->status;
+        default: return nullptr;
+    }
+}
+
+extern "C" int enkfmc_scatter_rows(double *d_dst, const int64_t *d_dst_rows, const double *d_src,
+                                   const int64_t *d_src_rows, int64_t nrows, int64_t nens, void *stream) {
+    if (nens < 1) { enkfmc_set_error("nens must be positive"); return ENKFMC_E_VALUE; }
+    CK(launch_scatter_rows(d_dst, d_dst_rows, d_src, d_src_rows, nrows, (int)nens, (cudaStream_t)stream));
+    return ENKFMC_OK;
+}
+
+extern "C" int enkfmc_assemble_band(enkfmc_plan *p, const double *d_T, const double *d_D, int64_t tile,
+                                    double *d_band, void *stream) {
+    if (tile < 0 || tile >= p->ntiles) { enkfmc_set_error("tile index out of range"); return ENKFMC_E_VALUE; }
+    int rc = ensure_device(p);
+    if (rc) return rc;
+    if ((rc = ensure_solve_layout(p, 2))) return rc;
+    DeviceState *d = p->dev;
+    SolveParams S = d->solve_layout;
+    S.T = d_T; S.D = d_D;
+    S.nloc = p->sum_nlocal(); S.nnz = p->nnz(); S.nstate2d = p->nstate2d;
+    S.tile_ptr = d->tile_ptr; S.row_ptr = d->row_ptr; S.csc_ptr = d->csc_ptr; S.csc_src = d->csc_src;
+    S.col_idx = d->col_idx; S.csc_row = d->csc_row; S.phys = d->phys; S.iphys = d->iphys; S.bw = d->bw;
+    S.state_row = d->state_row; S.obs_slot = d->state_row /* unused */; S.tile_nobs = d->bw /* unused */;
+    S.tile_order = d->tile_order; S.is_interior = d->is_interior; S.scratch = d->scratch;
+    S.status = nullptr; S.counter = d->counters + 1;
+    S.assemble_only = 1; S.tile_sel = (int)tile; S.band_out = d_band;
+    CK(launch_local_solve(S, 1, d->smem_limit, (cudaStream_t)stream));
+    p->counters[0] += 1;
+    return ENKFMC_OK;
+}
+
+extern "C" int enkfmc_precision_apply(enkfmc_plan *p, const double *d_T, const double *d_D, const double *d_V,
+                                      int64_t ncols, double *d_tmp, double *d_out, void *stream) {
+    if (p->ntiles != 1 || p->nfields != 1) {
+        enkfmc_set_error("precision_apply needs a single-tile plan");
+        return ENKFMC_E_VALUE;
+    }
+    int rc = ensure_device(p);
+    if (rc) return rc;
+    DeviceState *d = p->dev;
+    CK(launch_precision_apply(d->row_ptr, d->col_idx, d->csc_ptr, d->csc_row, d->csc_src, d_T, d_D, d_V, d_tmp,
+                              d_out, p->sum_nlocal(), ncols, (cudaStream_t)stream));
+    p->counters[0] += 2;
+    return ENKFMC_OK;
+}

@@ -1,0 +1,57 @@
+// Kernel parameter blocks and launchers (kernels.cu) used by api.cu.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define ENKFMC_MAX_NENS 256
+
+struct RegressParams {
+    const double *U;           // [nfields * nstate2d][N] centred anomalies
+    int N, ld;                 // ensemble size, odd column pitch of the per-warp workspace
+    int pmax;                  // largest predecessor count in the plan
+    int nfields;
+    int64_t nloc, nnz, nstate2d, nwork;
+    const int64_t *row_ptr;    // [nloc + 1]
+    const int32_t *pred_state; // [nnz] state row of each predecessor
+    const int32_t *state_row;  // [nloc]
+    const int32_t *work_order; // [nloc] rows, most predecessors first
+    double rank_tol, variance_floor, fast_ratio;
+    double *T;                 // [nfields][nnz]  (-beta)
+    double *D;                 // [nfields][nloc] floored
+    int32_t *flags;            // [nfields][nloc] or null
+    unsigned int *counter;     // work-fetch counter (zeroed by the launcher)
+};
+
+struct SolveParams {
+    const double *X, *T, *D, *rdiag, *Ys;
+    double *Xa;
+    int N, nfields, ntiles;
+    int64_t nloc, nnz, nstate2d;
+    const int64_t *tile_ptr, *row_ptr, *csc_ptr, *csc_src;
+    const int32_t *col_idx, *csc_row, *phys, *iphys, *bw, *state_row, *obs_slot, *tile_nobs, *tile_order;
+    const uint8_t *is_interior;
+    double *scratch;           // per-CTA scratch
+    int64_t scratch_stride;    // doubles per CTA
+    int64_t off_z, off_win_a, off_win_r;  // offsets (doubles) inside a CTA's scratch
+    int bmax;                  // largest half-bandwidth
+    int a_in_smem, r_in_smem;  // window placement
+    int32_t *status;           // [nfields * ntiles]
+    unsigned int *counter;
+    int assemble_only;         // 1: write the band of T^T D^-1 T (no obs term) of tile_sel to band_out
+    int tile_sel;
+    double *band_out;          // [n][b+1] column-form lower band
+};
+
+size_t regress_warp_workspace_doubles(int N, int pmax);
+cudaError_t launch_center_rows(const double *X, double *U, int64_t nrows, int N, cudaStream_t s);
+cudaError_t launch_regress(const RegressParams &p, int sm_count, size_t smem_limit, cudaStream_t s);
+// Fills scratch layout fields of p given bmax/nmax; returns doubles per CTA.
+int64_t solve_plan_scratch(SolveParams &p, int64_t max_band_doubles, int64_t nmax, size_t smem_limit);
+int solve_grid_size(int sm_count, const SolveParams &p, size_t smem_limit);
+cudaError_t launch_local_solve(const SolveParams &p, int grid, size_t smem_limit, cudaStream_t s);
+cudaError_t launch_scatter_rows(double *dst, const int64_t *dst_rows, const double *src, const int64_t *src_rows,
+                                int64_t nrows, int N, cudaStream_t s);
+// w = (v + L v) / D (phase 0), out = w + L^T w (phase 1); v, w, out: [n][ncols]
+cudaError_t launch_precision_apply(const int64_t *row_ptr, const int32_t *col_idx, const int64_t *csc_ptr,
+                                   const int32_t *csc_row, const int64_t *csc_src, const double *T, const double *D,
+                                   const double *V, double *Wtmp, double *Out, int64_t n, int64_t ncols, cudaStream_t s);

@@ -1,0 +1,53 @@
+// Internal plan layout shared by plan.cpp (host index maps) and api.cu (device side).
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "enkf_mc.h"
+
+struct DeviceState;  // defined in api.cu
+
+struct enkfmc_plan {
+    // geometry.py:22-66 descriptor (+ nfields extension)
+    int64_t nx = 0, ny = 0, nfields = 1, delta = 1, zeta = 0, pr = 1, pc = 1;
+    int row_major = 1, periodic = 0;
+    int kind = 0;  // 0 decompose, 1 explicit local_order, 2 explicit CSR pattern
+    int64_t ntiles = 0, n2d = 0, nstate2d = 0;  // nstate2d: rows of one field's state block
+
+    // tile-major maps, exactly the reference's arrays (int64)
+    std::vector<int64_t> tile_ptr, local_order, interior_ptr, interior, interior_pos, halo_ptr, halo;
+    std::vector<int64_t> row_ptr;       // sum n_local + 1
+    std::vector<int32_t> col_idx;       // nnz, local positions, ascending per row
+
+    // derived maps consumed by the kernels
+    std::vector<int32_t> state_row;     // per local row: row inside one field's state block
+    std::vector<int32_t> pred_state;    // per nnz: state_row of that predecessor
+    std::vector<int32_t> row_tile;      // per local row
+    std::vector<int32_t> phys, iphys;   // physical (band) order inside the tile and its inverse
+    std::vector<int32_t> bw;            // per tile: half-bandwidth of A in physical order
+    std::vector<uint8_t> is_interior;   // per local row
+    std::vector<int64_t> csc_ptr;       // per local row + 1: column lists of T (global offsets)
+    std::vector<int32_t> csc_row;       // local row j holding the entry
+    std::vector<int64_t> csc_src;       // offset of the entry in the CSR value array
+    std::vector<int32_t> work_order;    // local rows sorted by predecessor count, descending
+    std::vector<int32_t> tile_order;    // tiles sorted by solve cost, descending
+    int64_t max_nlocal = 0, max_pred = 0, max_bw = 0;
+
+    // observations (kernels.py:90-113), per (field, tile)
+    int64_t nobs = 0;
+    bool have_obs = false;
+    std::vector<int64_t> obs_indices, obs_ptr, obs_pos, obs_row;
+    std::vector<int32_t> obs_slot;      // nfields x sum n_local: parent obs row or -1
+    std::vector<int32_t> tile_nobs;     // nfields x ntiles
+
+    DeviceState *dev = nullptr;
+    int64_t counters[8] = {0, 0, 0, 0, -1, 0, 0, 0};
+
+    int64_t sum_nlocal() const { return tile_ptr.empty() ? 0 : tile_ptr.back(); }
+    int64_t nnz() const { return row_ptr.empty() ? 0 : row_ptr.back(); }
+};
+
+void enkfmc_set_error(const std::string &msg);
+void enkfmc_device_release(enkfmc_plan *plan);  // api.cu
+void enkfmc_device_invalidate_obs(enkfmc_plan *plan);

@@ -1,0 +1,142 @@
+"""Grid descriptor and integer index maps: same callables as the reference geometry module
+(geometry.py:22-222), computed by the C-ABI library's host routines (csrc/plan.cpp).
+
+``GridGeometry`` gains one optional trailing field, ``nfields`` (default 1 = the reference):
+``nfields`` independent 2-D fields stacked in one state vector, label = field*(nx*ny) + 2-D
+label.  Decomposition, halos and predecessor sets are per 2-D field.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .errors import ConfigurationError
+
+KINDS = ("ring1d", "grid2d")
+ORDERINGS = ("row_major", "column_major")
+BOUNDARIES = ("clipped", "periodic")
+
+
+@dataclass(frozen=True)
+class GridGeometry:
+    kind: str
+    nx: int
+    ny: int = 1
+    ordering: str = "row_major"
+    boundary: str = ""
+    nfields: int = 1
+
+    def __post_init__(self):
+        if self.kind not in KINDS:
+            raise ValueError(f"unknown geometry kind {self.kind!r}")
+        if self.ordering not in ORDERINGS:
+            raise ValueError(f"unknown ordering {self.ordering!r}")
+        if self.nx < 1 or self.ny < 1:
+            raise ValueError(f"grid extents must be positive, got nx={self.nx} ny={self.ny}")
+        if self.kind == "ring1d" and self.ny != 1:
+            raise ValueError(f"ring1d requires ny=1, got ny={self.ny}")
+        if self.nfields < 1:
+            raise ValueError(f"nfields must be positive, got {self.nfields}")
+        if not self.boundary:
+            object.__setattr__(self, "boundary", "periodic" if self.kind == "ring1d" else "clipped")
+        if self.boundary not in BOUNDARIES:
+            raise ValueError(f"unknown boundary {self.boundary!r}")
+
+    @property
+    def n2d(self) -> int:
+        return self.nx * self.ny
+
+    @property
+    def nstate(self) -> int:
+        return self.nx * self.ny * self.nfields
+
+    @property
+    def periodic(self) -> bool:
+        return self.boundary == "periodic"
+
+    @property
+    def row_major(self) -> bool:
+        return self.ordering == "row_major"
+
+
+@dataclass(frozen=True)
+class LocalBox:
+    center: int
+    zeta: int
+    members: np.ndarray
+
+
+@dataclass(frozen=True)
+class Subdomain:
+    id: int
+    interior: np.ndarray
+    halo: np.ndarray
+    local_order: np.ndarray = field(default=None)
+
+    def __post_init__(self):
+        if self.local_order is None:
+            object.__setattr__(self, "local_order", np.union1d(self.interior, self.halo))
+
+    @property
+    def n_local(self) -> int:
+        return self.local_order.size
+
+    def interior_positions(self) -> np.ndarray:
+        return np.searchsorted(self.local_order, self.interior)
+
+
+def linear_index(geometry: GridGeometry, row: int, col: int) -> int:
+    if not (0 <= row < geometry.ny and 0 <= col < geometry.nx):
+        raise ValueError(f"cell ({row}, {col}) outside {geometry.ny}x{geometry.nx} grid")
+    return row * geometry.nx + col if geometry.row_major else col * geometry.ny + row
+
+
+def grid_coords(geometry: GridGeometry, index: int) -> tuple[int, int]:
+    if not (0 <= index < geometry.n2d):
+        raise ValueError(f"index {index} outside [0, {geometry.n2d})")
+    if geometry.row_major:
+        return divmod(index, geometry.nx)
+    col, row = divmod(index, geometry.ny)
+    return row, col
+
+
+def _box_call(fn, geometry: GridGeometry, center: int, zeta: int) -> np.ndarray:
+    if zeta < 0:
+        raise ValueError(f"zeta must be nonnegative, got {zeta}")
+    if not (0 <= center < geometry.n2d):
+        raise ValueError(f"index {center} outside [0, {geometry.n2d})")
+    span = min(2 * zeta + 1, max(geometry.nx, geometry.ny))
+    out = np.empty(span * span, dtype=np.int64)
+    count = C.c_int64(0)
+    _lib.check(fn(geometry.nx, geometry.ny, int(geometry.row_major), int(geometry.periodic), int(center), int(zeta),
+                  _lib.ptr(out), C.addressof(count)))
+    return out[:count.value].astype(np.intp)
+
+
+def local_box(geometry: GridGeometry, center: int, zeta: int) -> LocalBox:
+    """Chebyshev box members, ascending (geometry.py:145-156)."""
+    return LocalBox(center=center, zeta=zeta, members=_box_call(_lib.lib().enkfmc_local_box, geometry, center, zeta))
+
+
+def predecessors(geometry: GridGeometry, center: int, zeta: int) -> np.ndarray:
+    """Box members with label below the centre's (geometry.py:159-162)."""
+    return _box_call(_lib.lib().enkfmc_predecessors, geometry, center, zeta)
+
+
+def decompose(geometry: GridGeometry, delta: int, zeta: int) -> list[Subdomain]:
+    """Tiles with zeta-ring halos (geometry.py:165-222), from the plan's host maps."""
+    from .plan import get_plan
+
+    if delta < 1:
+        raise ConfigurationError(f"delta must be >= 1, got {delta}")
+    if zeta < 0:
+        raise ValueError(f"zeta must be nonnegative, got {zeta}")
+    return get_plan(geometry, delta, zeta).subdomains()
+
+
+def nominal_local_size(nstate: int, delta: int, zeta: int) -> int:
+    return nstate // delta + (2 * zeta + 1) ** 2

@@ -1,0 +1,116 @@
+"""Python handle on an ``enkfmc_plan`` (index maps on host and device), cached per
+(geometry, delta, zeta): SURVEY 7.3-4 -- the maps are cycle-invariant, only Xb/Ys change."""
+
+from __future__ import annotations
+
+import ctypes as C
+from functools import lru_cache
+
+import numpy as np
+
+from . import _lib
+
+(TILE_PTR, LOCAL_ORDER, INTERIOR_PTR, INTERIOR, INTERIOR_POS, HALO_PTR, HALO, ROW_PTR, COL_IDX, OBS_PTR, OBS_POS,
+ OBS_ROW, BANDWIDTH, PHYS) = range(14)
+_SIZE_OF = {TILE_PTR: (0, 1), LOCAL_ORDER: (1, 0), INTERIOR_PTR: (0, 1), INTERIOR: (3, 0), INTERIOR_POS: (3, 0),
+            HALO_PTR: (0, 1), HALO: (4, 0), ROW_PTR: (1, 1), COL_IDX: (2, 0), OBS_POS: (6, 0), OBS_ROW: (6, 0),
+            BANDWIDTH: (0, 0), PHYS: (1, 0)}
+
+
+class Plan:
+    """Owns one enkfmc_plan*.  Not thread-safe (one analysis at a time per plan)."""
+
+    def __init__(self, handle: int):
+        self._h = C.c_void_p(handle)
+        self._obs_key = None
+        self._sub = None
+
+    # -- constructors ------------------------------------------------------------------
+    @classmethod
+    def decomposed(cls, geometry, delta: int, zeta: int) -> "Plan":
+        h = C.c_void_p()
+        _lib.check(_lib.lib().enkfmc_plan_create(geometry.nx, geometry.ny, int(geometry.row_major),
+                                                 int(geometry.periodic), int(geometry.nfields), int(delta), int(zeta),
+                                                 C.byref(h)))
+        return cls(h.value)
+
+    @classmethod
+    def local(cls, geometry, zeta: int, local_order: np.ndarray) -> "Plan":
+        lo = _lib.as_i64(local_order)
+        h = C.c_void_p()
+        _lib.check(_lib.lib().enkfmc_plan_create_local(geometry.nx, geometry.ny, int(geometry.row_major),
+                                                       int(geometry.periodic), int(zeta), lo.size, _lib.ptr(lo),
+                                                       C.byref(h)))
+        return cls(h.value)
+
+    @classmethod
+    def from_csr(cls, indptr: np.ndarray, indices: np.ndarray) -> "Plan":
+        ip, ii = _lib.as_i64(indptr), _lib.as_i64(indices)
+        h = C.c_void_p()
+        _lib.check(_lib.lib().enkfmc_plan_create_csr(ip.size - 1, _lib.ptr(ip), _lib.ptr(ii), C.byref(h)))
+        return cls(h.value)
+
+    def __del__(self):
+        try:
+            if self._h:
+                _lib.lib().enkfmc_plan_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+    # -- queries -----------------------------------------------------------------------
+    @property
+    def handle(self):
+        return self._h
+
+    def size(self, what: int) -> int:
+        return int(_lib.lib().enkfmc_plan_size(self._h, what))
+
+    ntiles = property(lambda self: self.size(0))
+    sum_nlocal = property(lambda self: self.size(1))
+    nnz = property(lambda self: self.size(2))
+    nobs = property(lambda self: self.size(5))
+    max_nlocal = property(lambda self: self.size(9))
+    max_pred = property(lambda self: self.size(10))
+    max_bw = property(lambda self: self.size(11))
+    nfields = property(lambda self: self.size(12))
+
+    def get(self, what: int) -> np.ndarray:
+        if what == OBS_PTR:
+            n = self.nfields * self.ntiles + 1
+        else:
+            sz, extra = _SIZE_OF[what]
+            n = self.size(sz) + extra
+        out = np.empty(n, dtype=np.int64)
+        _lib.check(_lib.lib().enkfmc_plan_get(self._h, what, _lib.ptr(out), n))
+        return out
+
+    def counter(self, what: int) -> int:
+        return int(_lib.lib().enkfmc_plan_counter(self._h, what))
+
+    def set_observations(self, obs_indices: np.ndarray) -> None:
+        obs = _lib.as_i64(obs_indices)
+        key = (obs.size, hash(obs.tobytes()))
+        if key == self._obs_key:
+            return
+        _lib.check(_lib.lib().enkfmc_plan_set_observations(self._h, obs.size, _lib.ptr(obs)))
+        self._obs_key = key
+
+    def subdomains(self):
+        """list[Subdomain] exactly as decompose returns them (geometry.py:204-221)."""
+        from .geometry import Subdomain
+
+        if self._sub is None:
+            tp, lo = self.get(TILE_PTR), self.get(LOCAL_ORDER).astype(np.intp)
+            ip, it = self.get(INTERIOR_PTR), self.get(INTERIOR).astype(np.intp)
+            hp, ha = self.get(HALO_PTR), self.get(HALO).astype(np.intp)
+            self._sub = [
+                Subdomain(id=t, interior=it[ip[t]:ip[t + 1]], halo=ha[hp[t]:hp[t + 1]], local_order=lo[tp[t]:tp[t + 1]])
+                for t in range(self.ntiles)
+            ]
+        return list(self._sub)
+
+
+@lru_cache(maxsize=16)
+def get_plan(geometry, delta: int, zeta: int) -> Plan:
+    return Plan.decomposed(geometry, delta, zeta)
