@@ -129,6 +129,9 @@ int64_t enkfmc_plan_counter(const enkfmc_plan *plan, int what);
  * what = 0 U, 1 T, 2 D, 3 flags, 4 status.  NULL if not allocated. */
 void *enkfmc_plan_device_buffer(const enkfmc_plan *plan, int what);
 
+/* Synchronise and copy `bytes` of that workspace buffer to host memory (parity tests). */
+int enkfmc_plan_read_buffer(const enkfmc_plan *plan, int what, void *host_out, int64_t bytes);
+
 /* ---- small device helpers behind the remaining reference callables ------------------ */
 
 /* dst[dst_rows[k]][:] = src[src_rows[k]][:]  -- merge_interiors, driver.py:116. */

@@ -23,7 +23,7 @@ SYMBOLS = (
     "enkfmc_plan_set_observations", "enkfmc_plan_size", "enkfmc_plan_get", "enkfmc_center_rows",
     "enkfmc_regress", "enkfmc_local_solve", "enkfmc_analysis_device", "enkfmc_analysis_host",
     "enkfmc_plan_counter", "enkfmc_plan_device_buffer", "enkfmc_scatter_rows", "enkfmc_assemble_band",
-    "enkfmc_precision_apply",
+    "enkfmc_precision_apply", "enkfmc_plan_read_buffer",
 )
 
 _lib = None
@@ -66,6 +66,7 @@ def lib():
     L.enkfmc_scatter_rows.argtypes = [vp, vp, vp, vp, i64, i64, vp]
     L.enkfmc_assemble_band.argtypes = [vp, vp, vp, i64, vp, vp]
     L.enkfmc_precision_apply.argtypes = [vp, vp, vp, vp, i64, vp, vp, vp]
+    L.enkfmc_plan_read_buffer.argtypes = [vp, C.c_int, vp, i64]
     _lib = L
     return L
 

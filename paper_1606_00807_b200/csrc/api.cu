@@ -383,3 +383,11 @@ extern "C" int enkfmc_precision_apply(enkfmc_plan *p, const double *d_T, const d
     p->counters[0] += 2;
     return ENKFMC_OK;
 }
+
+extern "C" int enkfmc_plan_read_buffer(const enkfmc_plan *p, int what, void *host_out, int64_t bytes) {
+    void *src = enkfmc_plan_device_buffer(p, what);
+    if (!src) { enkfmc_set_error("workspace buffer not allocated"); return ENKFMC_E_VALUE; }
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(host_out, src, (size_t)bytes, cudaMemcpyDeviceToHost));
+    return ENKFMC_OK;
+}

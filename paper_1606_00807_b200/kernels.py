@@ -1,0 +1,142 @@
+"""Boundary containers and the local analysis: same callables as the reference kernels module
+(kernels.py:28-218) for the EnKF-MC primal path."""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import device
+from .errors import NumericalError
+from .factors import PrecisionFactors
+from .validation import as_float_array, as_index_array, ensure_finite
+
+TAG_OBS_PERTURB = 2  # rng.py:15
+
+
+@dataclass(frozen=True)
+class EnsembleState:
+    X: np.ndarray
+    role: str = "background"
+
+    def __post_init__(self):
+        x = as_float_array(self.X, "X", ndim=2)
+        ensure_finite(x, "X")
+        if self.role not in ("background", "analysis"):
+            raise ValueError(f"unknown role {self.role!r}")
+        object.__setattr__(self, "X", x)
+
+    @property
+    def nstate(self) -> int:
+        return self.X.shape[0]
+
+    @property
+    def nens(self) -> int:
+        return self.X.shape[1]
+
+    def mean(self) -> np.ndarray:
+        return self.X.mean(axis=1)
+
+    def perturbations(self) -> np.ndarray:
+        return self.X - self.X.mean(axis=1, keepdims=True)
+
+
+@dataclass(frozen=True)
+class ObservationNetwork:
+    obs_indices: np.ndarray
+    r_diag: np.ndarray
+    y: np.ndarray
+
+    def __post_init__(self):
+        idx = as_index_array(self.obs_indices, "obs_indices")
+        r = as_float_array(self.r_diag, "r_diag", ndim=1)
+        y = as_float_array(self.y, "y", ndim=1)
+        ensure_finite(r, "r_diag")
+        ensure_finite(y, "y")
+        if not (idx.size == r.size == y.size):
+            raise ValueError(f"inconsistent lengths: {idx.size} indices, {r.size} variances, {y.size} values")
+        if np.any(r <= 0):
+            raise ValueError("r_diag must be strictly positive")
+        object.__setattr__(self, "obs_indices", idx)
+        object.__setattr__(self, "r_diag", r)
+        object.__setattr__(self, "y", y)
+
+    @property
+    def nobs(self) -> int:
+        return self.obs_indices.size
+
+    def project(self, v: np.ndarray) -> np.ndarray:
+        return v[self.obs_indices]
+
+
+def restrict_network(net: ObservationNetwork, members: np.ndarray):
+    """Observations inside `members`, re-indexed to positions, plus surviving parent rows
+    (kernels.py:90-113).  Integer host logic."""
+    members = as_index_array(members, "members")
+    if members.size == 0:
+        rows = np.zeros(0, dtype=np.intp)
+        return ObservationNetwork(rows, np.zeros(0), np.zeros(0)), rows
+    idx = np.searchsorted(members, net.obs_indices)
+    inside = (idx < members.size) & (members[np.minimum(idx, members.size - 1)] == net.obs_indices)
+    rows = np.flatnonzero(inside)
+    return ObservationNetwork(idx[inside], net.r_diag[inside], net.y[inside]), rows
+
+
+@dataclass(frozen=True)
+class PerturbedObservations:
+    Ys: np.ndarray
+    seed: int
+    cycle: int
+
+    def __post_init__(self):
+        ys = as_float_array(self.Ys, "Ys", ndim=2)
+        ensure_finite(ys, "Ys")
+        object.__setattr__(self, "Ys", ys)
+
+
+def perturb_observations(net: ObservationNetwork, nens: int, seed: int, cycle: int = 0) -> PerturbedObservations:
+    """Host-side draw from the reference stream (seed, cycle, tag=2), obs-major
+    (kernels.py:130-144, rng.py:22-32); north_star keeps this on the host."""
+    if nens < 1:
+        raise ValueError(f"nens must be positive, got {nens}")
+    if cycle < 0:
+        raise ValueError(f"cycle must be nonnegative, got {cycle}")
+    g = np.random.default_rng([int(seed) & ((1 << 64) - 1), int(cycle), TAG_OBS_PERTURB])
+    noise = g.standard_normal((net.nobs, nens))
+    ys = net.y[:, None] + np.sqrt(net.r_diag)[:, None] * noise
+    return PerturbedObservations(Ys=ys, seed=int(seed), cycle=int(cycle))
+
+
+def _check_analysis_inputs(Xb, factors, net, Ys) -> np.ndarray:
+    if factors.n != Xb.nstate:
+        raise ValueError(f"factors dimension {factors.n} does not match state dimension {Xb.nstate}")
+    if net.nobs and net.obs_indices[-1] >= Xb.nstate:
+        raise ValueError("observation indices exceed the state dimension")
+    Ys = as_float_array(Ys, "Ys", ndim=2)
+    if Ys.shape != (net.nobs, Xb.nens):
+        raise ValueError(f"Ys has shape {Ys.shape}, expected {(net.nobs, Xb.nens)}")
+    return Ys
+
+
+def analysis_primal(Xb: EnsembleState, factors: PrecisionFactors, net: ObservationNetwork, Ys: np.ndarray, *,
+                    dense_cap: int = 4096, cg_rtol: float = 1e-9) -> EnsembleState:
+    """Xa = Xb + [B^-1 + H^T R^-1 H]^-1 H^T R^-1 (Ys - H Xb) (kernels.py:163-218) on the GPU.
+
+    The K3 kernel always solves directly (banded Cholesky in the pattern's own order), so
+    ``dense_cap``/``cg_rtol`` are accepted for signature compatibility only.
+    """
+    Ys = _check_analysis_inputs(Xb, factors, net, Ys)
+    if net.nobs == 0:
+        return EnsembleState(Xb.X.copy(), role="analysis")
+    plan = factors.plan()
+    plan.set_observations(net.obs_indices)
+    dX = device.to_device(Xb.X)
+    dT, dD = factors._device_factors()
+    dXa, dS = device.local_solve_device(plan, dX, dT, dD, device.to_device(net.r_diag),
+                                        device.to_device(np.ascontiguousarray(Ys)))
+    status = int(dS.cpu()[0])
+    if status != 0:
+        why = "matrix not positive definite" if status == 1 else "non-finite pivot"
+        raise NumericalError(f"primal analysis solve failed: {why}")
+    return EnsembleState(dXa.cpu().numpy(), role="analysis")
