@@ -132,6 +132,29 @@ void *enkfmc_plan_device_buffer(const enkfmc_plan *plan, int what);
 /* Synchronise and copy `bytes` of that workspace buffer to host memory (parity tests). */
 int enkfmc_plan_read_buffer(const enkfmc_plan *plan, int what, void *host_out, int64_t bytes);
 
+/* ---- sharding and measurement ------------------------------------------------------- */
+
+/* Restrict the plan's work to tiles [tile_begin, tile_end) (one rank's share; tiles are
+ * independent units, driver.py:196-204).  Maps and state arrays stay global-sized; only rows
+ * of owned tiles are regressed and only owned interiors are written to d_Xa. */
+int enkfmc_plan_set_tile_range(enkfmc_plan *plan, int64_t tile_begin, int64_t tile_end);
+
+/* Per-stage CUDA-event timing of enkfmc_analysis_device on its launching stream.
+ * enable != 0 starts recording (and clears the log); stage_times synchronises and returns the
+ * number of recorded calls and the SUMMED milliseconds of K0 centre, K2 regress, K3 solve. */
+int enkfmc_plan_profile(enkfmc_plan *plan, int enable);
+int enkfmc_plan_stage_times(enkfmc_plan *plan, int64_t *ncalls, double *ms3);
+
+/* Algorithmic work of one analysis with the current tile range (SURVEY 8d definitions):
+ * flops2[0] = sum over owned local rows of 2*N*p^2 - (2/3)*p^3 + 4*N*p (Householder-QR least squares),
+ * flops2[1] = sum over owned tiles with observations of n*b^2 + 4*n*b*N (banded Cholesky + two sweeps),
+ * each times the number of fields. */
+int enkfmc_plan_work(const enkfmc_plan *plan, int64_t nens, double *flops2);
+
+/* FP64 DFMA peak of the current device, measured with a register-resident FMA-chain kernel
+ * (MEASURED_PEAKS.json has no FP64 figure).  Returns TFLOP/s in *tflops. */
+int enkfmc_fp64_peak(double *tflops, void *stream);
+
 /* ---- small device helpers behind the remaining reference callables ------------------ */
 
 /* dst[dst_rows[k]][:] = src[src_rows[k]][:]  -- merge_interiors, driver.py:116. */

@@ -23,7 +23,8 @@ SYMBOLS = (
     "enkfmc_plan_set_observations", "enkfmc_plan_size", "enkfmc_plan_get", "enkfmc_center_rows",
     "enkfmc_regress", "enkfmc_local_solve", "enkfmc_analysis_device", "enkfmc_analysis_host",
     "enkfmc_plan_counter", "enkfmc_plan_device_buffer", "enkfmc_scatter_rows", "enkfmc_assemble_band",
-    "enkfmc_precision_apply", "enkfmc_plan_read_buffer",
+    "enkfmc_precision_apply", "enkfmc_plan_read_buffer", "enkfmc_plan_set_tile_range", "enkfmc_plan_profile",
+    "enkfmc_plan_stage_times", "enkfmc_plan_work", "enkfmc_fp64_peak",
 )
 
 _lib = None
@@ -67,6 +68,11 @@ def lib():
     L.enkfmc_assemble_band.argtypes = [vp, vp, vp, i64, vp, vp]
     L.enkfmc_precision_apply.argtypes = [vp, vp, vp, vp, i64, vp, vp, vp]
     L.enkfmc_plan_read_buffer.argtypes = [vp, C.c_int, vp, i64]
+    L.enkfmc_plan_set_tile_range.argtypes = [vp, i64, i64]
+    L.enkfmc_plan_profile.argtypes = [vp, C.c_int]
+    L.enkfmc_plan_stage_times.argtypes = [vp, vp, vp]
+    L.enkfmc_plan_work.argtypes = [vp, i64, vp]
+    L.enkfmc_fp64_peak.argtypes = [vp, vp]
     _lib = L
     return L
 

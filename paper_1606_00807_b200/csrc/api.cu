@@ -28,7 +28,9 @@ struct DeviceState {
             *state_row = nullptr, *pred_state = nullptr, *work_order = nullptr, *tile_order = nullptr;
     uint8_t *is_interior = nullptr;
     int32_t *obs_slot = nullptr, *tile_nobs = nullptr;
-    bool obs_current = false;
+    bool obs_current = false, orders_current = false;
+    std::vector<cudaEvent_t> prof;   // 4 events per profiled analysis_device call
+    size_t prof_used = 0;
     // workspace
     int64_t ws_nens = 0;
     double *U = nullptr, *T = nullptr, *D = nullptr, *scratch = nullptr;
@@ -91,13 +93,21 @@ int ensure_device(enkfmc_plan *p) {
     if ((rc = upload(d->bw, p->bw))) return rc;
     if ((rc = upload(d->state_row, p->state_row))) return rc;
     if ((rc = upload(d->pred_state, p->pred_state))) return rc;
-    if ((rc = upload(d->work_order, p->work_order))) return rc;
-    if ((rc = upload(d->tile_order, p->tile_order))) return rc;
     if ((rc = upload(d->is_interior, p->is_interior))) return rc;
     CK(cudaMalloc(&d->counters, 4 * sizeof(unsigned int)));
     CK(cudaMemset(d->counters, 0, 4 * sizeof(unsigned int)));
     for (auto &ev : d->ev) CK(cudaEventCreate(&ev));
     CK(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
+    return ENKFMC_OK;
+}
+
+int ensure_orders(enkfmc_plan *p) {
+    DeviceState *d = p->dev;
+    if (d->orders_current) return ENKFMC_OK;
+    int rc;
+    if ((rc = upload(d->work_order, p->work_order))) return rc;
+    if ((rc = upload(d->tile_order, p->tile_order))) return rc;
+    d->orders_current = true;
     return ENKFMC_OK;
 }
 
@@ -139,6 +149,7 @@ int ensure_solve_layout(enkfmc_plan *p, int64_t nens) {
         band = std::max(band, (p->tile_ptr[t + 1] - p->tile_ptr[t]) * (int64_t)(p->bw[t] + 1));
     L.nfields = (int)p->nfields;
     L.ntiles = (int)p->ntiles;
+    L.ntiles_owned = (int)p->ntiles;
     const int64_t stride = solve_plan_scratch(L, band, std::max<int64_t>(p->max_nlocal, 1), d->smem_limit);
     d->solve_grid = solve_grid_size(d->sm_count, L, d->smem_limit);
     CK(cudaMalloc(&d->scratch, (size_t)stride * d->solve_grid * sizeof(double)));
@@ -162,10 +173,12 @@ int ensure_workspace(enkfmc_plan *p, int64_t nens) {
 int do_regress(enkfmc_plan *p, const double *d_U, int64_t nens, double rank_tol, double floor_, double *d_T,
                double *d_D, int32_t *d_flags, cudaStream_t s) {
     DeviceState *d = p->dev;
+    int rc0 = ensure_orders(p);
+    if (rc0) return rc0;
     RegressParams R{};
     R.U = d_U; R.N = (int)nens; R.ld = (int)nens | 1; R.pmax = (int)std::max<int64_t>(p->max_pred, 1);
     R.nfields = (int)p->nfields; R.nloc = p->sum_nlocal(); R.nnz = p->nnz(); R.nstate2d = p->nstate2d;
-    R.nwork = R.nloc * p->nfields;
+    R.nwork = (int64_t)p->work_order.size() * p->nfields;
     R.row_ptr = d->row_ptr; R.pred_state = d->pred_state; R.state_row = d->state_row; R.work_order = d->work_order;
     R.rank_tol = rank_tol; R.variance_floor = floor_; R.fast_ratio = 1e-6;
     R.T = d_T; R.D = d_D; R.flags = d_flags; R.counter = d->counters;
@@ -187,7 +200,9 @@ int do_solve(enkfmc_plan *p, const double *d_X, const double *d_T, const double 
     int rc = ensure_obs(p);
     if (rc) return rc;
     if ((rc = ensure_solve_layout(p, nens))) return rc;
+    if ((rc = ensure_orders(p))) return rc;
     SolveParams S = d->solve_layout;
+    S.ntiles_owned = (int)p->tile_order.size();
     S.X = d_X; S.T = d_T; S.D = d_D; S.rdiag = d_r; S.Ys = d_Ys; S.Xa = d_Xa;
     S.nloc = p->sum_nlocal(); S.nnz = p->nnz(); S.nstate2d = p->nstate2d;
     S.tile_ptr = d->tile_ptr; S.row_ptr = d->row_ptr; S.csc_ptr = d->csc_ptr; S.csc_src = d->csc_src;
@@ -207,6 +222,7 @@ int do_solve(enkfmc_plan *p, const double *d_X, const double *d_T, const double 
 }  // namespace
 
 void enkfmc_device_invalidate_obs(enkfmc_plan *p) { if (p->dev) p->dev->obs_current = false; }
+void enkfmc_device_invalidate_orders(enkfmc_plan *p) { if (p->dev) p->dev->orders_current = false; }
 
 void enkfmc_device_release(enkfmc_plan *p) {
     DeviceState *d = p->dev;
@@ -218,6 +234,7 @@ void enkfmc_device_release(enkfmc_plan *p) {
     release(d->flags); release(d->status); release(d->counters); release(d->dX); release(d->dXa); release(d->dR);
     release(d->dYs);
     for (auto &ev : d->ev) if (ev) cudaEventDestroy(ev);
+    for (auto &ev : d->prof) cudaEventDestroy(ev);
     if (d->stream) cudaStreamDestroy(d->stream);
     delete d;
     p->dev = nullptr;
@@ -255,10 +272,78 @@ extern "C" int enkfmc_analysis_device(enkfmc_plan *p, const double *d_X, const d
     if ((rc = ensure_workspace(p, nens))) return rc;
     DeviceState *d = p->dev;
     cudaStream_t s = (cudaStream_t)stream;
+    cudaEvent_t *ev = nullptr;
+    if (p->profile) {
+        while (d->prof.size() < d->prof_used + 4) {
+            cudaEvent_t e;
+            CK(cudaEventCreate(&e));
+            d->prof.push_back(e);
+        }
+        ev = d->prof.data() + d->prof_used;
+        d->prof_used += 4;
+        CK(cudaEventRecord(ev[0], s));
+    }
     CK(launch_center_rows(d_X, d->U, p->nstate2d * p->nfields, (int)nens, s));
     p->counters[0] += 1;
+    if (ev) CK(cudaEventRecord(ev[1], s));
     if ((rc = do_regress(p, d->U, nens, rank_tol, floor_, d->T, d->D, d->flags, s))) return rc;
-    return do_solve(p, d_X, d->T, d->D, d_r, d_Ys, nens, d_Xa, d->status, s);
+    if (ev) CK(cudaEventRecord(ev[2], s));
+    rc = do_solve(p, d_X, d->T, d->D, d_r, d_Ys, nens, d_Xa, d->status, s);
+    if (ev) CK(cudaEventRecord(ev[3], s));
+    return rc;
+}
+
+extern "C" int enkfmc_plan_profile(enkfmc_plan *p, int enable) {
+    p->profile = enable != 0;
+    if (p->dev) p->dev->prof_used = 0;
+    return ENKFMC_OK;
+}
+
+extern "C" int enkfmc_plan_stage_times(enkfmc_plan *p, int64_t *ncalls, double *ms3) {
+    ms3[0] = ms3[1] = ms3[2] = 0.0;
+    *ncalls = 0;
+    if (!p->dev) return ENKFMC_OK;
+    DeviceState *d = p->dev;
+    CK(cudaDeviceSynchronize());
+    for (size_t k = 0; k + 4 <= d->prof_used; k += 4) {
+        for (int st = 0; st < 3; ++st) {
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, d->prof[k + st], d->prof[k + st + 1]));
+            ms3[st] += ms;
+        }
+        ++*ncalls;
+    }
+    return ENKFMC_OK;
+}
+
+extern "C" int enkfmc_fp64_peak(double *tflops, void *stream) {
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, dev));
+    cudaStream_t s = (cudaStream_t)stream;
+    double *out = nullptr;
+    CK(cudaMalloc(&out, sizeof(double)));
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    const int iters = 4096;
+    double best = 0.0;
+    for (int rep = 0; rep < 6; ++rep) {
+        CK(cudaEventRecord(a, s));
+        CK(launch_fp64_peak(out, iters, prop.multiProcessorCount, s));
+        CK(cudaEventRecord(b, s));
+        CK(cudaEventSynchronize(b));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, a, b));
+        const double flops = 2.0 * 64.0 * iters * 256.0 * prop.multiProcessorCount * 8.0;
+        if (rep > 0) best = std::max(best, flops / (ms * 1e-3) * 1e-12);
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(out);
+    *tflops = best;
+    return ENKFMC_OK;
 }
 
 extern "C" int enkfmc_analysis_host(enkfmc_plan *p, const double *X, const double *r_diag, const double *Ys,
@@ -363,7 +448,7 @@ extern "C" int enkfmc_assemble_band(enkfmc_plan *p, const double *d_T, const dou
     S.state_row = d->state_row; S.obs_slot = d->state_row /* unused */; S.tile_nobs = d->bw /* unused */;
     S.tile_order = d->tile_order; S.is_interior = d->is_interior; S.scratch = d->scratch;
     S.status = nullptr; S.counter = d->counters + 1;
-    S.assemble_only = 1; S.tile_sel = (int)tile; S.band_out = d_band;
+    S.assemble_only = 1; S.tile_sel = (int)tile; S.band_out = d_band; S.ntiles_owned = 1;
     CK(launch_local_solve(S, 1, d->smem_limit, (cudaStream_t)stream));
     p->counters[0] += 1;
     return ENKFMC_OK;

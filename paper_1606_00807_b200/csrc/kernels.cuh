@@ -20,12 +20,13 @@ struct RegressParams {
     double *D;                 // [nfields][nloc] floored
     int32_t *flags;            // [nfields][nloc] or null
     unsigned int *counter;     // work-fetch counter (zeroed by the launcher)
+    int maxdefl;               // deflation vectors the workspace holds (set by the launcher)
 };
 
 struct SolveParams {
     const double *X, *T, *D, *rdiag, *Ys;
     double *Xa;
-    int N, nfields, ntiles;
+    int N, nfields, ntiles, ntiles_owned;   // ntiles: global count (indexing); owned: work items
     int64_t nloc, nnz, nstate2d;
     const int64_t *tile_ptr, *row_ptr, *csc_ptr, *csc_src;
     const int32_t *col_idx, *csc_row, *phys, *iphys, *bw, *state_row, *obs_slot, *tile_nobs, *tile_order;
@@ -55,3 +56,4 @@ cudaError_t launch_scatter_rows(double *dst, const int64_t *dst_rows, const doub
 cudaError_t launch_precision_apply(const int64_t *row_ptr, const int32_t *col_idx, const int64_t *csc_ptr,
                                    const int32_t *csc_row, const int64_t *csc_src, const double *T, const double *D,
                                    const double *V, double *Wtmp, double *Out, int64_t n, int64_t ncols, cudaStream_t s);
+cudaError_t launch_fp64_peak(double *out, int iters, int sm_count, cudaStream_t s);

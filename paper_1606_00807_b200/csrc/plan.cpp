@@ -218,21 +218,9 @@ void finish_plan(enkfmc_plan &p) {
             ++slot;
         }
     }
-    // regression work order: most predecessors first (stable, so deterministic)
-    p.work_order.resize(total);
-    std::iota(p.work_order.begin(), p.work_order.end(), 0);
-    std::stable_sort(p.work_order.begin(), p.work_order.end(), [&](int32_t a, int32_t b) {
-        return (p.row_ptr[a + 1] - p.row_ptr[a]) > (p.row_ptr[b + 1] - p.row_ptr[b]);
-    });
-    p.tile_order.resize(p.ntiles);
-    std::iota(p.tile_order.begin(), p.tile_order.end(), 0);
-    std::stable_sort(p.tile_order.begin(), p.tile_order.end(), [&](int32_t a, int32_t b) {
-        auto cost = [&](int32_t t) {
-            double n = (double)(p.tile_ptr[t + 1] - p.tile_ptr[t]), w = (double)p.bw[t] + 1.0;
-            return n * w * w;
-        };
-        return cost(a) > cost(b);
-    });
+    p.tile_begin = 0;
+    p.tile_end = p.ntiles;
+    enkfmc_build_orders(p);
 }
 
 int validate_increasing(const int64_t *a, int64_t n, const char *name) {
@@ -247,6 +235,62 @@ int validate_increasing(const int64_t *a, int64_t n, const char *name) {
 }
 
 }  // namespace
+
+// Work orders over the owned tiles [tile_begin, tile_end): regressions with the most
+// predecessors first, tiles with the largest solve cost first (stable sorts: deterministic).
+void enkfmc_build_orders(enkfmc_plan &p) {
+    p.work_order.clear();
+    p.tile_order.clear();
+    for (int64_t t = p.tile_begin; t < p.tile_end; ++t) {
+        p.tile_order.push_back((int32_t)t);
+        for (int64_t q = p.tile_ptr[t]; q < p.tile_ptr[t + 1]; ++q) p.work_order.push_back((int32_t)q);
+    }
+    std::stable_sort(p.work_order.begin(), p.work_order.end(), [&](int32_t a, int32_t b) {
+        return (p.row_ptr[a + 1] - p.row_ptr[a]) > (p.row_ptr[b + 1] - p.row_ptr[b]);
+    });
+    std::stable_sort(p.tile_order.begin(), p.tile_order.end(), [&](int32_t a, int32_t b) {
+        auto cost = [&](int32_t t) {
+            double n = (double)(p.tile_ptr[t + 1] - p.tile_ptr[t]), w = (double)p.bw[t] + 1.0;
+            return n * w * w;
+        };
+        return cost(a) > cost(b);
+    });
+}
+
+extern "C" int enkfmc_plan_set_tile_range(enkfmc_plan *p, int64_t t0, int64_t t1) {
+    if (t0 < 0 || t1 > p->ntiles || t0 > t1) {
+        enkfmc_set_error("tile range [" + std::to_string(t0) + ", " + std::to_string(t1) + ") outside [0, " +
+                         std::to_string(p->ntiles) + "]");
+        return ENKFMC_E_VALUE;
+    }
+    p->tile_begin = t0;
+    p->tile_end = t1;
+    enkfmc_build_orders(*p);
+    enkfmc_device_invalidate_orders(p);
+    return ENKFMC_OK;
+}
+
+extern "C" int enkfmc_plan_work(const enkfmc_plan *p, int64_t nens, double *flops2) {
+    const double N = (double)nens;
+    double reg = 0.0, sol = 0.0;
+    for (int64_t t = p->tile_begin; t < p->tile_end; ++t) {
+        for (int64_t q = p->tile_ptr[t]; q < p->tile_ptr[t + 1]; ++q) {
+            const double k = (double)(p->row_ptr[q + 1] - p->row_ptr[q]);
+            reg += 2.0 * N * k * k - (2.0 / 3.0) * k * k * k + 4.0 * N * k;
+        }
+    }
+    reg *= (double)p->nfields;
+    for (int64_t f = 0; f < p->nfields; ++f) {
+        for (int64_t t = p->tile_begin; t < p->tile_end; ++t) {
+            if (p->have_obs && p->tile_nobs[(size_t)(f * p->ntiles + t)] == 0) continue;
+            const double n = (double)(p->tile_ptr[t + 1] - p->tile_ptr[t]), b = (double)p->bw[t];
+            sol += n * b * b + 4.0 * n * b * N;
+        }
+    }
+    flops2[0] = reg;
+    flops2[1] = sol;
+    return ENKFMC_OK;
+}
 
 extern "C" int enkfmc_tiling(int64_t nx, int64_t ny, int64_t delta, int64_t *pr, int64_t *pc) {
     int rc = check_geometry(nx, ny, 0);

@@ -41,6 +41,9 @@ struct enkfmc_plan {
     std::vector<int32_t> obs_slot;      // nfields x sum n_local: parent obs row or -1
     std::vector<int32_t> tile_nobs;     // nfields x ntiles
 
+    int64_t tile_begin = 0, tile_end = 0;   // owned tiles (one rank's share)
+    bool profile = false;
+
     DeviceState *dev = nullptr;
     int64_t counters[8] = {0, 0, 0, 0, -1, 0, 0, 0};
 
@@ -51,3 +54,5 @@ struct enkfmc_plan {
 void enkfmc_set_error(const std::string &msg);
 void enkfmc_device_release(enkfmc_plan *plan);  // api.cu
 void enkfmc_device_invalidate_obs(enkfmc_plan *plan);
+void enkfmc_device_invalidate_orders(enkfmc_plan *plan);
+void enkfmc_build_orders(enkfmc_plan &p);  // plan.cpp

@@ -81,12 +81,35 @@ def analysis_device(plan, dX, dR, dYs, dXa, rank_tol: float = 1e-8, variance_flo
     return dXa
 
 
+_PINNED_POOL: list = []   # [tensor, weakref-to-the-array-handed-out]
+
+
+def pinned_empty(shape) -> np.ndarray:
+    """float64 host array in page-locked memory.  Buffers are recycled once the array handed out
+    earlier (and every view of it) has been garbage collected, so results stay caller-owned."""
+    import weakref
+
+    torch = _torch()
+    n = int(np.prod(shape))
+    for entry in _PINNED_POOL:
+        if entry[0].numel() == n and entry[1]() is None:
+            base = entry[0].numpy()          # every view handed out keeps `base` alive (numpy base collapsing)
+            entry[1] = weakref.ref(base)
+            return base.reshape(shape)
+    t = torch.empty(max(n, 1), dtype=torch.float64, pin_memory=True)[:n]
+    base = t.numpy()
+    if len(_PINNED_POOL) >= 4:
+        _PINNED_POOL.pop(0)
+    _PINNED_POOL.append([t, weakref.ref(base)])
+    return base.reshape(shape)
+
+
 def analysis_host(plan, X: np.ndarray, r_diag: np.ndarray, Ys: np.ndarray, Xa: np.ndarray | None = None,
                   rank_tol: float = 1e-8, variance_floor: float = 1e-10):
     """Host buffers in, host buffer out; H2D/D2H inside.  Returns (Xa, timings_ms[4])."""
     _torch()
     if Xa is None:
-        Xa = np.empty_like(X)
+        Xa = pinned_empty(X.shape)
     tm = np.zeros(4)
     _lib.check(_lib.lib().enkfmc_analysis_host(plan.handle, _lib.ptr(X), _lib.ptr(r_diag), _lib.ptr(Ys), X.shape[1],
                                                rank_tol, variance_floor, _lib.ptr(Xa), _lib.ptr(tm)))

@@ -96,6 +96,26 @@ class Plan:
         _lib.check(_lib.lib().enkfmc_plan_set_observations(self._h, obs.size, _lib.ptr(obs)))
         self._obs_key = key
 
+    def set_tile_range(self, begin: int, end: int) -> None:
+        """Own tiles [begin, end) only (one rank's share of the sub-domains)."""
+        _lib.check(_lib.lib().enkfmc_plan_set_tile_range(self._h, int(begin), int(end)))
+
+    def profile(self, enable: bool) -> None:
+        _lib.check(_lib.lib().enkfmc_plan_profile(self._h, int(enable)))
+
+    def stage_times(self):
+        """(ncalls, [ms centre, ms regress, ms solve] summed over the profiled calls)."""
+        n = C.c_int64(0)
+        ms = np.zeros(3)
+        _lib.check(_lib.lib().enkfmc_plan_stage_times(self._h, C.addressof(n), _lib.ptr(ms)))
+        return int(n.value), ms
+
+    def work(self, nens: int):
+        """Algorithmic flops (regress, solve) of one analysis over the owned tiles."""
+        fl = np.zeros(2)
+        _lib.check(_lib.lib().enkfmc_plan_work(self._h, int(nens), _lib.ptr(fl)))
+        return float(fl[0]), float(fl[1])
+
     def subdomains(self):
         """list[Subdomain] exactly as decompose returns them (geometry.py:204-221)."""
         from .geometry import Subdomain
