@@ -26,6 +26,10 @@ struct DeviceState {
     int64_t *tile_ptr = nullptr, *row_ptr = nullptr, *csc_ptr = nullptr, *csc_src = nullptr;
     int32_t *col_idx = nullptr, *csc_row = nullptr, *phys = nullptr, *iphys = nullptr, *bw = nullptr,
             *state_row = nullptr, *pred_state = nullptr, *work_order = nullptr, *tile_order = nullptr;
+    int64_t *rq_ptr = nullptr;
+    int64_t rq_stride = 0;
+    double *Rq = nullptr;
+    int64_t rq_fields = 0;          // fields the QR scratch holds
     uint8_t *is_interior = nullptr;
     int32_t *obs_slot = nullptr, *tile_nobs = nullptr;
     bool obs_current = false, orders_current = false;
@@ -94,6 +98,16 @@ int ensure_device(enkfmc_plan *p) {
     if ((rc = upload(d->state_row, p->state_row))) return rc;
     if ((rc = upload(d->pred_state, p->pred_state))) return rc;
     if ((rc = upload(d->is_interior, p->is_interior))) return rc;
+    {   // packed QR block of every local row: R by columns (min(j+1,K) entries), c[K], e2
+        std::vector<int64_t> rq(p->sum_nlocal() + 1, 0);
+        // K depends on the ensemble size; sized for K = p (the largest block), valid for any N
+        for (int64_t q = 0; q < p->sum_nlocal(); ++q) {
+            const int64_t k = p->row_ptr[q + 1] - p->row_ptr[q];
+            rq[q + 1] = rq[q] + k * (k + 1) / 2 + k + 1;
+        }
+        d->rq_stride = rq.back();
+        if ((rc = upload(d->rq_ptr, rq))) return rc;
+    }
     CK(cudaMalloc(&d->counters, 4 * sizeof(unsigned int)));
     CK(cudaMemset(d->counters, 0, 4 * sizeof(unsigned int)));
     for (auto &ev : d->ev) CK(cudaEventCreate(&ev));
@@ -182,15 +196,30 @@ int do_regress(enkfmc_plan *p, const double *d_U, int64_t nens, double rank_tol,
     R.row_ptr = d->row_ptr; R.pred_state = d->pred_state; R.state_row = d->state_row; R.work_order = d->work_order;
     R.rank_tol = rank_tol; R.variance_floor = floor_; R.fast_ratio = 1e-6;
     R.T = d_T; R.D = d_D; R.flags = d_flags; R.counter = d->counters;
-    if (R.nwork > 0xfffffff0LL) { enkfmc_set_error("too many regressions for one launch"); return ENKFMC_E_CAPACITY; }
-    cudaError_t e = launch_regress(R, d->sm_count, d->smem_limit, s);
-    if (e == cudaErrorInvalidConfiguration) {
-        enkfmc_set_error("regression workspace (nens=" + std::to_string(nens) + ", predecessors=" +
-                         std::to_string(p->max_pred) + ") exceeds shared memory");
-        return ENKFMC_E_CAPACITY;
+    R.rq_ptr = d->rq_ptr; R.rq_stride = d->rq_stride;
+    // QR scratch: as many fields per launch pair as fit in the budget (default 16 GiB)
+    const int64_t budget = (int64_t)16 << 30;
+    int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(p->nfields, budget / std::max<int64_t>(8 * d->rq_stride, 1)));
+    if (!d->Rq || d->rq_fields < chunk) {
+        release(d->Rq);
+        CK(cudaMalloc(&d->Rq, std::max<size_t>((size_t)chunk * d->rq_stride, 1) * sizeof(double)));
+        d->rq_fields = chunk;
     }
-    CK(e);
-    p->counters[0] += 1;
+    R.Rq = d->Rq;
+    for (int64_t f0 = 0; f0 < p->nfields; f0 += chunk) {
+        R.f0 = (int)f0;
+        R.f1 = (int)std::min<int64_t>(p->nfields, f0 + chunk);
+        R.nwork = (int64_t)p->work_order.size() * (R.f1 - R.f0);
+        if (R.nwork > 0xfffffff0LL) { enkfmc_set_error("too many regressions for one launch"); return ENKFMC_E_CAPACITY; }
+        cudaError_t e = launch_regress(R, d->sm_count, d->smem_limit, s);
+        if (e == cudaErrorInvalidConfiguration) {
+            enkfmc_set_error("regression workspace (nens=" + std::to_string(nens) + ", predecessors=" +
+                             std::to_string(p->max_pred) + ") exceeds shared memory or the 96-predecessor cap");
+            return ENKFMC_E_CAPACITY;
+        }
+        CK(e);
+        if (R.nwork > 0) p->counters[0] += 2;
+    }
     return ENKFMC_OK;
 }
 
@@ -208,7 +237,7 @@ int do_solve(enkfmc_plan *p, const double *d_X, const double *d_T, const double 
     S.tile_ptr = d->tile_ptr; S.row_ptr = d->row_ptr; S.csc_ptr = d->csc_ptr; S.csc_src = d->csc_src;
     S.col_idx = d->col_idx; S.csc_row = d->csc_row; S.phys = d->phys; S.iphys = d->iphys; S.bw = d->bw;
     S.state_row = d->state_row; S.obs_slot = d->obs_slot; S.tile_nobs = d->tile_nobs; S.tile_order = d->tile_order;
-    S.is_interior = d->is_interior; S.scratch = d->scratch; S.status = d_status; S.counter = d->counters + 1;
+    S.is_interior = d->is_interior; S.scratch = d->scratch; S.status = d_status; S.counter = d->counters + 2;
     cudaError_t e = launch_local_solve(S, d->solve_grid, d->smem_limit, s);
     if (e == cudaErrorInvalidConfiguration) {
         enkfmc_set_error("local-solve window (half-bandwidth " + std::to_string(p->max_bw) + ") exceeds shared memory");
@@ -231,7 +260,7 @@ void enkfmc_device_release(enkfmc_plan *p) {
     release(d->csc_row); release(d->phys); release(d->iphys); release(d->bw); release(d->state_row);
     release(d->pred_state); release(d->work_order); release(d->tile_order); release(d->is_interior);
     release(d->obs_slot); release(d->tile_nobs); release(d->U); release(d->T); release(d->D); release(d->scratch);
-    release(d->flags); release(d->status); release(d->counters); release(d->dX); release(d->dXa); release(d->dR);
+    release(d->flags); release(d->status); release(d->counters); release(d->rq_ptr); release(d->Rq); release(d->dX); release(d->dXa); release(d->dR);
     release(d->dYs);
     for (auto &ev : d->ev) if (ev) cudaEventDestroy(ev);
     for (auto &ev : d->prof) cudaEventDestroy(ev);
@@ -447,7 +476,7 @@ extern "C" int enkfmc_assemble_band(enkfmc_plan *p, const double *d_T, const dou
     S.col_idx = d->col_idx; S.csc_row = d->csc_row; S.phys = d->phys; S.iphys = d->iphys; S.bw = d->bw;
     S.state_row = d->state_row; S.obs_slot = d->state_row /* unused */; S.tile_nobs = d->bw /* unused */;
     S.tile_order = d->tile_order; S.is_interior = d->is_interior; S.scratch = d->scratch;
-    S.status = nullptr; S.counter = d->counters + 1;
+    S.status = nullptr; S.counter = d->counters + 2;
     S.assemble_only = 1; S.tile_sel = (int)tile; S.band_out = d_band; S.ntiles_owned = 1;
     CK(launch_local_solve(S, 1, d->smem_limit, (cudaStream_t)stream));
     p->counters[0] += 1;

@@ -96,37 +96,46 @@ cudaError_t launch_center_rows(const double *X, double *U, int64_t nrows, int N,
 }
 
 // ------------------------------------------------------------------------------------------
-// K2: one warp per regression (estimator.py:46-61,133-150 + factors.py:60).
+// K2: per-component regression (estimator.py:46-61,133-150 + factors.py:60), one warp per
+// regression, in two kernels so that each phase runs at its own occupancy.
 //
-// Workspace W (shared memory, column-major, odd pitch ld >= N): column j < p is predecessor
-// j's anomaly vector, column p is the target y.
-//   1. Householder QR of W[:, 0:p] (no pivoting; reflectors also applied to y, never stored):
-//      lanes own rows (S register slots), four columns share one transposing warp reduction.
-//   2. s_max(R) by power iteration; s_min(R) by inverse iteration (two triangular solves per
-//      step, vectors in registers).  The inverse-iteration estimate bounds s_min from above,
-//      so "estimate < rank_tol * s_max" proves the reference's truncation (estimator.py:55-57)
-//      is active; the converged pair (z, x = R z / s) is then deflated and the probe repeats in
-//      the orthogonal complement until the next singular value is kept.
-//   3. beta = (I - Z Z^T) R^-1 (I - X X^T) Q^T y: the minimum-norm solution over the retained
-//      singular triplets, i.e. exactly U S^+ V^T y of the reference's truncated SVD.
-//   4. Anything the probes cannot settle (zero pivots, p > N, no gap, a singular value within
-//      5 % above the threshold, more truncated values than the workspace holds) goes to the general
-//      fallback: one-sided Jacobi SVD on the rows of [R | Q^T y] with the same truncation rule.
-//   5. T = -beta; residual recomputed from the original rows (estimator.py:60),
-//      D = max(|resid|^2 / (N-1), floor)  (estimator.py:148, factors.py:60).
+// K2a regress_qr_kernel.  Workspace W (shared, column-major, odd pitch ld >= N): column j < p is
+//   predecessor j's anomaly vector, column p the target y.  Householder QR of W[:, 0:p] without
+//   pivoting (reflectors also applied to y, never stored): lanes own rows (S register slots),
+//   eight columns share two transposing warp reductions.  Output per regression, packed in
+//   global scratch: R by columns (min(j+1, K) entries of column j), c = (Q^T y)[0:K] and
+//   e2 = |(Q^T y)[K:N]|^2 -- the squared residual of the full least-squares fit.
+//
+// K2b regress_solve_kernel.  R (p x p) in shared memory, p-vectors in registers.
+//   s_max(R) is bracketed by a 3-step power iteration (lower bound) and |R|_F (upper bound);
+//   s_min(R) by inverse iteration (two triangular solves per step).  The inverse-iteration
+//   estimate bounds s_min from above, so "estimate < rank_tol * lower(s_max)" proves that the
+//   reference's truncation (estimator.py:55-57) is active; the converged pair (z, x = R z / s) is
+//   deflated and the probe repeats in the orthogonal complement until the next singular value is
+//   kept.  beta = (I - Z Z^T) R^-1 (I - X X^T) c is then exactly U S^+ V^T y of the reference's
+//   truncated SVD.  Anything the probes cannot settle (zero pivots, p > N, no gap, a singular
+//   value within 5 % of the threshold, more truncated values than the workspace holds) goes to
+//   the general fallback: one-sided Jacobi SVD on the rows of [R | c] with the same rule.
+//   T = -beta;  D = max((e2 + sum over truncated k of (x_k^T c)^2) / (N-1), floor): this is
+//   |y - A^T beta|^2 of estimator.py:60,148 evaluated in the QR basis (orthogonal invariance),
+//   so the predecessor rows are not read a second time.
 // ------------------------------------------------------------------------------------------
 #define REG_MAXDEFL_CAP 4
 #define JACOBI_MAX_SWEEPS 30
-#define POWER_ITERS 10
+#define POWER_ITERS 3
+#define POWER_ITERS_REFINE 24
 #define INVIT_MAX 40
 
-__host__ __device__ inline size_t regress_ws_doubles(int N, int pmax, int maxdefl) {
-    const int ld = N | 1;
-    // W | rdiag | rinv | aux | Z[maxdefl] | X[maxdefl]
-    size_t d = (size_t)ld * (pmax + 1) + (size_t)(3 + 2 * maxdefl) * pmax + 2;
+__host__ __device__ inline size_t regress_qr_ws_doubles(int N, int pmax) {
+    const size_t d = (size_t)(N | 1) * (pmax + 1) + (size_t)pmax + 2;   // W | rdiag
     return (d + 1) & ~(size_t)1;
 }
-size_t regress_warp_workspace_doubles(int N, int pmax) { return regress_ws_doubles(N, pmax, 1); }
+__host__ __device__ inline size_t regress_solve_ws_doubles(int pmax, int maxdefl) {
+    // R (pitch pmax|1, pmax+1 columns: the last is c) | rinv | aux | tmp | Z[maxdefl] | X[maxdefl]
+    const size_t d = (size_t)(pmax | 1) * (pmax + 1) + (size_t)(3 + 2 * maxdefl) * pmax + 2;
+    return (d + 1) & ~(size_t)1;
+}
+size_t regress_warp_workspace_doubles(int N, int pmax) { return regress_qr_ws_doubles(N, pmax); }
 
 namespace {
 
@@ -147,6 +156,109 @@ __device__ __forceinline__ void warp_sum4(double &d0, double &d1, double &d2, do
     d1 = __shfl_sync(FULL, t, 8);    // bit4 = 0, bit3 = 1
     d2 = __shfl_sync(FULL, t, 16);   // bit4 = 1, bit3 = 0
     d3 = __shfl_sync(FULL, t, 24);
+}
+
+// One Householder step on columns [jbeg, p] of W.  Rows below 32*S0 are final (all < k) and are
+// skipped; rows in [32*S0, k) carry v = 0, so re-storing them is exact.  NB columns per batch.
+template <int S, int S0, int NB>
+__device__ __forceinline__ void qr_apply(double *Wl, int ld, int jbeg, int jend, const double (&v)[S], double tau,
+                                         bool tail_ok, int lane) {
+    // Wl = W + lane ; tail_ok: row lane + 32 (S-1) exists (< N)
+    double *col = Wl + (size_t)jbeg * ld;
+    for (int j0 = jbeg; j0 + NB <= jend; j0 += NB, col += (size_t)NB * ld) {
+        double c[NB][S], d[NB];
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+            d[b] = 0.0;
+#pragma unroll
+            for (int s = S0; s < S; ++s) {
+                c[b][s] = (s < S - 1 || tail_ok) ? col[(size_t)b * ld + 32 * s] : 0.0;
+                d[b] += v[s] * c[b][s];
+            }
+        }
+#pragma unroll
+        for (int b = 0; b < NB; b += 4) warp_sum4(d[b], d[b + 1], d[b + 2], d[b + 3], lane);
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+            const double w = d[b] * tau;
+#pragma unroll
+            for (int s = S0; s < S; ++s)
+                if (s < S - 1 || tail_ok) col[(size_t)b * ld + 32 * s] = c[b][s] - w * v[s];
+        }
+    }
+}
+
+template <int S, int S0>
+__device__ __forceinline__ void qr_step(double *W, int ld, int N, int k, int p, double *rdiag, int lane) {
+    const bool tail_ok = lane + 32 * (S - 1) < N;
+    double *Wl = W + lane;
+    const double *ck = Wl + (size_t)k * ld;
+    double v[S];
+    double ss = 0.0;
+#pragma unroll
+    for (int s = 0; s < S; ++s) v[s] = 0.0;
+#pragma unroll
+    for (int s = S0; s < S; ++s) {
+        const int i = lane + 32 * s;
+        v[s] = (i >= k && (s < S - 1 || tail_ok)) ? ck[32 * s] : 0.0;
+        ss += v[s] * v[s];
+    }
+    ss = warp_sum(ss);
+    const double x0 = W[(size_t)k * ld + k];
+    const double nrm = sqrt(ss);
+    if (nrm == 0.0) {
+        if (lane == 0) rdiag[k] = 0.0;
+        return;
+    }
+    const double alpha = (x0 >= 0.0) ? -nrm : nrm;
+    const double tau = 1.0 / (nrm * (nrm + fabs(x0)));   // 2 / v^T v
+#pragma unroll
+    for (int s = S0; s < S; ++s) if (lane + 32 * s == k) v[s] = x0 - alpha;
+    if (lane == 0) rdiag[k] = alpha;
+    // columns k+1 .. p (p = the y column): batches of 8, then 4, then a clamped batch of 4
+    const int jend = p + 1;
+    int j = k + 1;
+    const int n8 = (jend - j) & ~7;
+    qr_apply<S, S0, 8>(Wl, ld, j, j + n8, v, tau, tail_ok, lane);
+    j += n8;
+    if (jend - j >= 4) { qr_apply<S, S0, 4>(Wl, ld, j, j + 4, v, tau, tail_ok, lane); j += 4; }
+    if (j < jend) {
+        double c[4][S], d[4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const double *col = Wl + (size_t)(j + b < jend ? j + b : jend - 1) * ld;
+            d[b] = 0.0;
+#pragma unroll
+            for (int s = S0; s < S; ++s) {
+                c[b][s] = (s < S - 1 || tail_ok) ? col[32 * s] : 0.0;
+                d[b] += v[s] * c[b][s];
+            }
+        }
+        warp_sum4(d[0], d[1], d[2], d[3], lane);
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            if (j + b >= jend) break;
+            double *col = Wl + (size_t)(j + b) * ld;
+            const double w = d[b] * tau;
+#pragma unroll
+            for (int s = S0; s < S; ++s)
+                if (s < S - 1 || tail_ok) col[32 * s] = c[b][s] - w * v[s];
+        }
+    }
+}
+
+template <int S>
+__device__ __forceinline__ void qr_step_dispatch(double *W, int ld, int N, int k, int p, double *rdiag, int lane) {
+    if constexpr (S <= 4) {
+        switch (k >> 5) {
+            case 0: qr_step<S, 0>(W, ld, N, k, p, rdiag, lane); break;
+            case 1: if constexpr (S > 1) qr_step<S, 1>(W, ld, N, k, p, rdiag, lane); break;
+            case 2: if constexpr (S > 2) qr_step<S, 2>(W, ld, N, k, p, rdiag, lane); break;
+            default: if constexpr (S > 3) qr_step<S, 3>(W, ld, N, k, p, rdiag, lane); break;
+        }
+    } else {
+        qr_step<S, 0>(W, ld, N, k, p, rdiag, lane);
+    }
 }
 
 // p-vectors live in registers: element e <-> lane e & 31, slot e >> 5 (PS slots).
@@ -182,16 +294,14 @@ template <int PS>
 __device__ __forceinline__ void solve_upper(Vec<PS> &b, const double *W, const double *rinv, int ld, int p, int lane) {
 #pragma unroll
     for (int sk = PS - 1; sk >= 0; --sk) {
-        for (int kk = 31; kk >= 0; --kk) {
+        const int ktop = (p - 32 * sk < 32 ? p - 32 * sk : 32) - 1;
+        const double *col = W + (size_t)(32 * sk + ktop) * ld + lane;
+        for (int kk = ktop; kk >= 0; --kk, col -= ld) {
             const int k = 32 * sk + kk;
-            if (k >= p) continue;
             const double xk = __shfl_sync(FULL, b.v[sk], kk) * rinv[k];
-            const double *col = W + (size_t)k * ld;
 #pragma unroll
-            for (int t = 0; t <= sk; ++t) {
-                const int i = lane + 32 * t;
-                if (i < k) b.v[t] -= col[i] * xk;
-            }
+            for (int t = 0; t <= sk; ++t)
+                if (lane + 32 * t < k) b.v[t] -= col[32 * t] * xk;
             if (lane == kk) b.v[sk] = xk;
         }
     }
@@ -202,15 +312,15 @@ template <int PS>
 __device__ __forceinline__ void solve_upper_t(Vec<PS> &z, const double *W, const double *rinv, int ld, int p, int lane) {
 #pragma unroll
     for (int sk = 0; sk < PS; ++sk) {
-        for (int kk = 0; kk < 32; ++kk) {
+        const int kend = p - 32 * sk < 32 ? p - 32 * sk : 32;
+        const double *row = W + 32 * sk + (size_t)lane * ld;   // R[k, lane + 32 t] = row[kk + 32 t ld]
+        for (int kk = 0; kk < kend; ++kk) {
             const int k = 32 * sk + kk;
-            if (k >= p) break;
             const double uk = __shfl_sync(FULL, z.v[sk], kk) * rinv[k];
-            const double *row = W + k;
 #pragma unroll
             for (int t = sk; t < PS; ++t) {
                 const int j = lane + 32 * t;
-                if (j > k && j < p) z.v[t] -= row[(size_t)j * ld] * uk;
+                if (j > k && j < p) z.v[t] -= row[kk + (size_t)32 * t * ld] * uk;
             }
             if (lane == kk) z.v[sk] = uk;
         }
@@ -225,16 +335,14 @@ __device__ __forceinline__ Vec<PS> mul_upper(const Vec<PS> &v, const double *W, 
     for (int t = 0; t < PS; ++t) y.v[t] = 0.0;
 #pragma unroll
     for (int sj = 0; sj < PS; ++sj) {
-        for (int jj = 0; jj < 32; ++jj) {
+        const int jend = p - 32 * sj < 32 ? p - 32 * sj : 32;
+        const double *col = W + (size_t)(32 * sj) * ld + lane;
+        for (int jj = 0; jj < jend; ++jj, col += ld) {
             const int j = 32 * sj + jj;
-            if (j >= p) break;
             const double vj = __shfl_sync(FULL, v.v[sj], jj);
-            const double *col = W + (size_t)j * ld;
 #pragma unroll
-            for (int t = 0; t <= sj; ++t) {
-                const int i = lane + 32 * t;
-                if (i <= j) y.v[t] += col[i] * vj;
-            }
+            for (int t = 0; t <= sj; ++t)
+                if (lane + 32 * t <= j) y.v[t] += col[32 * t] * vj;
         }
     }
     return y;
@@ -248,15 +356,15 @@ __device__ __forceinline__ Vec<PS> mul_upper_t(const Vec<PS> &y, const double *W
     for (int t = 0; t < PS; ++t) w.v[t] = 0.0;
 #pragma unroll
     for (int si = 0; si < PS; ++si) {
-        for (int ii = 0; ii < 32; ++ii) {
+        const int iend = p - 32 * si < 32 ? p - 32 * si : 32;
+        const double *row = W + 32 * si + (size_t)lane * ld;
+        for (int ii = 0; ii < iend; ++ii) {
             const int i = 32 * si + ii;
-            if (i >= p) break;
             const double yi = __shfl_sync(FULL, y.v[si], ii);
-            const double *row = W + i;
 #pragma unroll
             for (int t = si; t < PS; ++t) {
                 const int j = lane + 32 * t;
-                if (j >= i && j < p) w.v[t] += row[(size_t)j * ld] * yi;
+                if (j >= i && j < p) w.v[t] += row[ii + (size_t)32 * t * ld] * yi;
             }
         }
     }
@@ -264,9 +372,10 @@ __device__ __forceinline__ Vec<PS> mul_upper_t(const Vec<PS> &y, const double *W
 }
 
 // General fallback: one-sided Jacobi SVD on the rows of [R | c] (K x (p+1), explicit zeros below
-// the diagonal), truncation as estimator.py:55-57.  Writes beta to out[0..p); returns flag bits.
+// the diagonal), truncation as estimator.py:55-57.  Writes beta to out[0..p); returns flag bits and
+// the squared norm of the truncated part of c in *dropped2.
 __device__ int jacobi_solve(double *W, int ld, int K, int p, double rank_tol, double *s2buf, double *coef,
-                            double *out, int lane) {
+                            double *out, double *dropped2, int lane) {
     int flag = 0;
     const int M = (K + 1) & ~1;
     const int npairs = M >> 1;
@@ -323,12 +432,15 @@ __device__ int jacobi_solve(double *W, int ld, int K, int p, double rank_tol, do
     smax = sqrt(warp_max(smax));
     __syncwarp();
     bool dropped = false;
+    double d2 = 0.0;
     for (int k = lane; k < K; k += 32) {
         const double s = sqrt(s2buf[k]);
         const bool keep = (s >= rank_tol * smax) && (s > 0.0);
         coef[k] = keep ? cvec[k] / s2buf[k] : 0.0;
+        if (!keep) d2 += cvec[k] * cvec[k];
         dropped |= !keep;
     }
+    *dropped2 = warp_sum(d2);
     if (__any_sync(FULL, dropped)) flag |= 2;
     __syncwarp();
     for (int j = lane; j < p; j += 32) {
@@ -341,35 +453,46 @@ __device__ int jacobi_solve(double *W, int ld, int K, int p, double rank_tol, do
     return flag;
 }
 
+// offset of column j inside a packed R with K rows: sum_{i<j} min(i+1, K)
+__device__ __forceinline__ int64_t packed_col_offset(int j, int K) {
+    return j <= K ? (int64_t)j * (j + 1) / 2 : (int64_t)K * (K + 1) / 2 + (int64_t)(j - K) * K;
+}
+
+// Packed block -> dense [R | c] with p rows (rows >= K and the strict lower part are zero).
+__device__ __forceinline__ void unpack_rc(const double *in, double *W, int ld, int p, int K, int lane) {
+    for (int j = 0; j <= p; ++j) {
+        const int h = j < p ? (j + 1 < K ? j + 1 : K) : K;
+        const double *src = in + packed_col_offset(j, K);
+        double *col = W + (size_t)j * ld;
+        for (int i = lane; i < p; i += 32) col[i] = i < h ? src[i] : 0.0;
+    }
+}
+
 }  // namespace
 
-// S: register slots over the N ensemble members (N <= 32 S); PS: slots over the p predecessors.
-template <int S, int PS>
-__global__ void __launch_bounds__(512, 1) regress_kernel(const RegressParams P) {
+// ---- K2a: load + Householder QR ------------------------------------------------------------
+template <int S>
+__global__ void __launch_bounds__(512, 1) regress_qr_kernel(const RegressParams P) {
     extern __shared__ double smem[];
     const int lane = threadIdx.x & 31;
     const int N = P.N, ld = P.ld, pmax = P.pmax;
-    double *W = smem + (size_t)(threadIdx.x >> 5) * regress_ws_doubles(N, pmax, P.maxdefl);
+    double *W = smem + (size_t)(threadIdx.x >> 5) * regress_qr_ws_doubles(N, pmax);
     double *rdiag = W + (size_t)ld * (pmax + 1);
-    double *rinv = rdiag + pmax;
-    double *aux = rinv + pmax;
-    double *Zs = aux + pmax;                    // deflated right singular vectors
-    double *Xs = Zs + P.maxdefl * pmax;         // deflated left singular vectors
     const double denom = (double)(N - 1);
+    const unsigned nf = (unsigned)(P.f1 - P.f0);
 
     for (;;) {
         unsigned int wk = 0;
         if (lane == 0) wk = atomicAdd(P.counter, 1u);
         wk = __shfl_sync(FULL, wk, 0);
         if ((int64_t)wk >= P.nwork) break;
-        const int q = P.work_order[wk / (unsigned)P.nfields];
-        const int f = (int)(wk % (unsigned)P.nfields);
+        const int q = P.work_order[wk / nf];
+        const int fl = (int)(wk % nf), f = P.f0 + fl;
         const int64_t r0 = P.row_ptr[q];
         const int p = (int)(P.row_ptr[q + 1] - r0);
         const double *Uf = P.U + (int64_t)f * P.nstate2d * N;
         const double *yrow = Uf + (int64_t)P.state_row[q] * N;
         const int32_t *pred = P.pred_state + r0;
-        int flag = 0;
 
         if (p == 0) {  // estimator.py:139-144
             double s = 0.0;
@@ -381,8 +504,6 @@ __global__ void __launch_bounds__(512, 1) regress_kernel(const RegressParams P) 
             }
             continue;
         }
-
-        // ---- load [A^T | y] ----------------------------------------------------------
         for (int j = 0; j <= p; ++j) {
             const double *src = (j < p) ? Uf + (int64_t)pred[j] * N : yrow;
             double *dst = W + (size_t)j * ld;
@@ -390,93 +511,106 @@ __global__ void __launch_bounds__(512, 1) regress_kernel(const RegressParams P) 
             for (int s = 0; s < S; ++s) { const int i = lane + 32 * s; if (i < N) dst[i] = src[i]; }
         }
         __syncwarp();
-
-        // ---- Householder QR (lanes over rows) -----------------------------------------
         const int K = p < N ? p : N;
         for (int k = 0; k < K; ++k) {
-            const double *ck = W + (size_t)k * ld;
-            double v[S];
-            double ss = 0.0;
-#pragma unroll
-            for (int s = 0; s < S; ++s) {
-                const int i = lane + 32 * s;
-                v[s] = (i >= k && i < N) ? ck[i] : 0.0;
-                ss += v[s] * v[s];
-            }
-            ss = warp_sum(ss);
-            const double x0 = ck[k];
-            const double nrm = sqrt(ss);
-            if (nrm == 0.0) {
-                if (lane == 0) rdiag[k] = 0.0;
-                continue;
-            }
-            const double alpha = (x0 >= 0.0) ? -nrm : nrm;
-            const double tau = 1.0 / (nrm * (nrm + fabs(x0)));   // 2 / v^T v
-#pragma unroll
-            for (int s = 0; s < S; ++s) if (lane + 32 * s == k) v[s] = x0 - alpha;
-            if (lane == 0) rdiag[k] = alpha;
-            // apply H = I - tau v v^T to columns k+1..p, four at a time
-            for (int j0 = k + 1; j0 <= p; j0 += 4) {
-                double c[4][S], d[4];
-#pragma unroll
-                for (int b = 0; b < 4; ++b) {
-                    const int j = j0 + b <= p ? j0 + b : p;     // clamp: duplicates are not stored
-                    const double *col = W + (size_t)j * ld;
-                    d[b] = 0.0;
-#pragma unroll
-                    for (int s = 0; s < S; ++s) {
-                        const int i = lane + 32 * s;
-                        c[b][s] = (i >= k && i < N) ? col[i] : 0.0;
-                        d[b] += v[s] * c[b][s];
-                    }
-                }
-                warp_sum4(d[0], d[1], d[2], d[3], lane);
-#pragma unroll
-                for (int b = 0; b < 4; ++b) {
-                    if (j0 + b > p) break;
-                    double *col = W + (size_t)(j0 + b) * ld;
-                    const double w = d[b] * tau;
-#pragma unroll
-                    for (int s = 0; s < S; ++s) {
-                        const int i = lane + 32 * s;
-                        if (i >= k && i < N) col[i] = c[b][s] - w * v[s];
-                    }
-                }
-            }
+            qr_step_dispatch<S>(W, ld, N, k, p, rdiag, lane);
             __syncwarp();
         }
-        // explicit diagonal, reciprocals, zero-pivot test
-        double dmin = DBL_MAX, dmax = 0.0;
-        for (int k = lane; k < K; k += 32) {
-            const double r = rdiag[k];
-            W[(size_t)k * ld + k] = r;
-            rinv[k] = 1.0 / r;
-            dmin = fmin(dmin, fabs(r));
-            dmax = fmax(dmax, fabs(r));
+        // packed output: R by columns, then c[0:K], then e2
+        double *out = P.Rq + (int64_t)fl * P.rq_stride + P.rq_ptr[q];
+        for (int j = 0; j < p; ++j) {
+            const int h = j + 1 < K ? j + 1 : K;
+            const double *col = W + (size_t)j * ld;
+            double *dst = out + packed_col_offset(j, K);
+            for (int i = lane; i < h; i += 32) dst[i] = (i == j) ? rdiag[j] : col[i];
         }
+        double *cdst = out + packed_col_offset(p, K);
+        const double *ycol = W + (size_t)p * ld;
+        double e2 = 0.0;
+        for (int i = lane; i < N; i += 32) {
+            const double yv = ycol[i];
+            if (i < K) cdst[i] = yv; else e2 += yv * yv;
+        }
+        e2 = warp_sum(e2);
+        if (lane == 0) cdst[K] = e2;
+        __syncwarp();
+    }
+}
+
+// ---- K2b: truncation probes + solve --------------------------------------------------------
+template <int PS>
+__global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressParams P) {
+    extern __shared__ double smem[];
+    const int lane = threadIdx.x & 31;
+    const int N = P.N, pmax = P.pmax, ld = pmax | 1;
+    double *W = smem + (size_t)(threadIdx.x >> 5) * regress_solve_ws_doubles(pmax, P.maxdefl);
+    double *rinv = W + (size_t)ld * (pmax + 1);
+    double *aux = rinv + pmax;
+    double *tmp = aux + pmax;
+    double *Zs = tmp + pmax;                    // deflated right singular vectors
+    double *Xs = Zs + P.maxdefl * pmax;         // deflated left singular vectors
+    const double denom = (double)(N - 1);
+    const unsigned nf = (unsigned)(P.f1 - P.f0);
+
+    for (;;) {
+        unsigned int wk = 0;
+        if (lane == 0) wk = atomicAdd(P.counter + 1, 1u);
+        wk = __shfl_sync(FULL, wk, 0);
+        if ((int64_t)wk >= P.nwork) break;
+        const int q = P.work_order[wk / nf];
+        const int fl = (int)(wk % nf), f = P.f0 + fl;
+        const int64_t r0 = P.row_ptr[q];
+        const int p = (int)(P.row_ptr[q + 1] - r0);
+        if (p == 0) continue;                    // done in K2a
+        const int K = p < N ? p : N;
+        int flag = 0;
+
+        // ---- unpack R | c into the dense workspace, zeros below the diagonal ---------------
+        const double *in = P.Rq + (int64_t)fl * P.rq_stride + P.rq_ptr[q];
+        double dmin = DBL_MAX, dmax = 0.0, fro2 = 0.0;
+        unpack_rc(in, W, ld, p, K, lane);
+        __syncwarp();
+        for (int j = lane; j < K; j += 32) {
+            const double v = W[(size_t)j * ld + j];
+            rinv[j] = 1.0 / v;
+            dmin = fmin(dmin, fabs(v));
+            dmax = fmax(dmax, fabs(v));
+        }
+        for (int j = 0; j < p; ++j) {
+            const double *col = W + (size_t)j * ld;
+            for (int i = lane; i <= j && i < K; i += 32) fro2 += col[i] * col[i];
+        }
+        const double e2 = in[packed_col_offset(p, K) + K];
         dmin = warp_min(dmin);
         dmax = warp_max(dmax);
+        const double fro = sqrt(warp_sum(fro2));
         __syncwarp();
         const double *cvec = W + (size_t)p * ld;   // Q^T y
         bool fallback = (K < p) || !(dmin > 1e-13 * dmax);
         int m = 0;
+        double dropped2 = 0.0;
 
         if (!fallback) {
-            // s_max by power iteration on R^T R (a lower bound, converging from below)
+            // s_max bracket: power iteration from below, Frobenius norm from above
             Vec<PS> v;
 #pragma unroll
             for (int t = 0; t < PS; ++t) v.v[t] = (lane + 32 * t < p) ? 1.0 : 0.0;
-            double smax = 0.0;
-            for (int it = 0; it < POWER_ITERS; ++it) {
-                Vec<PS> y = mul_upper<PS>(v, W, ld, p, lane);
-                v = mul_upper_t<PS>(y, W, ld, p, lane);
-                const double nv = sqrt(vdot<PS>(v, v));
-                smax = sqrt(nv);
-                const double inv = 1.0 / nv;
+            double smax_lo = dmax;
+            int power_done = 0;
+            auto power = [&](int iters) {
+                for (int it = 0; it < iters; ++it) {
+                    Vec<PS> y = mul_upper<PS>(v, W, ld, p, lane);
+                    v = mul_upper_t<PS>(y, W, ld, p, lane);
+                    const double nv = sqrt(vdot<PS>(v, v));
+                    if (power_done + it > 0) smax_lo = fmax(smax_lo, sqrt(nv));   // first pass starts unnormalised
+                    const double inv = 1.0 / nv;
 #pragma unroll
-                for (int t = 0; t < PS; ++t) v.v[t] *= inv;
-            }
-            const double thr = P.rank_tol * smax;
+                    for (int t = 0; t < PS; ++t) v.v[t] *= inv;
+                }
+                power_done += iters;
+            };
+            power(POWER_ITERS);
+            bool refined = false;
             // probes: smallest singular triplets by inverse iteration, deflating truncated ones
             for (;;) {
                 Vec<PS> z;
@@ -494,7 +628,7 @@ __global__ void __launch_bounds__(512, 1) regress_kernel(const RegressParams P) 
                     for (int t = 0; t < PS; ++t) z.v[t] *= inv;
                 }
                 double s_old = 0.0, dz_old = 1.0, s_est = 0.0;
-                int state = 0;   // 1 = kept (above threshold), 2 = truncated (vector converged)
+                int state = 0;   // 1 = kept, 2 = truncated (vector converged), 3 = undecided bracket
                 for (int it = 0; it < INVIT_MAX && state == 0; ++it) {
                     Vec<PS> zz = z;
                     solve_upper_t<PS>(zz, W, rinv, ld, p, lane);
@@ -518,22 +652,25 @@ __global__ void __launch_bounds__(512, 1) regress_kernel(const RegressParams P) 
                         z.v[t] = zn;
                     }
                     dz = sqrt(warp_sum(dz));
-                    if (s_est < thr) {
+                    const double thr_lo = P.rank_tol * smax_lo, thr_hi = P.rank_tol * (refined ? smax_lo : fro);
+                    if (s_est < thr_lo) {                       // s_min <= s_est < tol * s_max: truncated for sure
                         if ((dz < 1e-6 && dz > 0.25 * dz_old) || dz < 1e-13) state = 2;
                     } else if (fabs(s_est - s_old) < 1e-3 * s_est) {
-                        state = 1;
+                        state = (s_est >= 1.05 * thr_hi) ? 1 : 3;
                     }
                     s_old = s_est;
                     dz_old = dz;
                 }
-                if (state == 0) { fallback = true; break; }                 // no gap: let Jacobi decide
-                if (state == 1) {
-                    if (s_est < 1.05 * thr) fallback = true;                // too close to call
-                    break;
+                if (state == 3 && !refined) {                    // tighten s_max and look again
+                    power(POWER_ITERS_REFINE);
+                    refined = true;
+                    continue;
                 }
+                if (state == 0 || state == 3) { fallback = true; break; }   // no gap / too close to call
+                if (state == 1) break;
                 const Vec<PS> rz = mul_upper<PS>(z, W, ld, p, lane);
                 const double s = sqrt(vdot<PS>(rz, rz));
-                if (!(s < thr) || m >= P.maxdefl) { fallback = true; break; }
+                if (!(s < P.rank_tol * smax_lo) || m >= P.maxdefl) { fallback = true; break; }
                 const double inv = 1.0 / s;
                 Vec<PS> x;
 #pragma unroll
@@ -551,6 +688,7 @@ __global__ void __launch_bounds__(512, 1) regress_kernel(const RegressParams P) 
             for (int mm = 0; mm < m; ++mm) {
                 const Vec<PS> xm = vload<PS>(Xs + mm * pmax, p, lane);
                 const double pr = vdot<PS>(b, xm);
+                dropped2 += pr * pr;
 #pragma unroll
                 for (int t = 0; t < PS; ++t) b.v[t] -= pr * xm.v[t];
             }
@@ -565,33 +703,25 @@ __global__ void __launch_bounds__(512, 1) regress_kernel(const RegressParams P) 
             __syncwarp();
         } else {
             flag |= 1 | 16;
-            // explicit upper-trapezoidal R (the strict lower part still holds pre-QR data)
-            for (int j = lane; j < p; j += 32) {
-                double *col = W + (size_t)j * ld;
-                if (j < K) col[j] = rdiag[j];
-                for (int i = j + 1; i < K; ++i) col[i] = 0.0;
-            }
-            __syncwarp();
-            flag |= jacobi_solve(W, ld, K, p, P.rank_tol, rdiag, rinv, aux, lane);
+            flag |= jacobi_solve(W, ld, K, p, P.rank_tol, rinv, tmp, aux, &dropped2, lane);
         }
 
-        // ---- T = -beta, residual from the original rows, D ------------------------------
         double *Tout = P.T + (int64_t)f * P.nnz + r0;
         for (int j = lane; j < p; j += 32) Tout[j] = -aux[j];
-        double res[S];
+        // |y - A^T beta|^2 = e2 + |c - R beta|^2 ; the second term vanishes (to rounding) unless
+        // singular values were truncated, and is then evaluated explicitly from R, c and beta.
+        double rest2 = 0.0;
+        if (fallback || m > 0) {
+            if (fallback) { unpack_rc(in, W, ld, p, K, lane); __syncwarp(); }
+            const Vec<PS> b = vload<PS>(aux, p, lane);
+            const Vec<PS> rb = mul_upper<PS>(b, W, ld, p, lane);
+            const Vec<PS> c0 = vload<PS>(cvec, p, lane);
 #pragma unroll
-        for (int s = 0; s < S; ++s) { const int i = lane + 32 * s; res[s] = (i < N) ? yrow[i] : 0.0; }
-        for (int j = 0; j < p; ++j) {
-            const double b = aux[j];
-            const double *src = Uf + (int64_t)pred[j] * N;
-#pragma unroll
-            for (int s = 0; s < S; ++s) { const int i = lane + 32 * s; if (i < N) res[s] -= b * src[i]; }
+            for (int t = 0; t < PS; ++t) { const double df = c0.v[t] - rb.v[t]; rest2 += df * df; }
+            rest2 = warp_sum(rest2);
         }
-        double d = 0.0;
-#pragma unroll
-        for (int s = 0; s < S; ++s) d += res[s] * res[s];
-        d = warp_sum(d) / denom;
         if (lane == 0) {
+            const double d = (e2 + rest2) / denom;
             if (d < P.variance_floor) flag |= 8;
             P.D[(int64_t)f * P.nloc + q] = fmax(d, P.variance_floor);
             if (P.flags) P.flags[(int64_t)f * P.nloc + q] = flag;
@@ -600,48 +730,66 @@ __global__ void __launch_bounds__(512, 1) regress_kernel(const RegressParams P) 
     }
 }
 
-template <int S, int PS>
-static cudaError_t launch_regress_t(const RegressParams &p, int grid, int warps, size_t smem, cudaStream_t s) {
-    cudaError_t e = cudaFuncSetAttribute(regress_kernel<S, PS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+template <int S>
+static cudaError_t launch_qr_t(const RegressParams &p, int grid, int warps, size_t smem, cudaStream_t s) {
+    cudaError_t e = cudaFuncSetAttribute(regress_qr_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    regress_kernel<S, PS><<<grid, warps * 32, smem, s>>>(p);
+    regress_qr_kernel<S><<<grid, warps * 32, smem, s>>>(p);
     return cudaGetLastError();
 }
 
-template <int S>
-static cudaError_t launch_regress_s(const RegressParams &p, int grid, int warps, size_t smem, cudaStream_t s) {
-    if (p.pmax <= 32) return launch_regress_t<S, 1>(p, grid, warps, smem, s);
-    if (p.pmax <= 64) return launch_regress_t<S, 2>(p, grid, warps, smem, s);
-    if (p.pmax <= 96) return launch_regress_t<S, 3>(p, grid, warps, smem, s);
-    return cudaErrorInvalidConfiguration;
+template <int PS>
+static cudaError_t launch_solve_t(const RegressParams &p, int grid, int warps, size_t smem, cudaStream_t s) {
+    cudaError_t e = cudaFuncSetAttribute(regress_solve_kernel<PS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    regress_solve_kernel<PS><<<grid, warps * 32, smem, s>>>(p);
+    return cudaGetLastError();
 }
 
+// Launches K2a + K2b for fields [p.f0, p.f1).  p.counter points at two zero-initialised words.
 cudaError_t launch_regress(const RegressParams &p_in, int sm_count, size_t smem_limit, cudaStream_t s) {
     if (p_in.nwork == 0) return cudaSuccess;
+    if (p_in.pmax > 96) return cudaErrorInvalidConfiguration;
     RegressParams p = p_in;
-    int warps = (int)(smem_limit / (regress_ws_doubles(p.N, p.pmax, 1) * sizeof(double)));
-    if (warps < 1) return cudaErrorInvalidConfiguration;
-    if (warps > 16) warps = 16;
-    p.maxdefl = 1;   // as many deflation vectors as fit without losing a resident warp
-    while (p.maxdefl < REG_MAXDEFL_CAP &&
-           regress_ws_doubles(p.N, p.pmax, p.maxdefl + 1) * sizeof(double) * warps <= smem_limit)
-        ++p.maxdefl;
-    const size_t ws = regress_ws_doubles(p.N, p.pmax, p.maxdefl) * sizeof(double);
-    const int ctas_per_sm = 1;   // one persistent CTA of <= 16 warps per SM (<= 128 registers per thread)
-    const size_t smem = ws * warps;
-    cudaError_t e = cudaMemsetAsync(p.counter, 0, sizeof(unsigned int), s);
+    cudaError_t e = cudaMemsetAsync(p.counter, 0, 2 * sizeof(unsigned int), s);
     if (e != cudaSuccess) return e;
-    int64_t grid = (int64_t)sm_count * ctas_per_sm;
-    const int64_t need = (p.nwork + warps - 1) / warps;
-    if (grid > need) grid = need;
-    const int S = (p.N + 31) / 32;
-    switch (S) {
-        case 1: return launch_regress_s<1>(p, (int)grid, warps, smem, s);
-        case 2: return launch_regress_s<2>(p, (int)grid, warps, smem, s);
-        case 3: return launch_regress_s<3>(p, (int)grid, warps, smem, s);
-        case 4: return launch_regress_s<4>(p, (int)grid, warps, smem, s);
-        default: return launch_regress_s<8>(p, (int)grid, warps, smem, s);
+    // K2a
+    {
+        const size_t ws = regress_qr_ws_doubles(p.N, p.pmax) * sizeof(double);
+        int warps = (int)(smem_limit / ws);
+        if (warps < 1) return cudaErrorInvalidConfiguration;
+        if (warps > 16) warps = 16;
+        int64_t grid = sm_count;
+        const int64_t need = (p.nwork + warps - 1) / warps;
+        if (grid > need) grid = need;
+        const int S = (p.N + 31) / 32;
+        switch (S) {
+            case 1: e = launch_qr_t<1>(p, (int)grid, warps, ws * warps, s); break;
+            case 2: e = launch_qr_t<2>(p, (int)grid, warps, ws * warps, s); break;
+            case 3: e = launch_qr_t<3>(p, (int)grid, warps, ws * warps, s); break;
+            case 4: e = launch_qr_t<4>(p, (int)grid, warps, ws * warps, s); break;
+            default: e = launch_qr_t<8>(p, (int)grid, warps, ws * warps, s); break;
+        }
+        if (e != cudaSuccess) return e;
     }
+    // K2b
+    {
+        int warps = (int)(smem_limit / (regress_solve_ws_doubles(p.pmax, 1) * sizeof(double)));
+        if (warps < 1) return cudaErrorInvalidConfiguration;
+        if (warps > 16) warps = 16;
+        p.maxdefl = 1;   // as many deflation vectors as fit without losing a resident warp
+        while (p.maxdefl < REG_MAXDEFL_CAP &&
+               regress_solve_ws_doubles(p.pmax, p.maxdefl + 1) * sizeof(double) * warps <= smem_limit)
+            ++p.maxdefl;
+        const size_t ws = regress_solve_ws_doubles(p.pmax, p.maxdefl) * sizeof(double);
+        int64_t grid = sm_count;
+        const int64_t need = (p.nwork + warps - 1) / warps;
+        if (grid > need) grid = need;
+        if (p.pmax <= 32) e = launch_solve_t<1>(p, (int)grid, warps, ws * warps, s);
+        else if (p.pmax <= 64) e = launch_solve_t<2>(p, (int)grid, warps, ws * warps, s);
+        else e = launch_solve_t<3>(p, (int)grid, warps, ws * warps, s);
+    }
+    return e;
 }
 
 // ------------------------------------------------------------------------------------------

@@ -19,8 +19,12 @@ struct RegressParams {
     double *T;                 // [nfields][nnz]  (-beta)
     double *D;                 // [nfields][nloc] floored
     int32_t *flags;            // [nfields][nloc] or null
-    unsigned int *counter;     // work-fetch counter (zeroed by the launcher)
+    unsigned int *counter;     // two work-fetch counters (zeroed by the launcher)
     int maxdefl;               // deflation vectors the workspace holds (set by the launcher)
+    int f0, f1;                // fields handled by this launch pair (scratch is sized for f1 - f0)
+    double *Rq;                // packed QR output scratch [f1 - f0][rq_stride]
+    int64_t rq_stride;
+    const int64_t *rq_ptr;     // [nloc + 1] offsets of each row's packed block
 };
 
 struct SolveParams {
