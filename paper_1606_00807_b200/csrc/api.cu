@@ -26,7 +26,10 @@ struct DeviceState {
     int64_t *tile_ptr = nullptr, *row_ptr = nullptr, *csc_ptr = nullptr, *csc_src = nullptr;
     int32_t *col_idx = nullptr, *csc_row = nullptr, *phys = nullptr, *iphys = nullptr, *bw = nullptr,
             *state_row = nullptr, *pred_state = nullptr, *work_order = nullptr, *tile_order = nullptr;
-    int64_t *rq_ptr = nullptr;
+    int64_t *rq_ptr = nullptr, *band_ptr = nullptr;
+    int32_t *row_tile = nullptr;
+    int64_t band_stride = 0, band_fields = 0;
+    double *band = nullptr;
     int64_t rq_stride = 0;
     double *Rq = nullptr;
     int64_t rq_fields = 0;          // fields the QR scratch holds
@@ -98,6 +101,14 @@ int ensure_device(enkfmc_plan *p) {
     if ((rc = upload(d->state_row, p->state_row))) return rc;
     if ((rc = upload(d->pred_state, p->pred_state))) return rc;
     if ((rc = upload(d->is_interior, p->is_interior))) return rc;
+    if ((rc = upload(d->row_tile, p->row_tile))) return rc;
+    {   // column-form band of every tile
+        std::vector<int64_t> bp(p->ntiles + 1, 0);
+        for (int64_t t = 0; t < p->ntiles; ++t)
+            bp[t + 1] = bp[t] + (p->tile_ptr[t + 1] - p->tile_ptr[t]) * (int64_t)(p->bw[t] + 1);
+        d->band_stride = bp.back();
+        if ((rc = upload(d->band_ptr, bp))) return rc;
+    }
     {   // packed QR block of every local row: R by columns (min(j+1,K) entries), c[K], e2
         std::vector<int64_t> rq(p->sum_nlocal() + 1, 0);
         // K depends on the ensemble size; sized for K = p (the largest block), valid for any N
@@ -158,15 +169,24 @@ int ensure_solve_layout(enkfmc_plan *p, int64_t nens) {
     L = SolveParams{};
     L.N = (int)nens;
     L.bmax = (int)p->max_bw;
-    int64_t band = 1;
-    for (int64_t t = 0; t < p->ntiles; ++t)
-        band = std::max(band, (p->tile_ptr[t + 1] - p->tile_ptr[t]) * (int64_t)(p->bw[t] + 1));
     L.nfields = (int)p->nfields;
     L.ntiles = (int)p->ntiles;
     L.ntiles_owned = (int)p->ntiles;
-    const int64_t stride = solve_plan_scratch(L, band, std::max<int64_t>(p->max_nlocal, 1), d->smem_limit);
+    const int64_t stride = solve_plan_scratch(L, std::max<int64_t>(p->max_nlocal, 1), d->smem_limit);
     d->solve_grid = solve_grid_size(d->sm_count, L, d->smem_limit);
     CK(cudaMalloc(&d->scratch, (size_t)stride * d->solve_grid * sizeof(double)));
+    return ENKFMC_OK;
+}
+
+// Band / Cholesky-factor buffer: as many fields per launch pair as fit in the budget (16 GiB).
+int ensure_band(enkfmc_plan *p) {
+    DeviceState *d = p->dev;
+    const int64_t budget = (int64_t)16 << 30;
+    const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(p->nfields, budget / std::max<int64_t>(8 * d->band_stride, 1)));
+    if (d->band && d->band_fields >= chunk) return ENKFMC_OK;
+    release(d->band);
+    CK(cudaMalloc(&d->band, std::max<size_t>((size_t)chunk * d->band_stride, 1) * sizeof(double)));
+    d->band_fields = chunk;
     return ENKFMC_OK;
 }
 
@@ -238,13 +258,23 @@ int do_solve(enkfmc_plan *p, const double *d_X, const double *d_T, const double 
     S.col_idx = d->col_idx; S.csc_row = d->csc_row; S.phys = d->phys; S.iphys = d->iphys; S.bw = d->bw;
     S.state_row = d->state_row; S.obs_slot = d->obs_slot; S.tile_nobs = d->tile_nobs; S.tile_order = d->tile_order;
     S.is_interior = d->is_interior; S.scratch = d->scratch; S.status = d_status; S.counter = d->counters + 2;
-    cudaError_t e = launch_local_solve(S, d->solve_grid, d->smem_limit, s);
-    if (e == cudaErrorInvalidConfiguration) {
-        enkfmc_set_error("local-solve window (half-bandwidth " + std::to_string(p->max_bw) + ") exceeds shared memory");
-        return ENKFMC_E_CAPACITY;
+    S.band_ptr = d->band_ptr; S.band_stride = d->band_stride; S.row_tile = d->row_tile; S.work_order = d->work_order;
+    S.nrows_owned = (int64_t)p->work_order.size();
+    int rc2 = ensure_band(p);
+    if (rc2) return rc2;
+    S.band = d->band;
+    for (int64_t f0 = 0; f0 < p->nfields; f0 += d->band_fields) {
+        S.f0 = (int)f0;
+        S.f1 = (int)std::min<int64_t>(p->nfields, f0 + d->band_fields);
+        CK(launch_assemble_band(S, d->sm_count, s));
+        cudaError_t e = launch_local_solve(S, d->solve_grid, d->smem_limit, s);
+        if (e == cudaErrorInvalidConfiguration) {
+            enkfmc_set_error("local-solve window (half-bandwidth " + std::to_string(p->max_bw) + ") exceeds shared memory");
+            return ENKFMC_E_CAPACITY;
+        }
+        CK(e);
+        p->counters[0] += 2;
     }
-    CK(e);
-    p->counters[0] += 1;
     return ENKFMC_OK;
 }
 
@@ -260,7 +290,7 @@ void enkfmc_device_release(enkfmc_plan *p) {
     release(d->csc_row); release(d->phys); release(d->iphys); release(d->bw); release(d->state_row);
     release(d->pred_state); release(d->work_order); release(d->tile_order); release(d->is_interior);
     release(d->obs_slot); release(d->tile_nobs); release(d->U); release(d->T); release(d->D); release(d->scratch);
-    release(d->flags); release(d->status); release(d->counters); release(d->rq_ptr); release(d->Rq); release(d->dX); release(d->dXa); release(d->dR);
+    release(d->flags); release(d->status); release(d->counters); release(d->rq_ptr); release(d->Rq); release(d->band_ptr); release(d->band); release(d->row_tile); release(d->dX); release(d->dXa); release(d->dR);
     release(d->dYs);
     for (auto &ev : d->ev) if (ev) cudaEventDestroy(ev);
     for (auto &ev : d->prof) cudaEventDestroy(ev);
@@ -464,21 +494,23 @@ extern "C" int enkfmc_scatter_rows(double *d_dst, const int64_t *d_dst_rows, con
 
 extern "C" int enkfmc_assemble_band(enkfmc_plan *p, const double *d_T, const double *d_D, int64_t tile,
                                     double *d_band, void *stream) {
-    if (tile < 0 || tile >= p->ntiles) { enkfmc_set_error("tile index out of range"); return ENKFMC_E_VALUE; }
+    if (p->ntiles != 1 || p->nfields != 1 || tile != 0) {
+        enkfmc_set_error("assemble_band needs a single-tile, single-field plan");
+        return ENKFMC_E_VALUE;
+    }
     int rc = ensure_device(p);
     if (rc) return rc;
-    if ((rc = ensure_solve_layout(p, 2))) return rc;
+    if ((rc = ensure_orders(p))) return rc;
     DeviceState *d = p->dev;
-    SolveParams S = d->solve_layout;
-    S.T = d_T; S.D = d_D;
+    SolveParams S{};
+    S.T = d_T; S.D = d_D; S.nfields = 1; S.ntiles = 1; S.ntiles_owned = 1; S.bmax = (int)p->max_bw;
     S.nloc = p->sum_nlocal(); S.nnz = p->nnz(); S.nstate2d = p->nstate2d;
     S.tile_ptr = d->tile_ptr; S.row_ptr = d->row_ptr; S.csc_ptr = d->csc_ptr; S.csc_src = d->csc_src;
-    S.col_idx = d->col_idx; S.csc_row = d->csc_row; S.phys = d->phys; S.iphys = d->iphys; S.bw = d->bw;
-    S.state_row = d->state_row; S.obs_slot = d->state_row /* unused */; S.tile_nobs = d->bw /* unused */;
-    S.tile_order = d->tile_order; S.is_interior = d->is_interior; S.scratch = d->scratch;
-    S.status = nullptr; S.counter = d->counters + 2;
-    S.assemble_only = 1; S.tile_sel = (int)tile; S.band_out = d_band; S.ntiles_owned = 1;
-    CK(launch_local_solve(S, 1, d->smem_limit, (cudaStream_t)stream));
+    S.col_idx = d->col_idx; S.csc_row = d->csc_row; S.phys = d->phys; S.bw = d->bw;
+    S.band_ptr = d->band_ptr; S.band_stride = d->band_stride; S.row_tile = d->row_tile; S.work_order = d->work_order;
+    S.nrows_owned = (int64_t)p->work_order.size();
+    S.assemble_only = 1; S.f0 = 0; S.f1 = 1; S.band = d_band;
+    CK(launch_assemble_band(S, d->sm_count, (cudaStream_t)stream));
     p->counters[0] += 1;
     return ENKFMC_OK;
 }

@@ -793,17 +793,71 @@ cudaError_t launch_regress(const RegressParams &p_in, int sm_count, size_t smem_
 }
 
 // ------------------------------------------------------------------------------------------
-// K3: one CTA per (field, tile).
+// K3: local analysis of every (field, tile), in two kernels.
 //
 // A = T~^T D^-1 T~ + H^T R^-1 H with T~ = I + strictly-lower T (factors.py:136-145,
-// kernels.py:189-191) is symmetric and banded (half-bandwidth b) in the tile's physical
-// order.  Phase A assembles its lower band column by column into CTA scratch (L2-resident);
-// phase B runs a right-looking banded Cholesky through a sliding (b+2)-row window, carrying
-// the N right-hand sides rhs[obs] = (Ys - Xb[obs]) / r (kernels.py:182-186) along (forward
-// substitution fused); phase C is the backward substitution and writes Xa = Xb + dx for the
-// interior rows straight into the global analysis (kernels.py:218, driver.py:116).
+// kernels.py:189-191) is symmetric and banded (half-bandwidth b) in the tile's physical order.
+//
+// K3a assemble_band_kernel: one warp per column I of A (high occupancy, the index chasing is
+//   latency-bound).  A[I+d, I] = sum_j T~[j,i] T~[j,k] / D_j over the rows j holding both i and
+//   k, accumulated in ascending j in a per-warp shared buffer (deterministic), stored as the
+//   column-form lower band band[tile][I][d].
+// K3b local_solve_kernel: one CTA per (field, tile).  Right-looking banded Cholesky through a
+//   sliding (b+2)-row window in shared memory, carrying the N right-hand sides
+//   rhs[obs] = (Ys - Xb[obs]) / r (kernels.py:182-186) along (forward substitution fused);
+//   L overwrites the band.  Then the backward substitution, which writes Xa = Xb + dx for the
+//   interior rows straight into the global analysis (kernels.py:218, driver.py:116).
 // ------------------------------------------------------------------------------------------
 #define SOLVE_THREADS 256
+#define ASM_WARPS 8
+
+__global__ void __launch_bounds__(ASM_WARPS * 32) assemble_band_kernel(const SolveParams P) {
+    extern __shared__ double smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double *acc = smem + (size_t)warp * (P.bmax + 1);
+    const int nf = P.f1 - P.f0;
+    const int64_t nrows = P.nrows_owned;
+    const int64_t total = nrows * nf;
+    const int64_t stride = (int64_t)gridDim.x * ASM_WARPS;
+    for (int64_t w = (int64_t)blockIdx.x * ASM_WARPS + warp; w < total; w += stride) {
+        const int fl = (int)(w / nrows), f = P.f0 + fl;
+        const int q = P.work_order[w % nrows];
+        const int t = P.row_tile[q];
+        if (!P.assemble_only && P.tile_nobs[(int64_t)f * P.ntiles + t] == 0) continue;
+        const int64_t base = P.tile_ptr[t];
+        const int i = (int)(q - base);
+        const int b = P.bw[t], bw1 = b + 1;
+        const int32_t *phys = P.phys + base;
+        const int I = phys[i];
+        const double *Tf = P.T + (int64_t)f * P.nnz;
+        const double *Df = P.D + (int64_t)f * P.nloc + base;
+        for (int d = lane; d <= b; d += 32) acc[d] = 0.0;
+        __syncwarp();
+        const int64_t c0 = P.csc_ptr[base + i], c1 = P.csc_ptr[base + i + 1];
+        for (int64_t e = c0 - 1; e < c1; ++e) {
+            int j; double tji;
+            if (e < c0) { j = i; tji = 1.0; } else { j = P.csc_row[e]; tji = Tf[P.csc_src[e]]; }
+            const double s = tji / Df[j];
+            const int64_t q0 = P.row_ptr[base + j];
+            const int cnt = (int)(P.row_ptr[base + j + 1] - q0);
+            for (int m = lane - 1; m < cnt; m += 32) {
+                int k; double tjk;
+                if (m < 0) { k = j; tjk = 1.0; } else { k = P.col_idx[q0 + m]; tjk = Tf[q0 + m]; }
+                const int Kp = phys[k];
+                if (Kp >= I) acc[Kp - I] += s * tjk;
+            }
+            __syncwarp();
+        }
+        if (lane == 0 && !P.assemble_only) {
+            const int sl = P.obs_slot[(int64_t)f * P.nloc + q];
+            if (sl >= 0) acc[0] += 1.0 / P.rdiag[sl];
+        }
+        __syncwarp();
+        double *dst = P.band + (int64_t)fl * P.band_stride + P.band_ptr[t] + (int64_t)I * bw1;
+        for (int d = lane; d <= b; d += 32) dst[d] = acc[d];
+        __syncwarp();
+    }
+}
 
 __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveParams P) {
     extern __shared__ double smem[];
@@ -813,7 +867,6 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
     const int nthreads = blockDim.x, nwarps = nthreads >> 5;
     const int N = P.N;
     double *scr = P.scratch + (int64_t)blockIdx.x * P.scratch_stride;
-    double *Acol = scr;                 // [n][b+1]  column-form lower band, overwritten by L
     double *Z = scr + P.off_z;          // [n][N]    forward-substituted right-hand sides
     // shared layout: lk[2][bmax+2] | red[nthreads] | window A | window RHS
     const int bmax = P.bmax;
@@ -823,7 +876,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
     const int WnMax = bmax + 2, PitchMax = WnMax | 1;
     double *Aw = P.a_in_smem ? sm_rest : scr + P.off_win_a;
     double *Rw = P.r_in_smem ? (P.a_in_smem ? sm_rest + (size_t)WnMax * PitchMax : sm_rest) : scr + P.off_win_r;
-    const int total_items = P.nfields * P.ntiles_owned;
+    const int total_items = (P.f1 - P.f0) * P.ntiles_owned;
 
     for (;;) {
         __syncthreads();
@@ -831,62 +884,27 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
         __syncthreads();
         const unsigned int item = s_item;
         if ((int)item >= total_items) break;
-        const int t = P.assemble_only ? P.tile_sel : P.tile_order[item / (unsigned)P.nfields];
-        const int f = P.assemble_only ? 0 : (int)(item % (unsigned)P.nfields);
-        if (P.assemble_only && item > 0) break;
+        const unsigned nf = (unsigned)(P.f1 - P.f0);
+        const int t = P.tile_order[item / nf];
+        const int fl = (int)(item % nf), f = P.f0 + fl;
         const int64_t base = P.tile_ptr[t];
         const int n = (int)(P.tile_ptr[t + 1] - base);
         const int b = P.bw[t];
         const int Wn = b + 2, pitch = Wn | 1, bw1 = b + 1;
+        double *Acol = P.band + (int64_t)fl * P.band_stride + P.band_ptr[t];   // [n][b+1], overwritten by L
         const double *Xf = P.X + (int64_t)f * P.nstate2d * N;
         double *Xaf = P.Xa + (int64_t)f * P.nstate2d * N;
-        const double *Tf = P.T + (int64_t)f * P.nnz;
-        const double *Df = P.D + (int64_t)f * P.nloc + base;
         const int32_t *slotf = P.obs_slot + (int64_t)f * P.nloc + base;
-        const int32_t *phys = P.phys + base, *iphys = P.iphys + base, *srow = P.state_row + base;
+        const int32_t *iphys = P.iphys + base, *srow = P.state_row + base;
         const uint8_t *inter = P.is_interior + base;
 
-        if (!P.assemble_only && P.tile_nobs[(int64_t)f * P.ntiles + t] == 0) {   // kernels.py:179-180: exact copy
+        if (P.tile_nobs[(int64_t)f * P.ntiles + t] == 0) {   // kernels.py:179-180: exact copy
             for (int j = warp; j < n; j += nwarps) {
                 if (!inter[j]) continue;
                 const int64_t g = (int64_t)srow[j] * N;
                 for (int m = lane; m < N; m += 32) Xaf[g + m] = Xf[g + m];
             }
             if (tid == 0) P.status[(int64_t)f * P.ntiles + t] = 0;
-            continue;
-        }
-
-        // ---- phase A: assemble the band, one warp per column I (physical index) ---------
-        {
-            double *acc = sm_rest + (size_t)warp * (bmax + 1);   // aliases the window: not live yet
-            for (int I = warp; I < n; I += nwarps) {
-                for (int d = lane; d <= b; d += 32) acc[d] = 0.0;
-                __syncwarp();
-                const int i = iphys[I];
-                const int64_t c0 = P.csc_ptr[base + i], c1 = P.csc_ptr[base + i + 1];
-                for (int64_t e = c0 - 1; e < c1; ++e) {
-                    int j; double tji;
-                    if (e < c0) { j = i; tji = 1.0; } else { j = P.csc_row[e]; tji = Tf[P.csc_src[e]]; }
-                    const double s = tji / Df[j];
-                    const int64_t q0 = P.row_ptr[base + j];
-                    const int cnt = (int)(P.row_ptr[base + j + 1] - q0);
-                    for (int m = lane - 1; m < cnt; m += 32) {
-                        int k; double tjk;
-                        if (m < 0) { k = j; tjk = 1.0; } else { k = P.col_idx[q0 + m]; tjk = Tf[q0 + m]; }
-                        const int Kp = phys[k];
-                        if (Kp >= I) acc[Kp - I] += s * tjk;
-                    }
-                    __syncwarp();
-                }
-                if (lane == 0 && !P.assemble_only) { const int sl = slotf[i]; if (sl >= 0) acc[0] += 1.0 / P.rdiag[sl]; }
-                __syncwarp();
-                for (int d = lane; d <= b; d += 32) Acol[(int64_t)I * bw1 + d] = acc[d];
-                __syncwarp();
-            }
-        }
-        __syncthreads();
-        if (P.assemble_only) {
-            for (int64_t e = tid; e < (int64_t)n * bw1; e += nthreads) P.band_out[e] = Acol[e];
             continue;
         }
 
@@ -913,7 +931,8 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
 
         // ---- phase B: banded Cholesky + forward substitution ----------------------------
         const int ty = tid >> 4, tx = tid & 15;
-        const int da = nthreads / N, dm = nthreads % N;
+        const int parts = nthreads / N > 0 ? nthreads / N : 1;
+        const int m_f = tid % N, part_f = tid / N;
         for (int k = 0; k < n; ++k) {
             const int hi = (k + b < n - 1) ? k + b : n - 1;
             const int cnt = hi - k;
@@ -945,15 +964,13 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
                     row[cc] -= la * lk[c];
                 }
             }
-            // right-hand sides of rows k+1..hi
-            {
-                const double *zk = Rw + (size_t)k0 * N;
-                int a = tid / N, m = tid % N;
-                while (a < cnt) {
-                    int ra = k1 + a; if (ra >= Wn) ra -= Wn;
-                    Rw[(size_t)ra * N + m] -= lk[a] * zk[m];
-                    a += da; m += dm;
-                    if (m >= N) { m -= N; ++a; }
+            // right-hand sides of rows k+1..hi: thread = (member m, row phase part)
+            if (part_f < parts) {
+                const double zk = Rw[(size_t)k0 * N + m_f];
+                int ra = (k1 + part_f) % Wn;
+                for (int a = part_f; a < cnt; a += parts) {
+                    Rw[(size_t)ra * N + m_f] -= lk[a] * zk;
+                    ra += parts; while (ra >= Wn) ra -= Wn;
                 }
             }
             // bring in the next row (its slot held row k-1, already retired)
@@ -966,7 +983,6 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
         }
 
         // ---- phase C: backward substitution, Xa = Xb + dx on interior rows -------------
-        const int parts = nthreads / N > 0 ? nthreads / N : 1;
         {
             const int k = n - 1;
             for (int d = tid; d < 1; d += nthreads) lk[d] = Acol[(int64_t)k * bw1 + d];
@@ -978,11 +994,14 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
             const double *lcur = lk + ((n - 1 - k) & 1) * (bmax + 2);
             double *lnext = lk + ((n - k) & 1) * (bmax + 2);
             // partial dot products over the already-solved rows k+1..hi
-            {
-                const int m = tid % N, part = tid / N;
+            if (part_f < parts) {
                 double s = 0.0;
-                if (part < parts) for (int d = 1 + part; d <= cnt; d += parts) s += lcur[d] * RW(k + d, m);
-                if (part < parts) red[part * N + m] = s;
+                int r = (k + 1 + part_f) % Wn;
+                for (int d = 1 + part_f; d <= cnt; d += parts) {
+                    s += lcur[d] * Rw[(size_t)r * N + m_f];
+                    r += parts; while (r >= Wn) r -= Wn;
+                }
+                red[part_f * N + m_f] = s;
             }
             // prefetch column k-1 of L
             if (k > 0) {
@@ -1010,7 +1029,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
 }
 
 // Scratch / shared-memory layout chosen on the host.
-int64_t solve_plan_scratch(SolveParams &p, int64_t max_band_doubles, int64_t nmax, size_t smem_limit) {
+int64_t solve_plan_scratch(SolveParams &p, int64_t nmax, size_t smem_limit) {
     const int64_t Wn = p.bmax + 2, pitch = Wn | 1;
     const size_t fixed = (size_t)(2 * (p.bmax + 2) + SOLVE_THREADS) * sizeof(double) + 64;
     const size_t a_bytes = (size_t)(Wn * pitch) * sizeof(double);
@@ -1019,7 +1038,7 @@ int64_t solve_plan_scratch(SolveParams &p, int64_t max_band_doubles, int64_t nma
     p.a_in_smem = fixed + a_bytes <= smem_limit;
     p.r_in_smem = fixed + (p.a_in_smem ? a_bytes : 0) + r_bytes <= smem_limit;
     (void)acc_bytes;
-    int64_t off = max_band_doubles;
+    int64_t off = 0;
     p.off_z = off; off += nmax * p.N;
     p.off_win_a = off; if (!p.a_in_smem) off += Wn * pitch;
     p.off_win_r = off; if (!p.r_in_smem) off += Wn * p.N;
@@ -1033,8 +1052,6 @@ static size_t solve_smem_bytes(const SolveParams &p) {
     size_t rest = 0;
     if (p.a_in_smem) rest += (size_t)(Wn * pitch);
     if (p.r_in_smem) rest += (size_t)(Wn * p.N);
-    const size_t acc = (size_t)(SOLVE_THREADS / 32) * (p.bmax + 1);
-    if (rest < acc) rest = acc;
     return (size_t)(2 * (p.bmax + 2) + SOLVE_THREADS + rest) * sizeof(double);
 }
 
@@ -1049,8 +1066,22 @@ int solve_grid_size(int sm_count, const SolveParams &p, size_t smem_limit) {
     return (int)(grid < 1 ? 1 : grid);
 }
 
+cudaError_t launch_assemble_band(const SolveParams &p, int sm_count, cudaStream_t s) {
+    const int64_t total = p.nrows_owned * (p.f1 - p.f0);
+    if (total == 0) return cudaSuccess;
+    int64_t grid = (total + ASM_WARPS - 1) / ASM_WARPS;
+    if (grid > (int64_t)sm_count * 8) grid = (int64_t)sm_count * 8;
+    const size_t smem = (size_t)ASM_WARPS * (p.bmax + 1) * sizeof(double);
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(assemble_band_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    assemble_band_kernel<<<(unsigned)grid, ASM_WARPS * 32, smem, s>>>(p);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_local_solve(const SolveParams &p, int grid, size_t smem_limit, cudaStream_t s) {
-    if (p.nfields * p.ntiles_owned == 0) return cudaSuccess;
+    if ((p.f1 - p.f0) * p.ntiles_owned == 0) return cudaSuccess;
     const size_t smem = solve_smem_bytes(p);
     if (smem > smem_limit) return cudaErrorInvalidConfiguration;
     cudaError_t e = cudaFuncSetAttribute(local_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

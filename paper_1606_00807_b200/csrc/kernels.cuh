@@ -42,16 +42,22 @@ struct SolveParams {
     int a_in_smem, r_in_smem;  // window placement
     int32_t *status;           // [nfields * ntiles]
     unsigned int *counter;
-    int assemble_only;         // 1: write the band of T^T D^-1 T (no obs term) of tile_sel to band_out
-    int tile_sel;
-    double *band_out;          // [n][b+1] column-form lower band
+    int assemble_only;         // 1: K3a writes T^T D^-1 T without the observation term, for every owned tile
+    int f0, f1;                // fields handled by this launch pair
+    double *band;              // [f1 - f0][band_stride]: per tile [n][b+1] column-form lower band / L
+    int64_t band_stride;
+    const int64_t *band_ptr;   // [ntiles] offset of each tile's band
+    const int32_t *row_tile;   // [nloc]
+    const int32_t *work_order; // owned local rows
+    int64_t nrows_owned;
 };
 
 size_t regress_warp_workspace_doubles(int N, int pmax);
 cudaError_t launch_center_rows(const double *X, double *U, int64_t nrows, int N, cudaStream_t s);
 cudaError_t launch_regress(const RegressParams &p, int sm_count, size_t smem_limit, cudaStream_t s);
 // Fills scratch layout fields of p given bmax/nmax; returns doubles per CTA.
-int64_t solve_plan_scratch(SolveParams &p, int64_t max_band_doubles, int64_t nmax, size_t smem_limit);
+int64_t solve_plan_scratch(SolveParams &p, int64_t nmax, size_t smem_limit);
+cudaError_t launch_assemble_band(const SolveParams &p, int sm_count, cudaStream_t s);
 int solve_grid_size(int sm_count, const SolveParams &p, size_t smem_limit);
 cudaError_t launch_local_solve(const SolveParams &p, int grid, size_t smem_limit, cudaStream_t s);
 cudaError_t launch_scatter_rows(double *dst, const int64_t *dst_rows, const double *src, const int64_t *src_rows,

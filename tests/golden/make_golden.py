@@ -24,6 +24,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
 
 import mcholkf  # noqa: E402
 from mcholkf.validation import center_rows  # noqa: E402
+from threadpoolctl import threadpool_limits  # noqa: E402
 
 from paper_1606_00807_b200 import synthetic  # noqa: E402
 
@@ -92,7 +93,8 @@ def analysis_case(w, tag):
         xb = w.X[sd.local_order]
         f = mcholkf.fit_factors(center_rows(xb), g, w.zeta, local_order=sd.local_order)
         net_l, rows = mcholkf.restrict_network(net, sd.local_order)
-        xl = mcholkf.analysis_primal(mcholkf.EnsembleState(xb), f, net_l, w.Ys[rows])
+        with threadpool_limits(limits=1):      # as assimilate_parallel does (driver.py:231)
+            xl = mcholkf.analysis_primal(mcholkf.EnsembleState(xb), f, net_l, w.Ys[rows])
         rowptr.append(f.lower.indptr + tptr[-1])
         tptr.append(tptr[-1] + f.lower.nnz)
         tind.append(f.lower.indices)

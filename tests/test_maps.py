@@ -1,0 +1,132 @@
+"""CPU: the C-ABI library's host index maps (csrc/plan.cpp) -- bit-exact against the golden
+fixtures and the oracle; no GPU needed (no compute entry point is called)."""
+
+import numpy as np
+import pytest
+
+import paper_1606_00807_b200 as mck
+from oracle import enkf_mc_oracle as orc
+from paper_1606_00807_b200 import plan as P
+from paper_1606_00807_b200.plan import Plan, get_plan
+
+
+def _geo(nx, ny, rm=True, per=False, nfields=1):
+    return mck.GridGeometry("ring1d" if ny == 1 else "grid2d", nx, ny, "row_major" if rm else "column_major",
+                            "periodic" if per else "clipped", nfields)
+
+
+def test_decompose_predecessors_golden(golden_geometry):
+    G = golden_geometry
+    for k in range(int(G["ncases"])):
+        nx, ny, rm, per, delta, zeta = [int(v) for v in G[f"g{k}_params"]]
+        g = _geo(nx, ny, bool(rm), bool(per))
+        sds = mck.decompose(g, delta, zeta)
+        assert [s.id for s in sds] == list(G[f"g{k}_ids"])
+        assert np.array_equal(np.concatenate([s.interior for s in sds]), G[f"g{k}_interior"])
+        assert np.array_equal(np.concatenate([s.halo for s in sds]), G[f"g{k}_halo"])
+        assert np.array_equal(np.concatenate([s.local_order for s in sds]), G[f"g{k}_local"])
+        assert np.array_equal(np.concatenate([s.interior_positions() for s in sds]), G[f"g{k}_intpos"])
+        assert all(s.interior.dtype == np.intp for s in sds)
+        pp, pr = G[f"g{k}_pred_ptr"], G[f"g{k}_pred"]
+        bp, bx = G[f"g{k}_box_ptr"], G[f"g{k}_box"]
+        for c in range(0, g.n2d, max(1, g.n2d // 97)):
+            assert np.array_equal(mck.predecessors(g, c, zeta), pr[pp[c]:pp[c + 1]])
+            assert np.array_equal(mck.local_box(g, c, zeta).members, bx[bp[c]:bp[c + 1]])
+        # the single-tile plan over the whole grid reproduces every predecessor list
+        pl = Plan.local(g, zeta, np.arange(g.n2d))
+        assert np.array_equal(pl.get(P.ROW_PTR), pp) and np.array_equal(pl.get(P.COL_IDX), pr)
+
+
+@pytest.mark.parametrize("cfg", [(64, 32, False, 8, 2), (64, 32, True, 8, 2), (192, 96, False, 64, 3), (48, 24, True, 6, 5)])
+def test_tile_csr_matches_oracle(cfg):
+    nx, ny, per, delta, zeta = cfg
+    g = _geo(nx, ny, True, per)
+    grid = orc.Grid(nx, ny, True, per)
+    pl = get_plan(g, delta, zeta)
+    tp, rp, ci = pl.get(P.TILE_PTR), pl.get(P.ROW_PTR), pl.get(P.COL_IDX)
+    bw, ph = pl.get(P.BANDWIDTH), pl.get(P.PHYS)
+    for t, tile in enumerate(orc.decompose(grid, delta, zeta)):
+        ip, ii = orc.predecessor_csr(grid, zeta, tile.local_order)
+        lo, hi = tp[t], tp[t + 1]
+        assert np.array_equal(rp[lo:hi + 1] - rp[lo], ip)
+        assert np.array_equal(ci[rp[lo]:rp[hi]], ii)
+        phys = ph[lo:hi]
+        assert np.array_equal(np.sort(phys), np.arange(hi - lo))          # a permutation
+        if not per:
+            assert np.array_equal(phys, np.arange(hi - lo))               # clipped: physical == label order
+        rows = np.repeat(np.arange(hi - lo), np.diff(ip))
+        span = max((max(phys[r], phys[ii[ip[r]:ip[r + 1]]].max(initial=0)) - min(phys[r], phys[ii[ip[r]:ip[r + 1]]].min(initial=10**9))
+                    for r in range(hi - lo)), default=0)
+        assert bw[t] == span and rows.size == ii.size
+    if not per and zeta == 3:
+        assert pl.max_bw == 93 and pl.sum_nlocal == 32292 and pl.nnz == 654624
+
+
+def test_restrict_observations_per_field_tile():
+    g = _geo(24, 16, True, True, nfields=3)
+    grid = orc.Grid(24, 16, True, True, 3)
+    rng = np.random.default_rng(4)
+    obs = np.sort(rng.choice(g.nstate, 300, replace=False))
+    pl = Plan.decomposed(g, 6, 2)
+    pl.set_observations(obs)
+    optr, opos, orow = pl.get(P.OBS_PTR), pl.get(P.OBS_POS), pl.get(P.OBS_ROW)
+    tiles = orc.decompose(grid, 6, 2)
+    for f in range(3):
+        sel = np.flatnonzero((obs >= f * g.n2d) & (obs < (f + 1) * g.n2d))
+        for t, tile in enumerate(tiles):
+            pos, rows = orc.restrict_observations(obs[sel] - f * g.n2d, tile.local_order)
+            a, b = optr[f * 6 + t], optr[f * 6 + t + 1]
+            assert np.array_equal(opos[a:b], pos) and np.array_equal(orow[a:b], sel[rows])
+    net = mck.ObservationNetwork(obs[obs < g.n2d], np.ones((obs < g.n2d).sum()), np.zeros((obs < g.n2d).sum()))
+    loc, rows = mck.restrict_network(net, tiles[2].local_order)
+    pos, rows_ref = orc.restrict_observations(net.obs_indices, tiles[2].local_order)
+    assert np.array_equal(loc.obs_indices, pos) and np.array_equal(rows, rows_ref)
+
+
+def test_work_counts_match_survey_and_tile_ranges():
+    g = _geo(192, 96, nfields=29)
+    pl = Plan.decomposed(g, 256, 4)
+    reg, sol = pl.work(80)
+    assert reg == pytest.approx(2.86e11, rel=0.01) and sol == pytest.approx(6.48e10, rel=0.01)
+    pl.set_tile_range(0, 128)
+    r0, _ = pl.work(80)
+    pl.set_tile_range(128, 256)
+    r1, _ = pl.work(80)
+    assert r0 + r1 == pytest.approx(reg, rel=1e-12)
+    with pytest.raises(ValueError):
+        pl.set_tile_range(10, 300)
+
+
+def test_errors_follow_the_reference():
+    with pytest.raises(mck.ConfigurationError, match="7"):
+        mck.decompose(_geo(3, 2), 7, 1)                                    # test_geometry.py:189-191
+    with pytest.raises(mck.ConfigurationError):
+        mck.decompose(_geo(3, 2), 0, 1)
+    with pytest.raises(ValueError):
+        mck.decompose(_geo(3, 2), 2, -1)
+    with pytest.raises(ValueError):
+        mck.predecessors(_geo(3, 2), 99, 1)
+    with pytest.raises(ValueError, match="strictly increasing"):
+        Plan.local(_geo(4, 4), 1, np.array([3, 2, 5]))
+    with pytest.raises(ValueError, match="strictly lower"):
+        Plan.from_csr(np.array([0, 1]), np.array([0]))
+    pl = Plan.decomposed(_geo(4, 4), 4, 1)
+    with pytest.raises(ValueError, match="exceed"):
+        pl.set_observations(np.array([3, 16]))
+    with pytest.raises(ValueError):
+        mck.GridGeometry("grid3d", 4, 4)
+    with pytest.raises(mck.ConfigurationError):
+        mck.AssimilationConfig(method="bogus")
+    with pytest.raises(ValueError, match="lengths"):
+        mck.ObservationNetwork(np.array([1, 2]), np.array([1.0]), np.array([0.0, 0.0]))
+    with pytest.raises(ValueError, match="positive"):
+        mck.ObservationNetwork(np.array([1]), np.array([0.0]), np.array([0.0]))
+    with pytest.raises(ValueError, match="finite"):
+        mck.EnsembleState(np.array([[np.nan, 1.0]]))
+    assert mck.linear_index(_geo(5, 3, rm=False), 2, 4) == 14 and mck.grid_coords(_geo(5, 3, rm=False), 14) == (2, 4)
+
+
+def test_perturb_observations_is_the_reference_stream(golden_analysis):
+    A = golden_analysis
+    net = mck.ObservationNetwork(A["a0_obs"], A["a0_r"], A["a0_y"])
+    assert np.array_equal(mck.perturb_observations(net, int(A["a0_params"][3]), 11, 0).Ys, A["a0_Ys"])

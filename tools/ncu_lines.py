@@ -1,0 +1,61 @@
+"""Attribute an ncu report's per-instruction counters to CUDA source lines (needs -lineinfo).
+
+usage: ncu_lines.py <report.ncu-rep> <kernel-regex> [top]
+Joins `ncu --page source --csv` (SASS rows, in address order) with `nvdisasm -g` line info of the
+same kernel extracted from libenkfmc.so.
+"""
+import csv
+import io
+import os
+import re
+import subprocess
+import sys
+import tempfile
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+rep, kre = sys.argv[1], sys.argv[2]
+top = int(sys.argv[3]) if len(sys.argv) > 3 else 30
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", "regex:" + kre], capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(out)))
+kname = rows[0][1]
+hdr = rows[1]
+ci, si, ai = hdr.index("Instructions Executed"), hdr.index("# Samples"), hdr.index("Address")
+mangled = None
+with tempfile.TemporaryDirectory() as td:
+    subprocess.run(["cuobjdump", "-xelf", "all", os.path.join(ROOT, "paper_1606_00807_b200", "libenkfmc.so")], cwd=td,
+                   capture_output=True)
+    dis = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(td, "kernels.sm_100a.cubin")], capture_output=True, text=True).stdout
+base_name = re.sub(r"^void ", "", kname).split("(")[0].split("<")[0]
+targs = re.findall(r"\(int\)(\d+)", kname)
+sections = re.split(r"\n\t\.section\t\.text\.", dis)
+sec = None
+for s in sections[1:]:
+    name = s.split(",")[0]
+    if base_name in name and all(f"Li{t}E" in name for t in targs) and name.count("Li") == len(targs):
+        sec = s
+        break
+assert sec is not None, kname
+addr2line, cur = {}, None
+for ln in sec.split("\n"):
+    m = re.search(r'//## File ".*?", line (\d+)', ln)
+    if m:
+        cur = int(m.group(1))
+        continue
+    m = re.match(r"\s*/\*([0-9a-f]+)\*/\s+\S", ln)
+    if m:
+        addr2line[int(m.group(1), 16)] = cur
+base = int(rows[2][ai], 16)
+agg = {}
+for r in rows[2:]:
+    try:
+        off, n, s = int(r[ai], 16) - base, int(r[ci]), int(r[si])
+    except (ValueError, IndexError):
+        continue
+    a = agg.setdefault(addr2line.get(off), [0, 0])
+    a[0] += n
+    a[1] += s
+src = open(os.path.join(ROOT, "paper_1606_00807_b200", "csrc", "kernels.cu")).read().split("\n")
+tot, ts = sum(a[0] for a in agg.values()), sum(a[1] for a in agg.values())
+print(f"{kname}: {tot:.4g} warp instructions, {ts} samples")
+for l, a in sorted(agg.items(), key=lambda kv: -kv[1][0])[:top]:
+    print("%5.1f%% inst %5.1f%% samp  L%s: %s" % (100 * a[0] / tot, 100 * a[1] / max(ts, 1), l, src[l - 1].strip()[:105] if l else "?"))
