@@ -161,8 +161,9 @@ int enkfmc_fp64_peak(double *tflops, void *stream);
 int enkfmc_scatter_rows(double *d_dst, const int64_t *d_dst_rows, const double *d_src,
                         const int64_t *d_src_rows, int64_t nrows, int64_t nens, void *stream);
 
-/* Lower band (column form, d_band[n_local][bw+1], physical order) of T^T D^-1 T of one tile,
- * field 0, without the observation term -- PrecisionFactors.dense_precision, factors.py:136-145. */
+/* Lower band of T^T D^-1 T (no observation term) of a single-tile plan, row form:
+ * d_band[n][Wr], Wr = 8 (Wb + 1), Wb = floor((bw + 7) / 8); entry e of row I is column
+ * 8 (I/8 - Wb) + e -- PrecisionFactors.dense_precision, factors.py:136-145. */
 int enkfmc_assemble_band(enkfmc_plan *plan, const double *d_T, const double *d_D, int64_t tile,
                          double *d_band, void *stream);
 

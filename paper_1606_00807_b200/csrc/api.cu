@@ -102,10 +102,10 @@ int ensure_device(enkfmc_plan *p) {
     if ((rc = upload(d->pred_state, p->pred_state))) return rc;
     if ((rc = upload(d->is_interior, p->is_interior))) return rc;
     if ((rc = upload(d->row_tile, p->row_tile))) return rc;
-    {   // column-form band of every tile
+    {   // row-form band of every tile: [8 ceil(n/8)][8 (Wb + 1)], Wb = floor((b + 7) / 8)
         std::vector<int64_t> bp(p->ntiles + 1, 0);
         for (int64_t t = 0; t < p->ntiles; ++t)
-            bp[t + 1] = bp[t] + (p->tile_ptr[t + 1] - p->tile_ptr[t]) * (int64_t)(p->bw[t] + 1);
+            bp[t + 1] = bp[t] + ((p->tile_ptr[t + 1] - p->tile_ptr[t] + 7) / 8 * 8) * (int64_t)(8 * ((p->bw[t] + 7) / 8 + 1));
         d->band_stride = bp.back();
         if ((rc = upload(d->band_ptr, bp))) return rc;
     }

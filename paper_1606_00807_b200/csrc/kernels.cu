@@ -10,6 +10,7 @@
 // All results are deterministic run to run: no floating-point atomics, fixed reduction
 // trees, work items are independent.
 
+#include <algorithm>
 #include <cfloat>
 #include <cmath>
 #include <cstdio>
@@ -797,24 +798,31 @@ cudaError_t launch_regress(const RegressParams &p_in, int sm_count, size_t smem_
 //
 // A = T~^T D^-1 T~ + H^T R^-1 H with T~ = I + strictly-lower T (factors.py:136-145,
 // kernels.py:189-191) is symmetric and banded (half-bandwidth b) in the tile's physical order.
+// Rows are grouped in blocks of 8; Wb = floor((b+7)/8) block sub-diagonals can be non-zero.
 //
-// K3a assemble_band_kernel: one warp per column I of A (high occupancy, the index chasing is
-//   latency-bound).  A[I+d, I] = sum_j T~[j,i] T~[j,k] / D_j over the rows j holding both i and
-//   k, accumulated in ascending j in a per-warp shared buffer (deterministic), stored as the
-//   column-form lower band band[tile][I][d].
-// K3b local_solve_kernel: one CTA per (field, tile).  Right-looking banded Cholesky through a
-//   sliding (b+2)-row window in shared memory, carrying the N right-hand sides
-//   rhs[obs] = (Ys - Xb[obs]) / r (kernels.py:182-186) along (forward substitution fused);
-//   L overwrites the band.  Then the backward substitution, which writes Xa = Xb + dx for the
-//   interior rows straight into the global analysis (kernels.py:218, driver.py:116).
+// K3a assemble_band_kernel: one warp per row I of A (high occupancy; the index chasing is
+//   latency-bound).  A[I, K] = sum_j T~[j,i] T~[j,k] / D_j over the rows j holding both i and k,
+//   accumulated in ascending j in a per-warp shared buffer (deterministic), stored in row form:
+//   band[tile][I][e] = A[I, 8 (I/8 - Wb) + e], e < Wr = 8 (Wb + 1), zeros elsewhere.
+// K3b local_solve_kernel: one CTA per (field, tile).  Right-looking blocked banded Cholesky
+//   through a sliding window of Wb+1 block rows in shared memory, carrying the N right-hand sides
+//   rhs[obs] = (Ys - Xb[obs]) / r (kernels.py:182-186) along (forward substitution fused).
+//   Per block column: 8x8 diagonal factor, panel solve, then register-tiled rank-8 updates of the
+//   trailing window (1x8 strips) and of the right-hand sides (one member per thread).  L
+//   overwrites the band block by block.  The backward substitution runs blockwise the same way
+//   and writes Xa = Xb + dx for the interior rows straight into the global analysis
+//   (kernels.py:218, driver.py:116).
 // ------------------------------------------------------------------------------------------
 #define SOLVE_THREADS 256
 #define ASM_WARPS 8
+#define LP_PITCH 10   // doubles per panel row: 16-byte aligned, conflict-free for 128-bit loads
+
+__host__ __device__ inline int solve_wb(int b) { return (b + 7) >> 3; }
 
 __global__ void __launch_bounds__(ASM_WARPS * 32) assemble_band_kernel(const SolveParams P) {
     extern __shared__ double smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    double *acc = smem + (size_t)warp * (P.bmax + 1);
+    double *acc = smem + (size_t)warp * (8 * (solve_wb(P.bmax) + 1));
     const int nf = P.f1 - P.f0;
     const int64_t nrows = P.nrows_owned;
     const int64_t total = nrows * nf;
@@ -826,12 +834,13 @@ __global__ void __launch_bounds__(ASM_WARPS * 32) assemble_band_kernel(const Sol
         if (!P.assemble_only && P.tile_nobs[(int64_t)f * P.ntiles + t] == 0) continue;
         const int64_t base = P.tile_ptr[t];
         const int i = (int)(q - base);
-        const int b = P.bw[t], bw1 = b + 1;
+        const int Wb = solve_wb(P.bw[t]), Wr = 8 * (Wb + 1);
         const int32_t *phys = P.phys + base;
         const int I = phys[i];
+        const int col0 = 8 * ((I >> 3) - Wb);          // column of band entry e = 0
         const double *Tf = P.T + (int64_t)f * P.nnz;
         const double *Df = P.D + (int64_t)f * P.nloc + base;
-        for (int d = lane; d <= b; d += 32) acc[d] = 0.0;
+        for (int e = lane; e < Wr; e += 32) acc[e] = 0.0;
         __syncwarp();
         const int64_t c0 = P.csc_ptr[base + i], c1 = P.csc_ptr[base + i + 1];
         for (int64_t e = c0 - 1; e < c1; ++e) {
@@ -844,17 +853,17 @@ __global__ void __launch_bounds__(ASM_WARPS * 32) assemble_band_kernel(const Sol
                 int k; double tjk;
                 if (m < 0) { k = j; tjk = 1.0; } else { k = P.col_idx[q0 + m]; tjk = Tf[q0 + m]; }
                 const int Kp = phys[k];
-                if (Kp >= I) acc[Kp - I] += s * tjk;
+                if (Kp <= I) acc[Kp - col0] += s * tjk;
             }
             __syncwarp();
         }
         if (lane == 0 && !P.assemble_only) {
             const int sl = P.obs_slot[(int64_t)f * P.nloc + q];
-            if (sl >= 0) acc[0] += 1.0 / P.rdiag[sl];
+            if (sl >= 0) acc[I - col0] += 1.0 / P.rdiag[sl];
         }
         __syncwarp();
-        double *dst = P.band + (int64_t)fl * P.band_stride + P.band_ptr[t] + (int64_t)I * bw1;
-        for (int d = lane; d <= b; d += 32) dst[d] = acc[d];
+        double *dst = P.band + (int64_t)fl * P.band_stride + P.band_ptr[t] + (int64_t)I * Wr;
+        for (int e = lane; e < Wr; e += 32) dst[e] = acc[e];
         __syncwarp();
     }
 }
@@ -863,20 +872,25 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
     extern __shared__ double smem[];
     __shared__ unsigned int s_item;
     __shared__ int s_fail;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int nthreads = blockDim.x, nwarps = nthreads >> 5;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int nthreads = SOLVE_THREADS;
     const int N = P.N;
     double *scr = P.scratch + (int64_t)blockIdx.x * P.scratch_stride;
-    double *Z = scr + P.off_z;          // [n][N]    forward-substituted right-hand sides
-    // shared layout: lk[2][bmax+2] | red[nthreads] | window A | window RHS
-    const int bmax = P.bmax;
-    double *lk = smem;
-    double *red = lk + 2 * (bmax + 2);
-    double *sm_rest = red + nthreads;
-    const int WnMax = bmax + 2, PitchMax = WnMax | 1;
+    double *Z = scr + P.off_z;                 // [nbp][N] forward-substituted right-hand sides
+    // shared layout: Lp[2][WrMax][LP_PITCH] | Zb[8][N] | invd[8] | strips | window A | window RHS
+    const int WbMax = solve_wb(P.bmax), WrMax = 8 * (WbMax + 1), PitchMax = WrMax + 2;
+    double *Lp0 = smem;
+    double *Zb = Lp0 + 2 * (size_t)WrMax * LP_PITCH;
+    double *invd = Zb + 8 * (size_t)N;
+    unsigned short *strips = reinterpret_cast<unsigned short *>(invd + 8);
+    double *sm_rest = invd + 8 + (((4 * WbMax * (WbMax + 1) * 2 + 7) / 8 + 1) & ~1);
     double *Aw = P.a_in_smem ? sm_rest : scr + P.off_win_a;
-    double *Rw = P.r_in_smem ? (P.a_in_smem ? sm_rest + (size_t)WnMax * PitchMax : sm_rest) : scr + P.off_win_r;
-    const int total_items = (P.f1 - P.f0) * P.ntiles_owned;
+    double *Rw = P.r_in_smem ? (P.a_in_smem ? sm_rest + P.a_doubles : sm_rest) : scr + P.off_win_r;
+    (void)PitchMax;
+    const unsigned nf = (unsigned)(P.f1 - P.f0);
+    const int total_items = (int)nf * P.ntiles_owned;
+    const int G = nthreads / N > 0 ? nthreads / N : 1;     // row groups for the per-member updates
+    const int m_f = tid % N, g_f = tid / N;
 
     for (;;) {
         __syncthreads();
@@ -884,22 +898,21 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
         __syncthreads();
         const unsigned int item = s_item;
         if ((int)item >= total_items) break;
-        const unsigned nf = (unsigned)(P.f1 - P.f0);
         const int t = P.tile_order[item / nf];
         const int fl = (int)(item % nf), f = P.f0 + fl;
         const int64_t base = P.tile_ptr[t];
         const int n = (int)(P.tile_ptr[t + 1] - base);
-        const int b = P.bw[t];
-        const int Wn = b + 2, pitch = Wn | 1, bw1 = b + 1;
-        double *Acol = P.band + (int64_t)fl * P.band_stride + P.band_ptr[t];   // [n][b+1], overwritten by L
+        const int Wb = solve_wb(P.bw[t]), nslot = Wb + 1, Wr = 8 * nslot, pitch = Wr + 2;
+        const int nb = (n + 7) >> 3;
         const double *Xf = P.X + (int64_t)f * P.nstate2d * N;
         double *Xaf = P.Xa + (int64_t)f * P.nstate2d * N;
         const int32_t *slotf = P.obs_slot + (int64_t)f * P.nloc + base;
         const int32_t *iphys = P.iphys + base, *srow = P.state_row + base;
         const uint8_t *inter = P.is_interior + base;
+        double *band = P.band + (int64_t)fl * P.band_stride + P.band_ptr[t];   // [8 nb][Wr]: A rows, then L blocks
 
         if (P.tile_nobs[(int64_t)f * P.ntiles + t] == 0) {   // kernels.py:179-180: exact copy
-            for (int j = warp; j < n; j += nwarps) {
+            for (int j = tid >> 5; j < n; j += nthreads >> 5) {
                 if (!inter[j]) continue;
                 const int64_t g = (int64_t)srow[j] * N;
                 for (int m = lane; m < N; m += 32) Xaf[g + m] = Xf[g + m];
@@ -908,73 +921,144 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
             continue;
         }
 
-        // window accessors (circular in both indices)
-#define AW(I, K) Aw[(size_t)((I) % Wn) * pitch + ((K) % Wn)]
-#define RW(I, m) Rw[(size_t)((I) % Wn) * N + (m)]
-        // load physical row R of the band and of the right-hand side into the window
-        auto load_row = [&](int R) {
-            const int klo = R - b > 0 ? R - b : 0;
-            for (int K = klo + tid; K <= R; K += nthreads) AW(R, K) = Acol[(int64_t)K * bw1 + (R - K)];
-            const int i = iphys[R];
-            const int sl = slotf[i];
-            if (sl >= 0) {
-                const double rinv = 1.0 / P.rdiag[sl];
-                const double *ys = P.Ys + (int64_t)sl * N;
-                const double *xb = Xf + (int64_t)srow[i] * N;
-                for (int m = tid; m < N; m += nthreads) RW(R, m) = (ys[m] - xb[m]) * rinv;
-            } else {
-                for (int m = tid; m < N; m += nthreads) RW(R, m) = 0.0;
+        // strips of the trailing update: (block column q, panel row r >= 8 q), ordered by q then r
+        const int nstrips = 4 * Wb * (Wb + 1);
+        for (int s = tid; s < nstrips; s += nthreads) {
+            int q = 0, rem = s;
+            while (rem >= 8 * (Wb - q)) { rem -= 8 * (Wb - q); ++q; }
+            strips[s] = (unsigned short)((q << 10) | (8 * q + rem));
+        }
+        // load block row R (8 rows of A and of the right-hand side) into its window slot
+        auto load_block_row = [&](int R) {
+            const int rs = (R % nslot) * 8;
+            const int rot = (((R - Wb) % nslot) + nslot) % nslot * 8;   // window column of band entry 0
+            for (int e = tid; e < 8 * Wr; e += nthreads) {
+                const int rr = e / Wr, ee = e - rr * Wr, i = 8 * R + rr;
+                double v;
+                if (i < n) v = band[(int64_t)i * Wr + ee];
+                else v = (ee == 8 * Wb + rr) ? 1.0 : 0.0;              // padding row: identity
+                int cc = rot + ee; if (cc >= Wr) cc -= Wr;
+                Aw[(size_t)(rs + rr) * pitch + cc] = v;
+            }
+            for (int e = tid; e < 8 * N; e += nthreads) {
+                const int rr = e / N, m = e - rr * N, i = 8 * R + rr;
+                double v = 0.0;
+                if (i < n) {
+                    const int il = iphys[i];
+                    const int sl = slotf[il];
+                    if (sl >= 0) v = (P.Ys[(int64_t)sl * N + m] - Xf[(int64_t)srow[il] * N + m]) * (1.0 / P.rdiag[sl]);
+                }
+                Rw[(size_t)(rs + rr) * N + m] = v;
             }
         };
-        for (int R = 0; R <= b && R < n; ++R) load_row(R);
+        for (int R = 0; R <= Wb && R < nb; ++R) load_block_row(R);
         __syncthreads();
 
-        // ---- phase B: banded Cholesky + forward substitution ----------------------------
-        const int ty = tid >> 4, tx = tid & 15;
-        const int parts = nthreads / N > 0 ? nthreads / N : 1;
-        const int m_f = tid % N, part_f = tid / N;
-        for (int k = 0; k < n; ++k) {
-            const int hi = (k + b < n - 1) ? k + b : n - 1;
-            const int cnt = hi - k;
-            const double piv = AW(k, k);
-            if (!(piv > 0.0) || !(piv < DBL_MAX)) { if (tid == 0) s_fail = (piv == piv) ? 1 : 2; }
-            const double lkk = sqrt(piv), inv = 1.0 / lkk;
-            // column k of L -> lk[] and global; z_k -> window (scaled) and global
-            for (int a = tid; a < cnt; a += nthreads) {
-                const double v = AW(k + 1 + a, k) * inv;
-                lk[a] = v;
-                Acol[(int64_t)k * bw1 + 1 + a] = v;
-            }
-            if (tid == 0) Acol[(int64_t)k * bw1] = lkk;
-            for (int m = tid; m < N; m += nthreads) {
-                const double z = RW(k, m) * inv;
-                RW(k, m) = z;
-                Z[(int64_t)k * N + m] = z;
+        // ---- forward: blocked Cholesky + forward substitution --------------------------------
+        double *Lp = Lp0;
+        for (int J = 0; J < nb; ++J) {
+            const int sJ = (J % nslot) * 8;
+            const int below = (nb - 1 - J < Wb ? nb - 1 - J : Wb) * 8;     // panel rows under the diagonal block
+            // (a) 8x8 Cholesky of the diagonal block, warp 0, result in Lp rows 0..7
+            if (tid < 32) {
+                double *Dg = Aw + (size_t)sJ * pitch + sJ;
+                for (int c = 0; c < 8; ++c) {
+                    const double piv = Dg[(size_t)c * pitch + c];
+                    if (!(piv > 0.0) || !(piv < DBL_MAX)) { if (lane == 0) s_fail = (piv == piv) ? 1 : 2; }
+                    const double inv = 1.0 / sqrt(piv);
+                    __syncwarp();
+                    if (lane > c && lane < 8) Dg[(size_t)lane * pitch + c] *= inv;
+                    if (lane == c) { Dg[(size_t)c * pitch + c] = piv * inv; invd[c] = inv; }
+                    __syncwarp();
+                    // rank-1 update of the remaining lower triangle: element (r, c2), c < c2 <= r < 8
+                    for (int e = lane; e < 64; e += 32) {
+                        const int r = e >> 3, c2 = e & 7;
+                        if (c2 > c && c2 <= r) Dg[(size_t)r * pitch + c2] -= Dg[(size_t)r * pitch + c] * Dg[(size_t)c2 * pitch + c];
+                    }
+                    __syncwarp();
+                }
+                for (int e = lane; e < 64; e += 32) {
+                    const int r = e >> 3, c = e & 7;
+                    Lp[r * LP_PITCH + c] = (c <= r) ? Dg[(size_t)r * pitch + c] : 0.0;
+                }
             }
             __syncthreads();
             if (s_fail) break;
-            // trailing update of the (cnt x cnt) lower triangle (window indices wrap at Wn)
-            const int k1 = (k + 1) % Wn, k0 = k % Wn;
-            for (int a = ty; a < cnt; a += SOLVE_THREADS / 16) {
-                const double la = lk[a];
-                int ra = k1 + a; if (ra >= Wn) ra -= Wn;
-                double *row = Aw + (size_t)ra * pitch;
-                for (int c = tx; c <= a; c += 16) {
-                    int cc = k1 + c; if (cc >= Wn) cc -= Wn;
-                    row[cc] -= la * lk[c];
+            // (b) panel rows: x L_JJ^T = a ; right-hand sides: L_JJ z = b
+            for (int r = tid; r < below; r += nthreads) {
+                const int R = J + 1 + (r >> 3);
+                const double *arow = Aw + (size_t)((R % nslot) * 8 + (r & 7)) * pitch + sJ;
+                double x[8];
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    double s = arow[c];
+#pragma unroll
+                    for (int c2 = 0; c2 < c; ++c2) s -= x[c2] * Lp[c * LP_PITCH + c2];
+                    x[c] = s * invd[c];
+                }
+#pragma unroll
+                for (int c = 0; c < 8; ++c) Lp[(8 + r) * LP_PITCH + c] = x[c];
+            }
+            for (int m = tid; m < N; m += nthreads) {
+                double z[8];
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    double s = Rw[(size_t)(sJ + c) * N + m];
+#pragma unroll
+                    for (int c2 = 0; c2 < c; ++c2) s -= z[c2] * Lp[c * LP_PITCH + c2];
+                    z[c] = s * invd[c];
+                    Zb[c * N + m] = z[c];
+                    Z[(int64_t)(8 * J + c) * N + m] = z[c];
                 }
             }
-            // right-hand sides of rows k+1..hi: thread = (member m, row phase part)
-            if (part_f < parts) {
-                const double zk = Rw[(size_t)k0 * N + m_f];
-                int ra = (k1 + part_f) % Wn;
-                for (int a = part_f; a < cnt; a += parts) {
-                    Rw[(size_t)ra * N + m_f] -= lk[a] * zk;
-                    ra += parts; while (ra >= Wn) ra -= Wn;
+            __syncthreads();
+            // L block -> global (overwrites the A rows of block J, already consumed)
+            for (int e = tid; e < (8 + below) * 8; e += nthreads)
+                band[(int64_t)8 * J * Wr + e] = Lp[(e >> 3) * LP_PITCH + (e & 7)];
+            // (c) trailing update, 1x8 strips: A[i, 8q..8q+7] -= L[i,:] . L[8q..8q+7,:]^T
+            const int ns_live = 4 * (below >> 3) * ((below >> 3) + 1);
+            for (int s = tid; s < nstrips; s += nthreads) {
+                const int q = strips[s] >> 10, r = strips[s] & 1023;
+                if (r >= below) continue;
+                (void)ns_live;
+                const double2 *li2 = reinterpret_cast<const double2 *>(Lp + (8 + r) * LP_PITCH);
+                const double2 l01 = li2[0], l23 = li2[1], l45 = li2[2], l67 = li2[3];
+                const int R = J + 1 + (r >> 3), Q = J + 1 + q;
+                double *arow = Aw + (size_t)((R % nslot) * 8 + (r & 7)) * pitch + (Q % nslot) * 8;
+                double2 *a2 = reinterpret_cast<double2 *>(arow);
+                double acc[8];
+                { const double2 t0 = a2[0], t1 = a2[1], t2 = a2[2], t3 = a2[3];
+                  acc[0] = t0.x; acc[1] = t0.y; acc[2] = t1.x; acc[3] = t1.y; acc[4] = t2.x; acc[5] = t2.y; acc[6] = t3.x; acc[7] = t3.y; }
+#pragma unroll
+                for (int jj = 0; jj < 8; ++jj) {
+                    const double2 *lj2 = reinterpret_cast<const double2 *>(Lp + (8 + 8 * q + jj) * LP_PITCH);
+                    const double2 m01 = lj2[0], m23 = lj2[1], m45 = lj2[2], m67 = lj2[3];
+                    double d = acc[jj];
+                    d = fma(-l01.x, m01.x, d); d = fma(-l01.y, m01.y, d); d = fma(-l23.x, m23.x, d); d = fma(-l23.y, m23.y, d);
+                    d = fma(-l45.x, m45.x, d); d = fma(-l45.y, m45.y, d); d = fma(-l67.x, m67.x, d); d = fma(-l67.y, m67.y, d);
+                    acc[jj] = d;
+                }
+                a2[0] = make_double2(acc[0], acc[1]); a2[1] = make_double2(acc[2], acc[3]);
+                a2[2] = make_double2(acc[4], acc[5]); a2[3] = make_double2(acc[6], acc[7]);
+            }
+            // (d) right-hand sides of the rows below: one member per thread, rows strided by G
+            if (g_f < G) {
+                double z[8];
+#pragma unroll
+                for (int c = 0; c < 8; ++c) z[c] = Zb[c * N + m_f];
+                for (int r = g_f; r < below; r += G) {
+                    const double2 *li2 = reinterpret_cast<const double2 *>(Lp + (8 + r) * LP_PITCH);
+                    const double2 l01 = li2[0], l23 = li2[1], l45 = li2[2], l67 = li2[3];
+                    const int R = J + 1 + (r >> 3);
+                    double *bp = Rw + (size_t)((R % nslot) * 8 + (r & 7)) * N + m_f;
+                    double d = *bp;
+                    d = fma(-l01.x, z[0], d); d = fma(-l01.y, z[1], d); d = fma(-l23.x, z[2], d); d = fma(-l23.y, z[3], d);
+                    d = fma(-l45.x, z[4], d); d = fma(-l45.y, z[5], d); d = fma(-l67.x, z[6], d); d = fma(-l67.y, z[7], d);
+                    *bp = d;
                 }
             }
-            // bring in the next row (its slot held row k-1, already retired)
-            if (k + b + 1 < n) load_row(k + b + 1);
+            // (e) bring in the next block row (its slot held block row J, now retired)
+            if (J + Wb + 1 < nb) load_block_row(J + Wb + 1);
             __syncthreads();
         }
         if (s_fail) {
@@ -982,77 +1066,96 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
             continue;
         }
 
-        // ---- phase C: backward substitution, Xa = Xb + dx on interior rows -------------
-        {
-            const int k = n - 1;
-            for (int d = tid; d < 1; d += nthreads) lk[d] = Acol[(int64_t)k * bw1 + d];
-        }
+        // ---- backward: L^T x = z blockwise, Xa = Xb + dx on interior rows --------------------
+        double *red = Aw;                       // [G][8][N] partial sums (the A window is dead now)
+        auto load_panel = [&](int J, double *dst) {
+            const int below = (nb - 1 - J < Wb ? nb - 1 - J : Wb) * 8;
+            for (int e = tid; e < (8 + below) * 8; e += nthreads)
+                dst[(e >> 3) * LP_PITCH + (e & 7)] = band[(int64_t)8 * J * Wr + e];
+        };
+        load_panel(nb - 1, Lp0);
         __syncthreads();
-        for (int k = n - 1; k >= 0; --k) {
-            const int hi = (k + b < n - 1) ? k + b : n - 1;
-            const int cnt = hi - k;
-            const double *lcur = lk + ((n - 1 - k) & 1) * (bmax + 2);
-            double *lnext = lk + ((n - k) & 1) * (bmax + 2);
-            // partial dot products over the already-solved rows k+1..hi
-            if (part_f < parts) {
-                double s = 0.0;
-                int r = (k + 1 + part_f) % Wn;
-                for (int d = 1 + part_f; d <= cnt; d += parts) {
-                    s += lcur[d] * Rw[(size_t)r * N + m_f];
-                    r += parts; while (r >= Wn) r -= Wn;
+        for (int J = nb - 1; J >= 0; --J) {
+            const double *Lc = Lp0 + (size_t)((nb - 1 - J) & 1) * WrMax * LP_PITCH;
+            double *Ln = Lp0 + (size_t)((nb - J) & 1) * WrMax * LP_PITCH;
+            const int below = (nb - 1 - J < Wb ? nb - 1 - J : Wb) * 8;
+            if (g_f < G) {
+                double acc[8];
+#pragma unroll
+                for (int c = 0; c < 8; ++c) acc[c] = 0.0;
+                for (int r = g_f; r < below; r += G) {
+                    const double2 *li2 = reinterpret_cast<const double2 *>(Lc + (8 + r) * LP_PITCH);
+                    const double2 l01 = li2[0], l23 = li2[1], l45 = li2[2], l67 = li2[3];
+                    const int R = J + 1 + (r >> 3);
+                    const double x = Rw[(size_t)((R % nslot) * 8 + (r & 7)) * N + m_f];
+                    acc[0] = fma(l01.x, x, acc[0]); acc[1] = fma(l01.y, x, acc[1]); acc[2] = fma(l23.x, x, acc[2]);
+                    acc[3] = fma(l23.y, x, acc[3]); acc[4] = fma(l45.x, x, acc[4]); acc[5] = fma(l45.y, x, acc[5]);
+                    acc[6] = fma(l67.x, x, acc[6]); acc[7] = fma(l67.y, x, acc[7]);
                 }
-                red[part_f * N + m_f] = s;
+#pragma unroll
+                for (int c = 0; c < 8; ++c) red[((size_t)g_f * 8 + c) * N + m_f] = acc[c];
             }
-            // prefetch column k-1 of L
-            if (k > 0) {
-                const int hi2 = (k - 1 + b < n - 1) ? k - 1 + b : n - 1;
-                for (int d = tid; d <= hi2 - (k - 1); d += nthreads) lnext[d] = Acol[(int64_t)(k - 1) * bw1 + d];
-            }
+            if (J > 0) load_panel(J - 1, Ln);
             __syncthreads();
-            if (tid < N) {
-                double s = Z[(int64_t)k * N + tid];
-                for (int pt = 0; pt < parts; ++pt) s -= red[pt * N + tid];
-                const double x = s / lcur[0];
-                RW(k, tid) = x;
-                const int i = iphys[k];
-                if (inter[i]) {
-                    const int64_t g = (int64_t)srow[i] * N + tid;
-                    Xaf[g] = Xf[g] + x;
+            for (int m = tid; m < N; m += nthreads) {
+                double x[8];
+#pragma unroll
+                for (int c = 7; c >= 0; --c) {
+                    double s = Z[(int64_t)(8 * J + c) * N + m];
+                    for (int g = 0; g < G; ++g) s -= red[((size_t)g * 8 + c) * N + m];
+#pragma unroll
+                    for (int c2 = c + 1; c2 < 8; ++c2) s -= Lc[c2 * LP_PITCH + c] * x[c2];
+                    x[c] = s / Lc[c * LP_PITCH + c];
+                    const int i = 8 * J + c;
+                    Rw[(size_t)((J % nslot) * 8 + c) * N + m] = x[c];
+                    if (i < n) {
+                        const int il = iphys[i];
+                        if (inter[il]) {
+                            const int64_t gidx = (int64_t)srow[il] * N + m;
+                            Xaf[gidx] = Xf[gidx] + x[c];
+                        }
+                    }
                 }
             }
             __syncthreads();
         }
         if (tid == 0) P.status[(int64_t)f * P.ntiles + t] = 0;
-#undef AW
-#undef RW
     }
 }
 
 // Scratch / shared-memory layout chosen on the host.
+static size_t solve_fixed_doubles(const SolveParams &p) {
+    const int Wb = solve_wb(p.bmax), Wr = 8 * (Wb + 1);
+    return 2 * (size_t)Wr * LP_PITCH + 8 * (size_t)p.N + 8 + (((4 * (size_t)Wb * (Wb + 1) * 2 + 7) / 8 + 1) & ~(size_t)1);
+}
+
 int64_t solve_plan_scratch(SolveParams &p, int64_t nmax, size_t smem_limit) {
-    const int64_t Wn = p.bmax + 2, pitch = Wn | 1;
-    const size_t fixed = (size_t)(2 * (p.bmax + 2) + SOLVE_THREADS) * sizeof(double) + 64;
-    const size_t a_bytes = (size_t)(Wn * pitch) * sizeof(double);
-    const size_t r_bytes = (size_t)(Wn * p.N) * sizeof(double);
-    const size_t acc_bytes = (size_t)(SOLVE_THREADS / 32) * (p.bmax + 1) * sizeof(double);
-    p.a_in_smem = fixed + a_bytes <= smem_limit;
-    p.r_in_smem = fixed + (p.a_in_smem ? a_bytes : 0) + r_bytes <= smem_limit;
-    (void)acc_bytes;
+    const int64_t Wb = solve_wb(p.bmax), Wr = 8 * (Wb + 1), pitch = Wr + 2;
+    const int G = SOLVE_THREADS / p.N > 0 ? SOLVE_THREADS / p.N : 1;
+    const size_t fixed = solve_fixed_doubles(p) * sizeof(double) + 64;
+    // the A window doubles as the [G][8][N] reduction buffer of the backward pass
+    const size_t a_doubles = std::max<size_t>((size_t)(Wr * pitch), (size_t)G * 8 * p.N);
+    const size_t r_bytes = (size_t)(Wr * p.N) * sizeof(double);
+    p.a_doubles = (int64_t)a_doubles;
+    p.a_in_smem = fixed + a_doubles * sizeof(double) <= smem_limit;
+    p.r_in_smem = fixed + (p.a_in_smem ? a_doubles * sizeof(double) : 0) + r_bytes <= smem_limit;
     int64_t off = 0;
-    p.off_z = off; off += nmax * p.N;
-    p.off_win_a = off; if (!p.a_in_smem) off += Wn * pitch;
-    p.off_win_r = off; if (!p.r_in_smem) off += Wn * p.N;
+    p.off_z = off; off += ((nmax + 7) / 8 * 8) * p.N;
+    p.off_win_a = off; if (!p.a_in_smem) off += (int64_t)a_doubles;
+    p.off_win_r = off; if (!p.r_in_smem) off += Wr * p.N;
     off = (off + 15) & ~(int64_t)15;
     p.scratch_stride = off;
     return off;
 }
 
 static size_t solve_smem_bytes(const SolveParams &p) {
-    const int64_t Wn = p.bmax + 2, pitch = Wn | 1;
+    const int64_t Wb = solve_wb(p.bmax), Wr = 8 * (Wb + 1), pitch = Wr + 2;
+    const int G = SOLVE_THREADS / p.N > 0 ? SOLVE_THREADS / p.N : 1;
     size_t rest = 0;
-    if (p.a_in_smem) rest += (size_t)(Wn * pitch);
-    if (p.r_in_smem) rest += (size_t)(Wn * p.N);
-    return (size_t)(2 * (p.bmax + 2) + SOLVE_THREADS + rest) * sizeof(double);
+    if (p.a_in_smem) rest += (size_t)p.a_doubles;
+    if (p.r_in_smem) rest += (size_t)(Wr * p.N);
+    (void)G; (void)pitch;
+    return (solve_fixed_doubles(p) + rest) * sizeof(double);
 }
 
 int solve_grid_size(int sm_count, const SolveParams &p, size_t smem_limit) {
@@ -1071,7 +1174,7 @@ cudaError_t launch_assemble_band(const SolveParams &p, int sm_count, cudaStream_
     if (total == 0) return cudaSuccess;
     int64_t grid = (total + ASM_WARPS - 1) / ASM_WARPS;
     if (grid > (int64_t)sm_count * 8) grid = (int64_t)sm_count * 8;
-    const size_t smem = (size_t)ASM_WARPS * (p.bmax + 1) * sizeof(double);
+    const size_t smem = (size_t)ASM_WARPS * 8 * (solve_wb(p.bmax) + 1) * sizeof(double);
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(assemble_band_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;

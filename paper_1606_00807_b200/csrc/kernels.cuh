@@ -40,6 +40,7 @@ struct SolveParams {
     int64_t off_z, off_win_a, off_win_r;  // offsets (doubles) inside a CTA's scratch
     int bmax;                  // largest half-bandwidth
     int a_in_smem, r_in_smem;  // window placement
+    int64_t a_doubles;         // size of the A window / backward reduction buffer
     int32_t *status;           // [nfields * ntiles]
     unsigned int *counter;
     int assemble_only;         // 1: K3a writes T^T D^-1 T without the observation term, for every owned tile

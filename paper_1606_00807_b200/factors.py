@@ -61,15 +61,19 @@ class PrecisionFactors:
         plan = self.plan()
         b = int(plan.get(BANDWIDTH)[0])
         dT, dD = self._device_factors()
-        band = device.empty((self.n, b + 1))
+        wb = (b + 7) // 8
+        wr = 8 * (wb + 1)
+        band = device.empty((self.n, wr))
         _lib.check(_lib.lib().enkfmc_assemble_band(plan.handle, dT.data_ptr(), dD.data_ptr(), 0, band.data_ptr(),
                                                    device.stream_ptr()))
-        band = band.cpu().numpy()                                 # band[I, d] = A[I + d, I], physical order
+        band = band.cpu().numpy()                 # band[I, e] = A[I, 8 (I // 8 - wb) + e]
         out = np.zeros((self.n, self.n))
-        for d in range(b + 1):                                    # layout only, no arithmetic
-            idx = np.arange(self.n - d)
-            out[idx + d, idx] = band[: self.n - d, d]
-            out[idx, idx + d] = band[: self.n - d, d]
+        rows = np.arange(self.n)
+        for e in range(wr):                       # layout only, no arithmetic
+            cols = 8 * (rows // 8 - wb) + e
+            ok = (cols >= 0) & (cols <= rows)
+            out[rows[ok], cols[ok]] = band[rows[ok], e]
+            out[cols[ok], rows[ok]] = band[rows[ok], e]
         return out
 
     def precision_apply(self, v: np.ndarray) -> np.ndarray:
