@@ -248,18 +248,144 @@ __device__ __forceinline__ void qr_step(double *W, int ld, int N, int k, int p, 
     }
 }
 
+// Two Householder steps (k, k+1) in one sweep over the trailing columns: each column is read and
+// written once for two reflectors (halves the shared-memory traffic of the one-step version).
+//   c' = H1 c = c - w1 v1,  w1 = tau1 v1.c ;  c'' = H2 c' = c' - w2 v2,  w2 = tau2 (v2.c - w1 v2.v1)
+template <int S, int S0, int NB>
+__device__ __forceinline__ void qr_apply2(double *Wl, int ld, int jbeg, int jend, const double (&v1)[S],
+                                          const double (&v2)[S], double tau1, double tau2, double g, bool tail_ok,
+                                          int lane) {
+    double *col = Wl + (size_t)jbeg * ld;
+    for (int j0 = jbeg; j0 + NB <= jend; j0 += NB, col += (size_t)NB * ld) {
+        double c[NB][S], d1[NB], d2[NB];
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+            d1[b] = 0.0; d2[b] = 0.0;
+#pragma unroll
+            for (int s = S0; s < S; ++s) {
+                c[b][s] = (s < S - 1 || tail_ok) ? col[(size_t)b * ld + 32 * s] : 0.0;
+                d1[b] += v1[s] * c[b][s];
+                d2[b] += v2[s] * c[b][s];
+            }
+        }
+#pragma unroll
+        for (int b = 0; b < NB; b += 4) {
+            warp_sum4(d1[b], d1[b + 1], d1[b + 2], d1[b + 3], lane);
+            warp_sum4(d2[b], d2[b + 1], d2[b + 2], d2[b + 3], lane);
+        }
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+            const double w1 = d1[b] * tau1;
+            const double w2 = (d2[b] - w1 * g) * tau2;
+#pragma unroll
+            for (int s = S0; s < S; ++s)
+                if (s < S - 1 || tail_ok) col[(size_t)b * ld + 32 * s] = c[b][s] - w1 * v1[s] - w2 * v2[s];
+        }
+    }
+}
+
+template <int S, int S0>
+__device__ __forceinline__ void qr_step2(double *W, int ld, int N, int k, int p, double *rdiag, int lane) {
+    const bool tail_ok = lane + 32 * (S - 1) < N;
+    double *Wl = W + lane;
+    // reflector 1 from column k
+    double v1[S], v2[S], c[S];
+    double ss = 0.0, x0 = 0.0;
+#pragma unroll
+    for (int s = 0; s < S; ++s) { v1[s] = 0.0; v2[s] = 0.0; c[s] = 0.0; }
+    const double *ck = Wl + (size_t)k * ld, *ck1 = Wl + (size_t)(k + 1) * ld;
+    double dc = 0.0;
+#pragma unroll
+    for (int s = S0; s < S; ++s) {
+        const int i = lane + 32 * s;
+        const bool live = (s < S - 1 || tail_ok);
+        v1[s] = (i >= k && live) ? ck[32 * s] : 0.0;
+        c[s] = live ? ck1[32 * s] : 0.0;
+        ss += v1[s] * v1[s];
+        if (i == k) x0 = v1[s];
+        dc += v1[s] * c[s];                       // raw v1 . c, corrected below for the modified v1[k]
+    }
+    double ck_k = 0.0;                            // c at row k
+#pragma unroll
+    for (int s = S0; s < S; ++s) if (lane + 32 * s == k) ck_k = c[s];
+    warp_sum4(ss, x0, dc, ck_k, lane);
+    const double nrm1 = sqrt(ss);
+    const double alpha1 = nrm1 == 0.0 ? 0.0 : ((x0 >= 0.0) ? -nrm1 : nrm1);
+    const double tau1 = nrm1 == 0.0 ? 0.0 : 1.0 / (nrm1 * (nrm1 + fabs(x0)));
+#pragma unroll
+    for (int s = S0; s < S; ++s) if (lane + 32 * s == k) v1[s] = x0 - alpha1;
+    // column k+1 through H1 (v1.c with the final v1[k] = x0 - alpha1: dc - alpha1 * c[k])
+    const double w1c = (dc - alpha1 * ck_k) * tau1;
+    double ss2 = 0.0, y0 = 0.0, graw = 0.0, v1k1 = 0.0;
+#pragma unroll
+    for (int s = S0; s < S; ++s) {
+        const int i = lane + 32 * s;
+        c[s] -= w1c * v1[s];
+        if (i == k) Wl[(size_t)(k + 1) * ld + 32 * s] = c[s];         // R[k][k+1] is final
+        v2[s] = (i >= k + 1) ? c[s] : 0.0;
+        if (s == S - 1 && !tail_ok) v2[s] = 0.0;
+        ss2 += v2[s] * v2[s];
+        graw += v2[s] * v1[s];
+        if (i == k + 1) { y0 = v2[s]; v1k1 = v1[s]; }
+    }
+    warp_sum4(ss2, y0, graw, v1k1, lane);
+    const double nrm2 = sqrt(ss2);
+    const double alpha2 = nrm2 == 0.0 ? 0.0 : ((y0 >= 0.0) ? -nrm2 : nrm2);
+    const double tau2 = nrm2 == 0.0 ? 0.0 : 1.0 / (nrm2 * (nrm2 + fabs(y0)));
+#pragma unroll
+    for (int s = S0; s < S; ++s) if (lane + 32 * s == k + 1) v2[s] = y0 - alpha2;
+    const double g = graw - alpha2 * v1k1;        // v2 . v1 with the final v2[k+1]
+    if (lane == 0) { rdiag[k] = alpha1; rdiag[k + 1] = alpha2; }
+    // remaining columns k+2 .. p
+    const int jend = p + 1;
+    int j = k + 2;
+    const int n8 = (jend - j) & ~7;
+    qr_apply2<S, S0, 8>(Wl, ld, j, j + n8, v1, v2, tau1, tau2, g, tail_ok, lane);
+    j += n8;
+    if (jend - j >= 4) { qr_apply2<S, S0, 4>(Wl, ld, j, j + 4, v1, v2, tau1, tau2, g, tail_ok, lane); j += 4; }
+    if (j < jend) {
+        double cc[4][S], d1[4], d2[4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const double *col = Wl + (size_t)(j + b < jend ? j + b : jend - 1) * ld;
+            d1[b] = 0.0; d2[b] = 0.0;
+#pragma unroll
+            for (int s = S0; s < S; ++s) {
+                cc[b][s] = (s < S - 1 || tail_ok) ? col[32 * s] : 0.0;
+                d1[b] += v1[s] * cc[b][s];
+                d2[b] += v2[s] * cc[b][s];
+            }
+        }
+        warp_sum4(d1[0], d1[1], d1[2], d1[3], lane);
+        warp_sum4(d2[0], d2[1], d2[2], d2[3], lane);
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            if (j + b >= jend) break;
+            double *col = Wl + (size_t)(j + b) * ld;
+            const double w1 = d1[b] * tau1;
+            const double w2 = (d2[b] - w1 * g) * tau2;
+#pragma unroll
+            for (int s = S0; s < S; ++s)
+                if (s < S - 1 || tail_ok) col[32 * s] = cc[b][s] - w1 * v1[s] - w2 * v2[s];
+        }
+    }
+}
+
+// Advances k by the number of reflectors applied (2 while two columns remain, else 1).
 template <int S>
-__device__ __forceinline__ void qr_step_dispatch(double *W, int ld, int N, int k, int p, double *rdiag, int lane) {
+__device__ __forceinline__ int qr_step_dispatch(double *W, int ld, int N, int k, int K, int p, double *rdiag, int lane) {
+    const bool two = k + 1 < K;
     if constexpr (S <= 4) {
         switch (k >> 5) {
-            case 0: qr_step<S, 0>(W, ld, N, k, p, rdiag, lane); break;
-            case 1: if constexpr (S > 1) qr_step<S, 1>(W, ld, N, k, p, rdiag, lane); break;
-            case 2: if constexpr (S > 2) qr_step<S, 2>(W, ld, N, k, p, rdiag, lane); break;
-            default: if constexpr (S > 3) qr_step<S, 3>(W, ld, N, k, p, rdiag, lane); break;
+            case 0: if (two) qr_step2<S, 0>(W, ld, N, k, p, rdiag, lane); else qr_step<S, 0>(W, ld, N, k, p, rdiag, lane); break;
+            case 1: if constexpr (S > 1) { if (two) qr_step2<S, 1>(W, ld, N, k, p, rdiag, lane); else qr_step<S, 1>(W, ld, N, k, p, rdiag, lane); } break;
+            case 2: if constexpr (S > 2) { if (two) qr_step2<S, 2>(W, ld, N, k, p, rdiag, lane); else qr_step<S, 2>(W, ld, N, k, p, rdiag, lane); } break;
+            default: if constexpr (S > 3) { if (two) qr_step2<S, 3>(W, ld, N, k, p, rdiag, lane); else qr_step<S, 3>(W, ld, N, k, p, rdiag, lane); } break;
         }
     } else {
-        qr_step<S, 0>(W, ld, N, k, p, rdiag, lane);
+        if (two) qr_step2<S, 0>(W, ld, N, k, p, rdiag, lane); else qr_step<S, 0>(W, ld, N, k, p, rdiag, lane);
     }
+    return two ? 2 : 1;
 }
 
 // p-vectors live in registers: element e <-> lane e & 31, slot e >> 5 (PS slots).
@@ -473,7 +599,7 @@ __device__ __forceinline__ void unpack_rc(const double *in, double *W, int ld, i
 
 // ---- K2a: load + Householder QR ------------------------------------------------------------
 template <int S>
-__global__ void __launch_bounds__(512, 1) regress_qr_kernel(const RegressParams P) {
+__global__ void __launch_bounds__(256, 1) regress_qr_kernel(const RegressParams P) {
     extern __shared__ double smem[];
     const int lane = threadIdx.x & 31;
     const int N = P.N, ld = P.ld, pmax = P.pmax;
@@ -513,8 +639,8 @@ __global__ void __launch_bounds__(512, 1) regress_qr_kernel(const RegressParams 
         }
         __syncwarp();
         const int K = p < N ? p : N;
-        for (int k = 0; k < K; ++k) {
-            qr_step_dispatch<S>(W, ld, N, k, p, rdiag, lane);
+        for (int k = 0; k < K;) {
+            k += qr_step_dispatch<S>(W, ld, N, k, K, p, rdiag, lane);
             __syncwarp();
         }
         // packed output: R by columns, then c[0:K], then e2
@@ -759,8 +885,11 @@ cudaError_t launch_regress(const RegressParams &p_in, int sm_count, size_t smem_
         const size_t ws = regress_qr_ws_doubles(p.N, p.pmax) * sizeof(double);
         int warps = (int)(smem_limit / ws);
         if (warps < 1) return cudaErrorInvalidConfiguration;
-        if (warps > 16) warps = 16;
-        int64_t grid = sm_count;
+        if (warps > 8) warps = 8;                      // <= 256 threads: the kernel may use up to 255 registers
+        int ctas = (int)(smem_limit / (ws * warps + 1024));
+        if (ctas > 2) ctas = 2;
+        if (ctas < 1) ctas = 1;
+        int64_t grid = (int64_t)sm_count * ctas;
         const int64_t need = (p.nwork + warps - 1) / warps;
         if (grid > need) grid = need;
         const int S = (p.N + 31) / 32;
@@ -813,7 +942,7 @@ cudaError_t launch_regress(const RegressParams &p_in, int sm_count, size_t smem_
 //   and writes Xa = Xb + dx for the interior rows straight into the global analysis
 //   (kernels.py:218, driver.py:116).
 // ------------------------------------------------------------------------------------------
-#define SOLVE_THREADS 256
+#define SOLVE_THREADS 512
 #define ASM_WARPS 8
 #define LP_PITCH 10   // doubles per panel row: 16-byte aligned, conflict-free for 128-bit loads
 
@@ -958,6 +1087,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
         double *Lp = Lp0;
         for (int J = 0; J < nb; ++J) {
             const int sJ = (J % nslot) * 8;
+            const int s1 = ((J + 1) % nslot) * 8;      // window row of panel row r is wrap(s1 + r)
             const int below = (nb - 1 - J < Wb ? nb - 1 - J : Wb) * 8;     // panel rows under the diagonal block
             // (a) 8x8 Cholesky of the diagonal block, warp 0, result in Lp rows 0..7
             if (tid < 32) {
@@ -986,8 +1116,8 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
             if (s_fail) break;
             // (b) panel rows: x L_JJ^T = a ; right-hand sides: L_JJ z = b
             for (int r = tid; r < below; r += nthreads) {
-                const int R = J + 1 + (r >> 3);
-                const double *arow = Aw + (size_t)((R % nslot) * 8 + (r & 7)) * pitch + sJ;
+                int wr = s1 + r; if (wr >= Wr) wr -= Wr;
+                const double *arow = Aw + (size_t)wr * pitch + sJ;
                 double x[8];
 #pragma unroll
                 for (int c = 0; c < 8; ++c) {
@@ -1023,8 +1153,9 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
                 (void)ns_live;
                 const double2 *li2 = reinterpret_cast<const double2 *>(Lp + (8 + r) * LP_PITCH);
                 const double2 l01 = li2[0], l23 = li2[1], l45 = li2[2], l67 = li2[3];
-                const int R = J + 1 + (r >> 3), Q = J + 1 + q;
-                double *arow = Aw + (size_t)((R % nslot) * 8 + (r & 7)) * pitch + (Q % nslot) * 8;
+                int wr = s1 + r; if (wr >= Wr) wr -= Wr;
+                int wc = s1 + 8 * q; if (wc >= Wr) wc -= Wr;
+                double *arow = Aw + (size_t)wr * pitch + wc;
                 double2 *a2 = reinterpret_cast<double2 *>(arow);
                 double acc[8];
                 { const double2 t0 = a2[0], t1 = a2[1], t2 = a2[2], t3 = a2[3];
@@ -1049,8 +1180,8 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
                 for (int r = g_f; r < below; r += G) {
                     const double2 *li2 = reinterpret_cast<const double2 *>(Lp + (8 + r) * LP_PITCH);
                     const double2 l01 = li2[0], l23 = li2[1], l45 = li2[2], l67 = li2[3];
-                    const int R = J + 1 + (r >> 3);
-                    double *bp = Rw + (size_t)((R % nslot) * 8 + (r & 7)) * N + m_f;
+                    int wr = s1 + r; if (wr >= Wr) wr -= Wr;
+                    double *bp = Rw + (size_t)wr * N + m_f;
                     double d = *bp;
                     d = fma(-l01.x, z[0], d); d = fma(-l01.y, z[1], d); d = fma(-l23.x, z[2], d); d = fma(-l23.y, z[3], d);
                     d = fma(-l45.x, z[4], d); d = fma(-l45.y, z[5], d); d = fma(-l67.x, z[6], d); d = fma(-l67.y, z[7], d);
@@ -1079,6 +1210,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
             const double *Lc = Lp0 + (size_t)((nb - 1 - J) & 1) * WrMax * LP_PITCH;
             double *Ln = Lp0 + (size_t)((nb - J) & 1) * WrMax * LP_PITCH;
             const int below = (nb - 1 - J < Wb ? nb - 1 - J : Wb) * 8;
+            const int s1 = ((J + 1) % nslot) * 8;
             if (g_f < G) {
                 double acc[8];
 #pragma unroll
@@ -1086,8 +1218,8 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
                 for (int r = g_f; r < below; r += G) {
                     const double2 *li2 = reinterpret_cast<const double2 *>(Lc + (8 + r) * LP_PITCH);
                     const double2 l01 = li2[0], l23 = li2[1], l45 = li2[2], l67 = li2[3];
-                    const int R = J + 1 + (r >> 3);
-                    const double x = Rw[(size_t)((R % nslot) * 8 + (r & 7)) * N + m_f];
+                    int wr = s1 + r; if (wr >= Wr) wr -= Wr;
+                    const double x = Rw[(size_t)wr * N + m_f];
                     acc[0] = fma(l01.x, x, acc[0]); acc[1] = fma(l01.y, x, acc[1]); acc[2] = fma(l23.x, x, acc[2]);
                     acc[3] = fma(l23.y, x, acc[3]); acc[4] = fma(l45.x, x, acc[4]); acc[5] = fma(l45.y, x, acc[5]);
                     acc[6] = fma(l67.x, x, acc[6]); acc[7] = fma(l67.y, x, acc[7]);
