@@ -739,10 +739,12 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
             power(POWER_ITERS);
             bool refined = false;
             // probes: smallest singular triplets by inverse iteration, deflating truncated ones
+            Vec<PS> zwarm;                   // start of the next probe (see below)
+            bool have_warm = false;
             for (;;) {
                 Vec<PS> z;
 #pragma unroll
-                for (int t = 0; t < PS; ++t) z.v[t] = (lane + 32 * t < p) ? 1.0 : 0.0;
+                for (int t = 0; t < PS; ++t) z.v[t] = have_warm ? zwarm.v[t] : ((lane + 32 * t < p) ? 1.0 : 0.0);
                 for (int mm = 0; mm < m; ++mm) {
                     const Vec<PS> zm = vload<PS>(Zs + mm * pmax, p, lane);
                     const double pr = vdot<PS>(z, zm);
@@ -750,10 +752,22 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
                     for (int t = 0; t < PS; ++t) z.v[t] -= pr * zm.v[t];
                 }
                 {
+                    const double nz0 = vdot<PS>(z, z);
+                    if (!(nz0 > 1e-24)) {        // degenerate start: fall back to the all-ones vector
+#pragma unroll
+                        for (int t = 0; t < PS; ++t) z.v[t] = (lane + 32 * t < p) ? 1.0 : 0.0;
+                        for (int mm = 0; mm < m; ++mm) {
+                            const Vec<PS> zm = vload<PS>(Zs + mm * pmax, p, lane);
+                            const double pr = vdot<PS>(z, zm);
+#pragma unroll
+                            for (int t = 0; t < PS; ++t) z.v[t] -= pr * zm.v[t];
+                        }
+                    }
                     const double inv = 1.0 / sqrt(vdot<PS>(z, z));
 #pragma unroll
                     for (int t = 0; t < PS; ++t) z.v[t] *= inv;
                 }
+                have_warm = false;
                 double s_old = 0.0, dz_old = 1.0, s_est = 0.0;
                 int state = 0;   // 1 = kept, 2 = truncated (vector converged), 3 = undecided bracket
                 for (int it = 0; it < INVIT_MAX && state == 0; ++it) {
@@ -776,9 +790,13 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
                         const double zn = zz.v[t] * inv;
                         const double df = zn - sg * z.v[t];
                         dz += df * df;
+                        // the change of the iterate points along the next singular vector (the slowest
+                        // decaying error component of the power iteration): start the next probe there
+                        if (dz_old > 1e-5) zwarm.v[t] = df;
                         z.v[t] = zn;
                     }
                     dz = sqrt(warp_sum(dz));
+                    if (dz_old > 1e-5) have_warm = true;
                     const double thr_lo = P.rank_tol * smax_lo, thr_hi = P.rank_tol * (refined ? smax_lo : fro);
                     if (s_est < thr_lo) {                       // s_min <= s_est < tol * s_max: truncated for sure
                         if ((dz < 1e-6 && dz > 0.25 * dz_old) || dz < 1e-13) state = 2;
@@ -791,6 +809,7 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
                 if (state == 3 && !refined) {                    // tighten s_max and look again
                     power(POWER_ITERS_REFINE);
                     refined = true;
+                    have_warm = false;
                     continue;
                 }
                 if (state == 0 || state == 3) { fallback = true; break; }   // no gap / too close to call
