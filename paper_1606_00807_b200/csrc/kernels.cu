@@ -121,7 +121,7 @@ cudaError_t launch_center_rows(const double *X, double *U, int64_t nrows, int N,
 //   |y - A^T beta|^2 of estimator.py:60,148 evaluated in the QR basis (orthogonal invariance),
 //   so the predecessor rows are not read a second time.
 // ------------------------------------------------------------------------------------------
-#define REG_MAXDEFL_CAP 4
+#define REG_MAXDEFL_CAP 12
 #define JACOBI_MAX_SWEEPS 30
 #define POWER_ITERS 3
 #define POWER_ITERS_REFINE 24
@@ -132,8 +132,8 @@ __host__ __device__ inline size_t regress_qr_ws_doubles(int N, int pmax) {
     return (d + 1) & ~(size_t)1;
 }
 __host__ __device__ inline size_t regress_solve_ws_doubles(int pmax, int maxdefl) {
-    // R (pitch pmax|1, pmax+1 columns: the last is c) | rinv | aux | tmp | Z[maxdefl] | X[maxdefl]
-    const size_t d = (size_t)(pmax | 1) * (pmax + 1) + (size_t)(3 + 2 * maxdefl) * pmax + 2;
+    // R (pitch pmax|1, pmax+1 columns: the last is c) | rinv | aux | tmp | Z[maxdefl]
+    const size_t d = (size_t)(pmax | 1) * (pmax + 1) + (size_t)(3 + maxdefl) * pmax + 2;
     return (d + 1) & ~(size_t)1;
 }
 size_t regress_warp_workspace_doubles(int N, int pmax) { return regress_qr_ws_doubles(N, pmax); }
@@ -674,8 +674,7 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
     double *rinv = W + (size_t)ld * (pmax + 1);
     double *aux = rinv + pmax;
     double *tmp = aux + pmax;
-    double *Zs = tmp + pmax;                    // deflated right singular vectors
-    double *Xs = Zs + P.maxdefl * pmax;         // deflated left singular vectors
+    double *Zs = tmp + pmax;                    // deflated right singular vectors (x = R z / s is rebuilt on use)
     const double denom = (double)(N - 1);
     const unsigned nf = (unsigned)(P.f1 - P.f0);
 
@@ -715,7 +714,6 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
         const double *cvec = W + (size_t)p * ld;   // Q^T y
         bool fallback = (K < p) || !(dmin > 1e-13 * dmax);
         int m = 0;
-        double dropped2 = 0.0;
 
         if (!fallback) {
             // s_max bracket: power iteration from below, Frobenius norm from above
@@ -738,13 +736,61 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
             };
             power(POWER_ITERS);
             bool refined = false;
+            double smax_hi = fro;            // upper bound of s_max: |R|_F until the power iteration has converged
             // probes: smallest singular triplets by inverse iteration, deflating truncated ones
-            Vec<PS> zwarm;                   // start of the next probe (see below)
-            bool have_warm = false;
-            for (;;) {
-                Vec<PS> z;
+            // Rigorous certificate for "nothing (left) below the threshold": with X = R^-1,
+            // |X|_F^2 = sum_i 1/s_i^2, so after deflating converged triplets s_1..s_m the next singular
+            // value obeys s_next >= (|X|_F^2 - sum_k 1/s_k^2)^(-1/2).  X^T is built in the unused strict
+            // lower triangle of W (lane j owns column j of X), O(p^3/6) like three triangular solves.
+            double tail = 0.0;               // |X|_F^2 minus the deflated 1/s_k^2
+            bool cert_ok = true;             // false once cancellation has eaten the certificate
+            {
+                double xs[PS], rj[PS];       // squared norm of this lane's columns of X; X[j, j]
 #pragma unroll
-                for (int t = 0; t < PS; ++t) z.v[t] = have_warm ? zwarm.v[t] : ((lane + 32 * t < p) ? 1.0 : 0.0);
+                for (int t = 0; t < PS; ++t) { const int j = lane + 32 * t; rj[t] = j < p ? rinv[j] : 0.0; xs[t] = rj[t] * rj[t]; }
+                for (int k = p - 2; k >= 0; --k) {
+                    double acc[PS];
+#pragma unroll
+                    for (int t = 0; t < PS; ++t) acc[t] = 0.0;
+                    const double *rrow = W + k;                              // R[k, i] = rrow[i ld]
+                    for (int i = k + 1; i < p; ++i) {
+                        const double rki = rrow[(size_t)i * ld];
+#pragma unroll
+                        for (int t = 0; t < PS; ++t) {
+                            const int j = lane + 32 * t;
+                            if (j < p && j >= i) acc[t] += rki * (j == i ? rj[t] : W[(size_t)i * ld + j]);   // X[i, j]
+                        }
+                    }
+                    const double rk = rinv[k];
+#pragma unroll
+                    for (int t = 0; t < PS; ++t) {
+                        const int j = lane + 32 * t;
+                        if (j < p && j > k) {
+                            const double x = -rk * acc[t];
+                            W[(size_t)k * ld + j] = x;                       // X[k, j] stored at (row j, column k)
+                            xs[t] += x * x;
+                        }
+                    }
+                    __syncwarp();
+                }
+                double tsum = 0.0;
+#pragma unroll
+                for (int t = 0; t < PS; ++t) tsum += xs[t];
+                tail = warp_sum(tsum);
+            }
+            // One inverse-iteration probe in the complement of the deflated vectors, from a pseudo-random
+            // start.  The estimate bounds the smallest remaining singular value from above; once it is below
+            // rank_tol * lower(s_max) the truncation is proven and the vector is iterated to convergence.
+            // Returns true with the converged pair, false if the estimate stays above the threshold (the
+            // certificate was inconclusive) or the vector does not converge (no gap).
+            auto probe = [&](unsigned seed, Vec<PS> &z) -> bool {
+#pragma unroll
+                for (int t = 0; t < PS; ++t) {
+                    const int e = lane + 32 * t;
+                    unsigned h = (unsigned)(e + 1) * 2654435761u ^ (seed * 40503u + 0x9e3779b9u);
+                    h ^= h >> 15; h *= 2246822519u; h ^= h >> 13; h *= 3266489917u; h ^= h >> 16;
+                    z.v[t] = e < p ? (double)(h >> 8) * (1.0 / 8388608.0) - 1.0 : 0.0;
+                }
                 for (int mm = 0; mm < m; ++mm) {
                     const Vec<PS> zm = vload<PS>(Zs + mm * pmax, p, lane);
                     const double pr = vdot<PS>(z, zm);
@@ -752,25 +798,12 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
                     for (int t = 0; t < PS; ++t) z.v[t] -= pr * zm.v[t];
                 }
                 {
-                    const double nz0 = vdot<PS>(z, z);
-                    if (!(nz0 > 1e-24)) {        // degenerate start: fall back to the all-ones vector
-#pragma unroll
-                        for (int t = 0; t < PS; ++t) z.v[t] = (lane + 32 * t < p) ? 1.0 : 0.0;
-                        for (int mm = 0; mm < m; ++mm) {
-                            const Vec<PS> zm = vload<PS>(Zs + mm * pmax, p, lane);
-                            const double pr = vdot<PS>(z, zm);
-#pragma unroll
-                            for (int t = 0; t < PS; ++t) z.v[t] -= pr * zm.v[t];
-                        }
-                    }
                     const double inv = 1.0 / sqrt(vdot<PS>(z, z));
 #pragma unroll
                     for (int t = 0; t < PS; ++t) z.v[t] *= inv;
                 }
-                have_warm = false;
-                double s_old = 0.0, dz_old = 1.0, s_est = 0.0;
-                int state = 0;   // 1 = kept, 2 = truncated (vector converged), 3 = undecided bracket
-                for (int it = 0; it < INVIT_MAX && state == 0; ++it) {
+                double dz_old = 1.0;
+                for (int it = 0; it < INVIT_MAX; ++it) {
                     Vec<PS> zz = z;
                     solve_upper_t<PS>(zz, W, rinv, ld, p, lane);
                     solve_upper<PS>(zz, W, rinv, ld, p, lane);
@@ -782,7 +815,7 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
                     }
                     const double nz = sqrt(vdot<PS>(zz, zz));
                     const double inv = 1.0 / nz;
-                    s_est = 1.0 / sqrt(nz);
+                    const double s_est = 1.0 / sqrt(nz);
                     const double sg = vdot<PS>(zz, z) >= 0.0 ? 1.0 : -1.0;
                     double dz = 0.0;
 #pragma unroll
@@ -790,51 +823,66 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
                         const double zn = zz.v[t] * inv;
                         const double df = zn - sg * z.v[t];
                         dz += df * df;
-                        // the change of the iterate points along the next singular vector (the slowest
-                        // decaying error component of the power iteration): start the next probe there
-                        if (dz_old > 1e-5) zwarm.v[t] = df;
                         z.v[t] = zn;
                     }
                     dz = sqrt(warp_sum(dz));
-                    if (dz_old > 1e-5) have_warm = true;
-                    const double thr_lo = P.rank_tol * smax_lo, thr_hi = P.rank_tol * (refined ? smax_lo : fro);
-                    if (s_est < thr_lo) {                       // s_min <= s_est < tol * s_max: truncated for sure
-                        if ((dz < 1e-6 && dz > 0.25 * dz_old) || dz < 1e-13) state = 2;
-                    } else if (fabs(s_est - s_old) < 1e-3 * s_est) {
-                        state = (s_est >= 1.05 * thr_hi) ? 1 : 3;
+                    if (s_est < P.rank_tol * smax_lo) {          // s_next <= s_est < tol * s_max: truncated for sure
+                        if ((dz < 1e-6 && dz > 0.9 * dz_old) || dz < 1e-12) return true;    // at the rounding floor
+                    } else if (it >= 12) {
+                        return false;                            // stays above the threshold: cannot certify here
                     }
-                    s_old = s_est;
                     dz_old = dz;
                 }
-                if (state == 3 && !refined) {                    // tighten s_max and look again
-                    power(POWER_ITERS_REFINE);
-                    refined = true;
-                    have_warm = false;
+                return false;
+            };
+            unsigned seed = (unsigned)q * 7919u + (unsigned)f * 104729u;
+            for (;;) {
+                const double lb = cert_ok ? 1.0 / sqrt(fmax(tail, 1e-300)) : 0.0;   // s_next >= lb
+                if (lb >= P.rank_tol * smax_hi * (1.0 + 1e-3)) break;        // nothing (left) to truncate
+                Vec<PS> z;
+                if (probe(seed++, z) && m < P.maxdefl) {
+                    const Vec<PS> rz = mul_upper<PS>(z, W, ld, p, lane);
+                    const double sv = sqrt(vdot<PS>(rz, rz));
+                    if (!(sv < P.rank_tol * smax_lo)) { fallback = true; break; }
+                    vstore<PS>(Zs + m * pmax, z, p, lane);
+                    __syncwarp();
+                    ++m;
+                    // X carries a relative error of about eps * cond; the remainder must stay well above it
+                    const double rest = tail - 1.0 / (sv * sv);
+                    if (!(rest > 1e-12 * (smax_hi / sv) * tail)) cert_ok = false;
+                    tail = rest;
                     continue;
                 }
-                if (state == 0 || state == 3) { fallback = true; break; }   // no gap / too close to call
-                if (state == 1) break;
-                const Vec<PS> rz = mul_upper<PS>(z, W, ld, p, lane);
-                const double s = sqrt(vdot<PS>(rz, rz));
-                if (!(s < P.rank_tol * smax_lo) || m >= P.maxdefl) { fallback = true; break; }
-                const double inv = 1.0 / s;
-                Vec<PS> x;
-#pragma unroll
-                for (int t = 0; t < PS; ++t) x.v[t] = rz.v[t] * inv;
-                vstore<PS>(Zs + m * pmax, z, p, lane);
-                vstore<PS>(Xs + m * pmax, x, p, lane);
-                __syncwarp();
-                ++m;
+                // inconclusive: maybe only because |R|_F overestimates s_max -- tighten it once
+                if (!refined && cert_ok && lb >= P.rank_tol * smax_lo * (1.0 + 1e-3)) {
+                    double prev = smax_lo, inc_old = 0.0;
+                    bool conv = false;
+                    for (int round = 0; round < 25 && !conv; ++round) {
+                        power(8);
+                        const double inc = smax_lo - prev;
+                        prev = smax_lo;
+                        const double qq = inc_old > 0.0 ? inc / inc_old : 1.0;
+                        if (inc <= 1e-9 * smax_lo && qq < 0.9) { conv = true; smax_hi = smax_lo * (1.0 + 1e-6) + 10.0 * inc; }
+                        inc_old = inc;
+                    }
+                    refined = true;
+                    if (conv) continue;
+                }
+                fallback = true;                                             // the Jacobi SVD decides
+                break;
             }
         }
 
         if (!fallback) {
             if (m > 0) flag |= 1 | 2;
             Vec<PS> b = vload<PS>(cvec, p, lane);
-            for (int mm = 0; mm < m; ++mm) {
-                const Vec<PS> xm = vload<PS>(Xs + mm * pmax, p, lane);
+            for (int mm = 0; mm < m; ++mm) {         // c -= x (x.c) with x = R z / |R z|
+                const Vec<PS> zm = vload<PS>(Zs + mm * pmax, p, lane);
+                Vec<PS> xm = mul_upper<PS>(zm, W, ld, p, lane);
+                const double inv = 1.0 / sqrt(vdot<PS>(xm, xm));
+#pragma unroll
+                for (int t = 0; t < PS; ++t) xm.v[t] *= inv;
                 const double pr = vdot<PS>(b, xm);
-                dropped2 += pr * pr;
 #pragma unroll
                 for (int t = 0; t < PS; ++t) b.v[t] -= pr * xm.v[t];
             }
@@ -849,6 +897,9 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
             __syncwarp();
         } else {
             flag |= 1 | 16;
+            unpack_rc(in, W, ld, p, K, lane);      // the lower triangle may hold X^T
+            __syncwarp();
+            double dropped2;
             flag |= jacobi_solve(W, ld, K, p, P.rank_tol, rinv, tmp, aux, &dropped2, lane);
         }
 
@@ -926,10 +977,16 @@ cudaError_t launch_regress(const RegressParams &p_in, int sm_count, size_t smem_
         int warps = (int)(smem_limit / (regress_solve_ws_doubles(p.pmax, 1) * sizeof(double)));
         if (warps < 1) return cudaErrorInvalidConfiguration;
         if (warps > 16) warps = 16;
-        p.maxdefl = 1;   // as many deflation vectors as fit without losing a resident warp
-        while (p.maxdefl < REG_MAXDEFL_CAP &&
-               regress_solve_ws_doubles(p.pmax, p.maxdefl + 1) * sizeof(double) * warps <= smem_limit)
+        // deflation vectors: as many (<= 12) as fit while giving up at most two resident warps
+        const int warps1 = warps;
+        p.maxdefl = 1;
+        while (p.maxdefl < REG_MAXDEFL_CAP) {
+            const int wn = (int)(smem_limit / (regress_solve_ws_doubles(p.pmax, p.maxdefl + 1) * sizeof(double)));
+            if (wn < 1 || wn < std::min(warps1, 16) - 2) break;
             ++p.maxdefl;
+        }
+        warps = (int)(smem_limit / (regress_solve_ws_doubles(p.pmax, p.maxdefl) * sizeof(double)));
+        if (warps > 16) warps = 16;
         const size_t ws = regress_solve_ws_doubles(p.pmax, p.maxdefl) * sizeof(double);
         int64_t grid = sm_count;
         const int64_t need = (p.nwork + warps - 1) / warps;

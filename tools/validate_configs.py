@@ -1,0 +1,85 @@
+"""Parity of the CUDA path against the CPU oracle on the BASELINE.json configurations (GPU box).
+
+For each configuration: index maps bit-exact, T / D / Xa errors against the oracle (all tiles for the
+small configs, a sample of fields for cfg3/cfg5), regression path statistics and stage times.
+Writes a Markdown table to stdout (committed under profiles/)."""
+import argparse
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, __file__.rsplit("/", 2)[0])
+import torch  # noqa: E402
+
+import paper_1606_00807_b200 as mck  # noqa: E402
+from oracle import enkf_mc_oracle as orc  # noqa: E402
+from paper_1606_00807_b200 import device, synthetic  # noqa: E402
+from paper_1606_00807_b200.plan import COL_IDX, LOCAL_ORDER, ROW_PTR, Plan  # noqa: E402
+
+
+def run(name, w, oracle_fields):
+    geo = mck.GridGeometry("grid2d", w.nx, w.ny, boundary=w.boundary, nfields=w.nfields)
+    plan = Plan.decomposed(geo, w.delta, w.zeta)
+    plan.set_observations(w.obs_indices)
+    dX, dR, dYs = device.to_device(w.X), device.to_device(w.r_diag), device.to_device(w.Ys)
+    dXa = torch.empty_like(dX)
+    device.analysis_device(plan, dX, dR, dYs, dXa)
+    torch.cuda.synchronize()
+    plan.profile(True)
+    for _ in range(3):
+        device.analysis_device(plan, dX, dR, dYs, dXa)
+    n, ms = plan.stage_times()
+    ms = ms / n
+    Xa = dXa.cpu().numpy()
+    T = device.workspace_tensor(plan, 1, (plan.nfields, plan.nnz))
+    D = device.workspace_tensor(plan, 2, (plan.nfields, plan.sum_nlocal))
+    flags = device.workspace_tensor(plan, 3, (plan.nfields, plan.sum_nlocal), "i32")
+    grid = orc.Grid(w.nx, w.ny, True, w.boundary == "periodic", w.nfields)
+    t0 = time.perf_counter()
+    ref, kept = orc.assimilate(w.X, w.obs_indices, w.r_diag, w.Ys, grid, w.delta, w.zeta, keep_tiles=True,
+                               fields=oracle_fields)
+    t_cpu = time.perf_counter() - t0
+    maps_ok = np.array_equal(plan.get(LOCAL_ORDER), np.concatenate([r.tile.local_order for r in kept[0]]))
+    maps_ok &= np.array_equal(plan.get(COL_IDX), np.concatenate([r.factors.indices for r in kept[0]]))
+    terr = derr = xerr = 0.0
+    for k, f in enumerate(oracle_fields):
+        tref = np.concatenate([r.factors.data for r in kept[k]])
+        dref = np.concatenate([r.factors.d for r in kept[k]])
+        terr = max(terr, np.linalg.norm(T[f] - tref) / np.linalg.norm(tref))
+        derr = max(derr, np.max(np.abs(D[f] - dref) / dref))
+        sl = slice(f * w.n2d, (f + 1) * w.n2d)
+        xerr = max(xerr, np.linalg.norm(Xa[sl] - ref[sl]) / np.linalg.norm(ref[sl]))
+    fl = plan.work(w.nens)
+    nrow = flags.size
+    print(f"| {name} | {w.nstate} | {w.nens} | {w.zeta} | {'yes' if maps_ok else 'NO'} | {terr:.1e} | {derr:.1e} | {xerr:.1e} | "
+          f"{100 * ((flags & 2) > 0).sum() / nrow:.1f} | {100 * ((flags & 16) > 0).sum() / nrow:.2f} | {100 * ((flags & 8) > 0).sum() / nrow:.1f} | "
+          f"{ms[1]:.2f} | {ms[2]:.2f} | {w.nstate / (ms.sum() * 1e-3) / 1e6:.2f} | {fl[0] / ms[1] / 1e9:.2f} | {fl[1] / ms[2] / 1e9:.2f} | "
+          f"{len(oracle_fields)} field(s), {t_cpu:.1f} s |", flush=True)
+
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--which", default="cfg1,cfg1p,cfg2,cfg2n,cfg4,cfg3,cfg3n,cfg5")
+a = ap.parse_args()
+print("| config | n_state | N | zeta | maps bit-exact | T err (norm-wise) | D err (max rel) | Xa err (norm-wise) | rows truncated % | "
+      "Jacobi fallback % | D at floor % | K2 ms | K3 ms | Mpts/s | K2 TF/s | K3 TF/s | oracle sample |")
+print("|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|")
+for which in a.which.split(","):
+    if which == "cfg1":
+        run("cfg1 clipped", synthetic.config("cfg1"), [0])
+    elif which == "cfg1p":
+        run("cfg1 periodic", synthetic.config("cfg1", boundary="periodic"), [0])
+    elif which == "cfg2":
+        run("cfg2", synthetic.config("cfg2"), [0])
+    elif which == "cfg2n":
+        run("cfg2 + 1% nugget", synthetic.config("cfg2", nugget=0.01), [0])
+    elif which == "cfg4":
+        for z in range(1, 7):
+            run(f"cfg4 r={z}", synthetic.config("cfg4", zeta=z), [0])
+        run("cfg4 r=5 + 1% nugget", synthetic.config("cfg4", zeta=5, nugget=0.01), [0])
+    elif which == "cfg3":
+        run("cfg3 (29 fields)", synthetic.config("cfg3"), [0, 14, 28])
+    elif which == "cfg3n":
+        run("cfg3 + 1% nugget", synthetic.config("cfg3", nugget=0.01), [0, 28])
+    elif which == "cfg5":
+        run("cfg5 (8 of 40 fields)", synthetic.config("cfg5", fields=8), [0])
