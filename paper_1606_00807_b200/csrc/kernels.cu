@@ -749,16 +749,26 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
 #pragma unroll
                 for (int t = 0; t < PS; ++t) { const int j = lane + 32 * t; rj[t] = j < p ? rinv[j] : 0.0; xs[t] = rj[t] * rj[t]; }
                 for (int k = p - 2; k >= 0; --k) {
+                    // x_kj = -(1/r_kk) sum_{i=k+1..j} R[k,i] X[i,j]; the i = j term uses X[j,j] = 1/r_jj
                     double acc[PS];
-#pragma unroll
-                    for (int t = 0; t < PS; ++t) acc[t] = 0.0;
                     const double *rrow = W + k;                              // R[k, i] = rrow[i ld]
-                    for (int i = k + 1; i < p; ++i) {
-                        const double rki = rrow[(size_t)i * ld];
 #pragma unroll
-                        for (int t = 0; t < PS; ++t) {
-                            const int j = lane + 32 * t;
-                            if (j < p && j >= i) acc[t] += rki * (j == i ? rj[t] : W[(size_t)i * ld + j]);   // X[i, j]
+                    for (int t = 0; t < PS; ++t) {
+                        const int j = lane + 32 * t;
+                        acc[t] = (j > k && j < p) ? rrow[(size_t)j * ld] * rj[t] : 0.0;
+                    }
+#pragma unroll
+                    for (int tlo = 0; tlo < PS; ++tlo) {
+                        // i in this 32-block: slot tlo needs j > i, higher slots always qualify
+                        const int ibeg = k + 1 > 32 * tlo ? k + 1 : 32 * tlo;
+                        const int iend = p - 1 < 32 * (tlo + 1) ? p - 1 : 32 * (tlo + 1);
+                        const double *xi = W + (size_t)ibeg * ld + lane;     // X[i, lane + 32 t] = xi[32 t]
+                        for (int i = ibeg; i < iend; ++i, xi += ld) {
+                            const double rki = rrow[(size_t)i * ld];
+                            if (lane + 32 * tlo > i) acc[tlo] += rki * xi[32 * tlo];
+#pragma unroll
+                            for (int t = tlo + 1; t < PS; ++t)
+                                if (lane + 32 * t < p) acc[t] += rki * xi[32 * t];
                         }
                     }
                     const double rk = rinv[k];
