@@ -845,7 +845,7 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
                 }
                 return false;
             };
-            unsigned seed = (unsigned)q * 7919u + (unsigned)f * 104729u;
+            unsigned seed = (unsigned)q * 7919u;   // independent of the field: stacked fields stay bitwise independent
             for (;;) {
                 const double lb = cert_ok ? 1.0 / sqrt(fmax(tail, 1e-300)) : 0.0;   // s_next >= lb
                 if (lb >= P.rank_tol * smax_hi * (1.0 + 1e-3)) break;        // nothing (left) to truncate
