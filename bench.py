@@ -122,7 +122,8 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     from paper_1606_00807_b200 import synthetic
-    w = synthetic.config(args.workload, fields=1 if args.workload in ("cfg3", "cfg5") else None)
+    full_fields = {"cfg3": 29, "cfg5": 40}.get(args.workload)
+    w = synthetic.config(args.workload, fields=1 if full_fields else None)
     cores = os.cpu_count() or 1
     ntiles = cpu_sample_setup(w, 0)
     ctx = mp.get_context("fork")
@@ -137,7 +138,7 @@ def run_reference(args, rank, world):
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(args.workload, w, full_fields=None),
+        "config": workload_config(args.workload, w, full_fields=full_fields),
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
@@ -288,6 +289,11 @@ def run_b200(args, rank, world, local_rank):
             "stage_ms": {"center": stage_ms[0] / max(ncalls, 1), "regress": t_reg * 1e3, "solve": t_sol * 1e3},
             "cpu_baseline": cpu_baseline,
             "e2e": {"value": nstate / t_e2e, "unit": UNIT, "ms_per_step": t_e2e * 1e3,
+                    "breakdown_ms": {"h2d": rep.t_h2d * 1e3, "estimation": float(rep.t_estimation.sum()) * 1e3,
+                                     "analysis": float(rep.t_analysis.sum()) * 1e3, "d2h": rep.t_d2h * 1e3,
+                                     "host_validation_and_python": (rep.t_total - rep.t_h2d - rep.t_d2h
+                                                                    - float(rep.t_estimation.sum())
+                                                                    - float(rep.t_analysis.sum())) * 1e3},
                     "h2d_bytes_per_step": int(w.X.nbytes + w.Ys.nbytes + w.r_diag.nbytes),
                     "d2h_bytes_per_step": int(w.X.nbytes),
                     "api": "assimilate_parallel(EnsembleState, ObservationNetwork, AssimilationConfig, GridGeometry, Ys=)"},

@@ -1324,6 +1324,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
 #pragma unroll
                     for (int c2 = c + 1; c2 < 8; ++c2) s -= Lc[c2 * LP_PITCH + c] * x[c2];
                     x[c] = s / Lc[c * LP_PITCH + c];
+                    if (!(fabs(x[c]) < DBL_MAX)) s_fail = 2;        // non-finite analysis increment (benign race)
                     const int i = 8 * J + c;
                     Rw[(size_t)((J % nslot) * 8 + c) * N + m] = x[c];
                     if (i < n) {
@@ -1337,7 +1338,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
             }
             __syncthreads();
         }
-        if (tid == 0) P.status[(int64_t)f * P.ntiles + t] = 0;
+        if (tid == 0) P.status[(int64_t)f * P.ntiles + t] = s_fail;
     }
 }
 
