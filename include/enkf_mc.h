@@ -122,7 +122,8 @@ int enkfmc_analysis_host(enkfmc_plan *plan, const double *X, const double *r_dia
 
 /* Counters of the last device run: what = 0 kernels launched, 1 regressions on the SVD path,
  * 2 regressions with truncation, 3 rows at the variance floor (filled only when the call
- * collected flags), 4 first failing work item (field*ntiles+tile) or -1. */
+ * collected flags), 4 first failing work item (field*ntiles+tile) or -1, 5 Cholesky pivots clamped at the
+ * rounding level in the last enkfmc_analysis_host call (A is positive semi-definite by construction). */
 int64_t enkfmc_plan_counter(const enkfmc_plan *plan, int what);
 
 /* Device pointers of the plan's workspace after enkfmc_analysis_device/_host:

@@ -263,6 +263,7 @@ int do_solve(enkfmc_plan *p, const double *d_X, const double *d_T, const double 
     int rc2 = ensure_band(p);
     if (rc2) return rc2;
     S.band = d->band;
+    CK(cudaMemsetAsync(d->counters + 3, 0, sizeof(unsigned int), s));   // clamped-pivot counter
     for (int64_t f0 = 0; f0 < p->nfields; f0 += d->band_fields) {
         S.f0 = (int)f0;
         S.f1 = (int)std::min<int64_t>(p->nfields, f0 + d->band_fields);
@@ -450,6 +451,11 @@ extern "C" int enkfmc_analysis_host(enkfmc_plan *p, const double *X, const doubl
             CK(cudaEventElapsedTime(&ms, d->ev[k], d->ev[k + 1]));
             timings_ms[k] = ms;
         }
+    }
+    {
+        unsigned int clamped = 0;
+        CK(cudaMemcpy(&clamped, d->counters + 3, sizeof(unsigned int), cudaMemcpyDeviceToHost));
+        p->counters[5] = clamped;
     }
     // per-tile status -> NumericalError naming the sub-domain
     std::vector<int32_t> st((size_t)(p->ntiles * p->nfields));

@@ -123,8 +123,6 @@ cudaError_t launch_center_rows(const double *X, double *U, int64_t nrows, int N,
 // ------------------------------------------------------------------------------------------
 #define REG_MAXDEFL_CAP 12
 #define JACOBI_MAX_SWEEPS 30
-#define POWER_ITERS 3
-#define POWER_ITERS_REFINE 24
 #define INVIT_MAX 40
 
 __host__ __device__ inline size_t regress_qr_ws_doubles(int N, int pmax) {
@@ -586,13 +584,32 @@ __device__ __forceinline__ int64_t packed_col_offset(int j, int K) {
 }
 
 // Packed block -> dense [R | c] with p rows (rows >= K and the strict lower part are zero).
-__device__ __forceinline__ void unpack_rc(const double *in, double *W, int ld, int p, int K, int lane) {
-    for (int j = 0; j <= p; ++j) {
-        const int h = j < p ? (j + 1 < K ? j + 1 : K) : K;
-        const double *src = in + packed_col_offset(j, K);
-        double *col = W + (size_t)j * ld;
-        for (int i = lane; i < p; i += 32) col[i] = i < h ? src[i] : 0.0;
+__device__ __forceinline__ void unpack_rc(const double *in, double *W, int ld, int p, int K, int lane,
+                                          double *fro2 = nullptr, double *maxcol2 = nullptr) {
+    double f2 = 0.0, mc2 = 0.0;
+    for (int j0 = 0; j0 <= p; j0 += 4) {               // four columns in flight: the loads are latency-bound
+        double v[4][3];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int j = j0 + b <= p ? j0 + b : p;
+            const int h = j < p ? (j + 1 < K ? j + 1 : K) : K;
+            const double *src = in + packed_col_offset(j, K);
+#pragma unroll
+            for (int t = 0; t < 3; ++t) { const int i = lane + 32 * t; v[b][t] = i < h ? src[i] : 0.0; }
+        }
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int j = j0 + b;
+            if (j > p) break;
+            double *col = W + (size_t)j * ld;
+            double c2 = 0.0;
+#pragma unroll
+            for (int t = 0; t < 3; ++t) { const int i = lane + 32 * t; if (i < p) col[i] = v[b][t]; c2 += v[b][t] * v[b][t]; }
+            if (maxcol2 && j < p) { c2 = warp_sum(c2); f2 += c2; mc2 = fmax(mc2, c2); }
+        }
     }
+    if (fro2) *fro2 = f2;
+    if (maxcol2) *maxcol2 = mc2;
 }
 
 }  // namespace
@@ -693,8 +710,8 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
 
         // ---- unpack R | c into the dense workspace, zeros below the diagonal ---------------
         const double *in = P.Rq + (int64_t)fl * P.rq_stride + P.rq_ptr[q];
-        double dmin = DBL_MAX, dmax = 0.0, fro2 = 0.0;
-        unpack_rc(in, W, ld, p, K, lane);
+        double dmin = DBL_MAX, dmax = 0.0, fro2 = 0.0, maxcol2 = 0.0;
+        unpack_rc(in, W, ld, p, K, lane, &fro2, &maxcol2);
         __syncwarp();
         for (int j = lane; j < K; j += 32) {
             const double v = W[(size_t)j * ld + j];
@@ -702,14 +719,10 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
             dmin = fmin(dmin, fabs(v));
             dmax = fmax(dmax, fabs(v));
         }
-        for (int j = 0; j < p; ++j) {
-            const double *col = W + (size_t)j * ld;
-            for (int i = lane; i <= j && i < K; i += 32) fro2 += col[i] * col[i];
-        }
         const double e2 = in[packed_col_offset(p, K) + K];
         dmin = warp_min(dmin);
         dmax = warp_max(dmax);
-        const double fro = sqrt(warp_sum(fro2));
+        const double fro = sqrt(fro2);
         __syncwarp();
         const double *cvec = W + (size_t)p * ld;   // Q^T y
         bool fallback = (K < p) || !(dmin > 1e-13 * dmax);
@@ -720,7 +733,7 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
             Vec<PS> v;
 #pragma unroll
             for (int t = 0; t < PS; ++t) v.v[t] = (lane + 32 * t < p) ? 1.0 : 0.0;
-            double smax_lo = dmax;
+            double smax_lo = fmax(dmax, sqrt(maxcol2));   // |R e_j| <= s_max
             int power_done = 0;
             auto power = [&](int iters) {
                 for (int it = 0; it < iters; ++it) {
@@ -734,7 +747,6 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
                 }
                 power_done += iters;
             };
-            power(POWER_ITERS);
             bool refined = false;
             double smax_hi = fro;            // upper bound of s_max: |R|_F until the power iteration has converged
             // probes: smallest singular triplets by inverse iteration, deflating truncated ones
@@ -863,8 +875,9 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
                     tail = rest;
                     continue;
                 }
-                // inconclusive: maybe only because |R|_F overestimates s_max -- tighten it once
-                if (!refined && cert_ok && lb >= P.rank_tol * smax_lo * (1.0 + 1e-3)) {
+                // inconclusive: maybe only because the bracket [largest column norm, |R|_F] of s_max is wide --
+                // run the power iteration to convergence once and look again
+                if (!refined) {
                     double prev = smax_lo, inc_old = 0.0;
                     bool conv = false;
                     for (int round = 0; round < 25 && !conv; ++round) {
@@ -1171,6 +1184,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
 
         // ---- forward: blocked Cholesky + forward substitution --------------------------------
         double *Lp = Lp0;
+        double pivmax = 0.0;                         // largest pivot so far (warp 0 tracks it redundantly per lane)
         for (int J = 0; J < nb; ++J) {
             const int sJ = (J % nslot) * 8;
             const int s1 = ((J + 1) % nslot) * 8;      // window row of panel row r is wrap(s1 + r)
@@ -1179,8 +1193,16 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
             if (tid < 32) {
                 double *Dg = Aw + (size_t)sJ * pitch + sJ;
                 for (int c = 0; c < 8; ++c) {
-                    const double piv = Dg[(size_t)c * pitch + c];
-                    if (!(piv > 0.0) || !(piv < DBL_MAX)) { if (lane == 0) s_fail = (piv == piv) ? 1 : 2; }
+                    double piv = Dg[(size_t)c * pitch + c];
+                    // A = T~^T D^-1 T~ + H^T R^-1 H is positive semi-definite by construction, so a pivot at
+                    // or below the rounding level of the largest pivot seen is cancellation noise, not
+                    // indefiniteness: clamp it (counted) instead of failing.  NaN / inf still fail.
+                    if (!(piv == piv) || !(fabs(piv) < DBL_MAX)) { if (lane == 0) s_fail = 2; }
+                    else if (!(piv > 1e-13 * pivmax)) {
+                        if (pivmax == 0.0) { if (lane == 0) s_fail = 1; }           // non-positive leading entry
+                        else { piv = 1e-13 * pivmax; if (lane == 0) atomicAdd(P.counter + 1, 1u); }
+                    }
+                    pivmax = fmax(pivmax, piv);
                     const double inv = 1.0 / sqrt(piv);
                     __syncwarp();
                     if (lane > c && lane < 8) Dg[(size_t)lane * pitch + c] *= inv;
@@ -1408,7 +1430,7 @@ cudaError_t launch_local_solve(const SolveParams &p, int grid, size_t smem_limit
     if (smem > smem_limit) return cudaErrorInvalidConfiguration;
     cudaError_t e = cudaFuncSetAttribute(local_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    e = cudaMemsetAsync(p.counter, 0, sizeof(unsigned int), s);
+    e = cudaMemsetAsync(p.counter, 0, sizeof(unsigned int), s);   // p.counter[1] counts clamped pivots (caller zeroes)
     if (e != cudaSuccess) return e;
     local_solve_kernel<<<grid, SOLVE_THREADS, smem, s>>>(p);
     return cudaGetLastError();
