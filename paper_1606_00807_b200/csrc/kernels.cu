@@ -747,6 +747,7 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
                 }
                 power_done += iters;
             };
+            power(2);                        // two steps put the lower bound within a few per cent of s_max
             bool refined = false;
             double smax_hi = fro;            // upper bound of s_max: |R|_F until the power iteration has converged
             // probes: smallest singular triplets by inverse iteration, deflating truncated ones
@@ -880,12 +881,13 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
                 if (!refined) {
                     double prev = smax_lo, inc_old = 0.0;
                     bool conv = false;
-                    for (int round = 0; round < 25 && !conv; ++round) {
-                        power(8);
+                    for (int round = 0; round < 40 && !conv; ++round) {
+                        power(4);
                         const double inc = smax_lo - prev;
                         prev = smax_lo;
+                        // the Rayleigh estimate rises monotonically; with ratio qq per round the tail is inc qq/(1-qq)
                         const double qq = inc_old > 0.0 ? inc / inc_old : 1.0;
-                        if (inc <= 1e-9 * smax_lo && qq < 0.9) { conv = true; smax_hi = smax_lo * (1.0 + 1e-6) + 10.0 * inc; }
+                        if (inc <= 3e-5 * smax_lo && qq < 0.9) { conv = true; smax_hi = smax_lo * (1.0 + 1e-6) + 10.0 * inc; }
                         inc_old = inc;
                     }
                     refined = true;
