@@ -156,6 +156,9 @@ int enkfmc_plan_work(const enkfmc_plan *plan, int64_t nens, double *flops2);
  * (MEASURED_PEAKS.json has no FP64 figure).  Returns TFLOP/s in *tflops. */
 int enkfmc_fp64_peak(double *tflops, void *stream);
 
+/* FP64 tensor-core (mma.sync m8n8k4 f64) peak of the current device, TFLOP/s. */
+int enkfmc_fp64_mma_peak(double *tflops, void *stream);
+
 /* ---- small device helpers behind the remaining reference callables ------------------ */
 
 /* dst[dst_rows[k]][:] = src[src_rows[k]][:]  -- merge_interiors, driver.py:116. */

@@ -406,6 +406,37 @@ extern "C" int enkfmc_fp64_peak(double *tflops, void *stream) {
     return ENKFMC_OK;
 }
 
+extern "C" int enkfmc_fp64_mma_peak(double *tflops, void *stream) {
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, dev));
+    cudaStream_t s = (cudaStream_t)stream;
+    double *out = nullptr;
+    CK(cudaMalloc(&out, sizeof(double)));
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    const int iters = 2048;
+    double best = 0.0;
+    for (int rep = 0; rep < 6; ++rep) {
+        CK(cudaEventRecord(a, s));
+        CK(launch_dmma_peak(out, iters, prop.multiProcessorCount, s));
+        CK(cudaEventRecord(b, s));
+        CK(cudaEventSynchronize(b));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, a, b));
+        // 8 tiles x (8*8*4 FMA) per warp per iteration, 8 warps per block, 8 blocks per SM
+        const double flops = 2.0 * 8.0 * 256.0 * iters * 8.0 * prop.multiProcessorCount * 8.0;
+        if (rep > 0) best = std::max(best, flops / (ms * 1e-3) * 1e-12);
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(out);
+    *tflops = best;
+    return ENKFMC_OK;
+}
+
 extern "C" int enkfmc_analysis_host(enkfmc_plan *p, const double *X, const double *r_diag, const double *Ys,
                                     int64_t nens, double rank_tol, double floor_, double *Xa, double *timings_ms) {
     int rc = check_nens(nens);

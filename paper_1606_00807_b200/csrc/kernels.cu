@@ -1509,6 +1509,28 @@ __global__ void __launch_bounds__(256) fp64_peak_kernel(double *out, int iters, 
     if (s == 123.456) out[0] = s;   // never true; keeps the chains alive
 }
 
+// FP64 tensor-core peak: mma.sync m8n8k4 f64, 8 independent accumulator tiles per warp.
+__global__ void __launch_bounds__(256) dmma_peak_kernel(double *out, int iters, double a, double b) {
+    double c[8][2];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) { c[u][0] = threadIdx.x * 1e-3 + u; c[u][1] = c[u][0] + 0.5; }
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                         : "+d"(c[u][0]), "+d"(c[u][1]) : "d"(a), "d"(b));
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s += c[u][0] + c[u][1];
+    if (s == 123.456) out[0] = s;
+}
+
+cudaError_t launch_dmma_peak(double *out, int iters, int sm_count, cudaStream_t s) {
+    dmma_peak_kernel<<<sm_count * 8, 256, 0, s>>>(out, iters, 0.999999, 1e-7);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_fp64_peak(double *out, int iters, int sm_count, cudaStream_t s) {
     fp64_peak_kernel<<<sm_count * 8, 256, 0, s>>>(out, iters, 0.999999, 1e-7);
     return cudaGetLastError();

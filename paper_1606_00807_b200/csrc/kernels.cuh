@@ -68,3 +68,4 @@ cudaError_t launch_precision_apply(const int64_t *row_ptr, const int32_t *col_id
                                    const int32_t *csc_row, const int64_t *csc_src, const double *T, const double *D,
                                    const double *V, double *Wtmp, double *Out, int64_t n, int64_t ncols, cudaStream_t s);
 cudaError_t launch_fp64_peak(double *out, int iters, int sm_count, cudaStream_t s);
+cudaError_t launch_dmma_peak(double *out, int iters, int sm_count, cudaStream_t s);
