@@ -131,7 +131,7 @@ __host__ __device__ inline size_t regress_qr_ws_doubles(int N, int pmax) {
 }
 __host__ __device__ inline size_t regress_solve_ws_doubles(int pmax, int maxdefl) {
     // R (pitch pmax|1, pmax+1 columns: the last is c) | rinv | aux | tmp | Z[maxdefl]
-    const size_t d = (size_t)(pmax | 1) * (pmax + 1) + (size_t)(3 + maxdefl) * pmax + 2;
+    const size_t d = (size_t)(pmax | 1) * (pmax + 1) + (size_t)(3 + maxdefl) * pmax + 2 + 64;   // + mma staging
     return (d + 1) & ~(size_t)1;
 }
 size_t regress_warp_workspace_doubles(int N, int pmax) { return regress_qr_ws_doubles(N, pmax); }
@@ -496,6 +496,92 @@ __device__ __forceinline__ Vec<PS> mul_upper_t(const Vec<PS> &y, const double *W
     return w;
 }
 
+// ---- tensor-core helpers for the truncation certificate ---------------------------------------
+__device__ __forceinline__ void mma_f64(double &d0, double &d1, double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+        : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+// R[r, c] (upper triangular incl. diagonal, column-major in W) with zero padding beyond p
+__device__ __forceinline__ double r_elem(const double *W, int ld, int p, int r, int c) {
+    return (r <= c && c < p) ? W[(size_t)c * ld + r] : 0.0;
+}
+// X = R^-1: strictly upper part stored transposed in the strict lower triangle of W, diagonal = rinv
+__device__ __forceinline__ double x_elem(const double *W, const double *rinv, int ld, int p, int r, int c) {
+    if (r > c || c >= p) return 0.0;
+    return r == c ? rinv[r] : W[(size_t)r * ld + c];
+}
+
+// |X|_F^2 = sum 1/s_i^2 and |X X^T|_F^2 = sum 1/s_i^4 of X = R^-1, by 8 x 8 blocks on the FP64 tensor
+// cores (mma.sync m8n8k4): X_jj by back-substitution (one lane per column), X_ij = -X_ii sum_k R_ik X_kj.
+// X^T is left in the strict lower triangle of W; stage = 64 doubles of per-warp scratch.
+__device__ void inverse_norms_mma(double *W, const double *rinv, int ld, int p, double *stage, int lane, double *n2,
+                                  double *n4) {
+    const int t4 = lane & 3, m = lane >> 2;
+    const int nbk = (p + 7) >> 3;
+    double f2 = 0.0, g4 = 0.0;
+    for (int j = 0; j < nbk; ++j) {
+        {   // diagonal block: lane c' < 8 owns column c = 8 j + c'
+            const int c = 8 * j + lane;
+            const bool act = lane < 8 && c < p;
+            const double rc = act ? rinv[c] : 0.0;
+            f2 += rc * rc;
+            const int ktop = (8 * j + 7 < p - 1 ? 8 * j + 7 : p - 1) - 1;
+            for (int k = ktop; k >= 8 * j; --k) {
+                if (act && c > k) {
+                    double acc = W[(size_t)c * ld + k] * rc;                        // R[k,c] X[c,c]
+                    for (int i = k + 1; i < c; ++i) acc += W[(size_t)i * ld + k] * W[(size_t)i * ld + c];   // R[k,i] X[i,c]
+                    const double x = -rinv[k] * acc;
+                    W[(size_t)k * ld + c] = x;
+                    f2 += x * x;
+                }
+            }
+        }
+        __syncwarp();
+        for (int i = j - 1; i >= 0; --i) {
+            double s0 = 0.0, s1 = 0.0;
+            for (int k = i + 1; k <= j; ++k) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const double a = r_elem(W, ld, p, 8 * i + m, 8 * k + 4 * h + t4);
+                    const double b = x_elem(W, rinv, ld, p, 8 * k + 4 * h + t4, 8 * j + m);
+                    mma_f64(s0, s1, a, b);
+                }
+            }
+            stage[m * 8 + 2 * t4] = s0;                     // S (8 x 8, row-major) -> B fragments of the next product
+            stage[m * 8 + 2 * t4 + 1] = s1;
+            __syncwarp();
+            double x0 = 0.0, x1 = 0.0;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const double a = x_elem(W, rinv, ld, p, 8 * i + m, 8 * i + 4 * h + t4);
+                mma_f64(x0, x1, a, stage[(4 * h + t4) * 8 + m]);
+            }
+            const int row = 8 * i + m, c0 = 8 * j + 2 * t4;
+            if (c0 < p) W[(size_t)row * ld + c0] = -x0;     // X[row, c0] at (row c0, column row); row < 8 j <= c0
+            if (c0 + 1 < p) W[(size_t)row * ld + c0 + 1] = -x1;
+            f2 += x0 * x0 + x1 * x1;                        // padded entries are exactly zero
+            __syncwarp();
+        }
+    }
+    // H = X X^T by blocks a <= b: H_ab = sum_{c >= b} X_ac X_bc^T ; only its Frobenius norm is needed
+    for (int a = 0; a < nbk; ++a) {
+        for (int b = a; b < nbk; ++b) {
+            double h0 = 0.0, h1 = 0.0;
+            for (int c = b; c < nbk; ++c) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const double av = x_elem(W, rinv, ld, p, 8 * a + m, 8 * c + 4 * h + t4);
+                    const double bv = x_elem(W, rinv, ld, p, 8 * b + m, 8 * c + 4 * h + t4);   // (X_bc^T)[k][n] = X_bc[n][k]
+                    mma_f64(h0, h1, av, bv);
+                }
+            }
+            g4 += (a == b ? 1.0 : 2.0) * (h0 * h0 + h1 * h1);
+        }
+    }
+    *n2 = warp_sum(f2);
+    *n4 = warp_sum(g4);
+}
+
 // General fallback: one-sided Jacobi SVD on the rows of [R | c] (K x (p+1), explicit zeros below
 // the diagonal), truncation as estimator.py:55-57.  Writes beta to out[0..p); returns flag bits and
 // the squared norm of the truncated part of c in *dropped2.
@@ -691,7 +777,8 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
     double *rinv = W + (size_t)ld * (pmax + 1);
     double *aux = rinv + pmax;
     double *tmp = aux + pmax;
-    double *Zs = tmp + pmax;                    // deflated right singular vectors (x = R z / s is rebuilt on use)
+    double *stage = tmp + pmax;                 // 64 doubles of scratch for the tensor-core block products
+    double *Zs = stage + 64;                    // deflated right singular vectors (x = R z / s is rebuilt on use)
     const double denom = (double)(N - 1);
     const unsigned nf = (unsigned)(P.f1 - P.f0);
 
@@ -752,55 +839,13 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
             double smax_hi = fro;            // upper bound of s_max: |R|_F until the power iteration has converged
             // probes: smallest singular triplets by inverse iteration, deflating truncated ones
             // Rigorous certificate for "nothing (left) below the threshold": with X = R^-1,
-            // |X|_F^2 = sum_i 1/s_i^2, so after deflating converged triplets s_1..s_m the next singular
-            // value obeys s_next >= (|X|_F^2 - sum_k 1/s_k^2)^(-1/2).  X^T is built in the unused strict
-            // lower triangle of W (lane j owns column j of X), O(p^3/6) like three triangular solves.
-            double tail = 0.0;               // |X|_F^2 minus the deflated 1/s_k^2
-            bool cert_ok = true;             // false once cancellation has eaten the certificate
-            {
-                double xs[PS], rj[PS];       // squared norm of this lane's columns of X; X[j, j]
-#pragma unroll
-                for (int t = 0; t < PS; ++t) { const int j = lane + 32 * t; rj[t] = j < p ? rinv[j] : 0.0; xs[t] = rj[t] * rj[t]; }
-                for (int k = p - 2; k >= 0; --k) {
-                    // x_kj = -(1/r_kk) sum_{i=k+1..j} R[k,i] X[i,j]; the i = j term uses X[j,j] = 1/r_jj
-                    double acc[PS];
-                    const double *rrow = W + k;                              // R[k, i] = rrow[i ld]
-#pragma unroll
-                    for (int t = 0; t < PS; ++t) {
-                        const int j = lane + 32 * t;
-                        acc[t] = (j > k && j < p) ? rrow[(size_t)j * ld] * rj[t] : 0.0;
-                    }
-#pragma unroll
-                    for (int tlo = 0; tlo < PS; ++tlo) {
-                        // i in this 32-block: slot tlo needs j > i, higher slots always qualify
-                        const int ibeg = k + 1 > 32 * tlo ? k + 1 : 32 * tlo;
-                        const int iend = p - 1 < 32 * (tlo + 1) ? p - 1 : 32 * (tlo + 1);
-                        const double *xi = W + (size_t)ibeg * ld + lane;     // X[i, lane + 32 t] = xi[32 t]
-                        for (int i = ibeg; i < iend; ++i, xi += ld) {
-                            const double rki = rrow[(size_t)i * ld];
-                            if (lane + 32 * tlo > i) acc[tlo] += rki * xi[32 * tlo];
-#pragma unroll
-                            for (int t = tlo + 1; t < PS; ++t)
-                                if (lane + 32 * t < p) acc[t] += rki * xi[32 * t];
-                        }
-                    }
-                    const double rk = rinv[k];
-#pragma unroll
-                    for (int t = 0; t < PS; ++t) {
-                        const int j = lane + 32 * t;
-                        if (j < p && j > k) {
-                            const double x = -rk * acc[t];
-                            W[(size_t)k * ld + j] = x;                       // X[k, j] stored at (row j, column k)
-                            xs[t] += x * x;
-                        }
-                    }
-                    __syncwarp();
-                }
-                double tsum = 0.0;
-#pragma unroll
-                for (int t = 0; t < PS; ++t) tsum += xs[t];
-                tail = warp_sum(tsum);
-            }
+            // |X|_F^2 = sum_i 1/s_i^2 and |X X^T|_F^2 = sum_i 1/s_i^4, so after deflating converged triplets
+            // s_1..s_m the next singular value obeys
+            //     s_next >= max( (sum_2 - sum_k 1/s_k^2)^(-1/2), (sum_4 - sum_k 1/s_k^4)^(-1/4) ).
+            // The fourth-power bound is within a few per cent of s_next even for clustered spectra.
+            double tail2 = 0.0, tail4 = 0.0; // sum 1/s^2 and sum 1/s^4 over the singular values not yet deflated
+            bool ok2 = true, ok4 = true;     // false once cancellation has eaten the respective certificate
+            inverse_norms_mma(W, rinv, ld, p, stage, lane, &tail2, &tail4);
             // One inverse-iteration probe in the complement of the deflated vectors, from a pseudo-random
             // start.  The estimate bounds the smallest remaining singular value from above; once it is below
             // rank_tol * lower(s_max) the truncation is proven and the vector is iterated to convergence.
@@ -860,7 +905,8 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
             };
             unsigned seed = (unsigned)q * 7919u;   // independent of the field: stacked fields stay bitwise independent
             for (;;) {
-                const double lb = cert_ok ? 1.0 / sqrt(fmax(tail, 1e-300)) : 0.0;   // s_next >= lb
+                const double lb = fmax(ok2 ? 1.0 / sqrt(fmax(tail2, 1e-300)) : 0.0,
+                                       ok4 ? 1.0 / sqrt(sqrt(fmax(tail4, 1e-300))) : 0.0);   // s_next >= lb
                 if (lb >= P.rank_tol * smax_hi * (1.0 + 1e-3)) break;        // nothing (left) to truncate
                 Vec<PS> z;
                 if (probe(seed++, z) && m < P.maxdefl) {
@@ -870,10 +916,14 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
                     vstore<PS>(Zs + m * pmax, z, p, lane);
                     __syncwarp();
                     ++m;
-                    // X carries a relative error of about eps * cond; the remainder must stay well above it
-                    const double rest = tail - 1.0 / (sv * sv);
-                    if (!(rest > 1e-12 * (smax_hi / sv) * tail)) cert_ok = false;
-                    tail = rest;
+                    const double i2 = 1.0 / (sv * sv);
+                    const double rest2 = tail2 - i2, rest4 = tail4 - i2 * i2;
+                    // X carries a relative error of about eps * cond(R); what is left must stay well above it
+                    const double noise = 2.2e-14 * (smax_hi / sv);
+                    if (!(rest2 > noise * tail2)) ok2 = false;
+                    if (!(rest4 > 4.0 * noise * tail4)) ok4 = false;
+                    tail2 = rest2;
+                    tail4 = rest4;
                     continue;
                 }
                 // inconclusive: maybe only because the bracket [largest column norm, |R|_F] of s_max is wide --
