@@ -813,7 +813,7 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
         __syncwarp();
         const double *cvec = W + (size_t)p * ld;   // Q^T y
         bool fallback = (K < p) || !(dmin > 1e-13 * dmax);
-        int m = 0;
+        int m = 0, why = fallback ? 1 : 0;   // fallback reason, reported in flag bits 5-7
 
         if (!fallback) {
             // s_max bracket: power iteration from below, Frobenius norm from above
@@ -909,10 +909,12 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
                                        ok4 ? 1.0 / sqrt(sqrt(fmax(tail4, 1e-300))) : 0.0);   // s_next >= lb
                 if (lb >= P.rank_tol * smax_hi * (1.0 + 1e-3)) break;        // nothing (left) to truncate
                 Vec<PS> z;
-                if (probe(seed++, z) && m < P.maxdefl) {
+                const bool found = probe(seed++, z);
+                if (found && m >= P.maxdefl) { fallback = true; why = 3; break; }
+                if (found) {
                     const Vec<PS> rz = mul_upper<PS>(z, W, ld, p, lane);
                     const double sv = sqrt(vdot<PS>(rz, rz));
-                    if (!(sv < P.rank_tol * smax_lo)) { fallback = true; break; }
+                    if (!(sv < P.rank_tol * smax_lo)) { fallback = true; why = 4; break; }
                     vstore<PS>(Zs + m * pmax, z, p, lane);
                     __syncwarp();
                     ++m;
@@ -944,6 +946,7 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
                     if (conv) continue;
                 }
                 fallback = true;                                             // the Jacobi SVD decides
+                why = (ok2 || ok4) ? 2 : 5;                                  // 2: certificate alive but inconclusive, 5: lost to cancellation
                 break;
             }
         }
@@ -971,7 +974,7 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
             vstore<PS>(aux, b, p, lane);
             __syncwarp();
         } else {
-            flag |= 1 | 16;
+            flag |= 1 | 16 | (why << 5);
             unpack_rc(in, W, ld, p, K, lane);      // the lower triangle may hold X^T
             __syncwarp();
             double dropped2;
