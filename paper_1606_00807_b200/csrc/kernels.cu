@@ -130,8 +130,8 @@ __host__ __device__ inline size_t regress_qr_ws_doubles(int N, int pmax) {
     return (d + 1) & ~(size_t)1;
 }
 __host__ __device__ inline size_t regress_solve_ws_doubles(int pmax, int maxdefl) {
-    // R (pitch pmax|1, pmax+1 columns: the last is c) | rinv | aux | tmp | Z[maxdefl]
-    const size_t d = (size_t)(pmax | 1) * (pmax + 1) + (size_t)(3 + maxdefl) * pmax + 2 + 64;   // + mma staging
+    // R (pitch pmax|1, pmax+1 columns: the last is c) | rinv | aux | tmp | mma staging | Z[maxdefl] | W[maxdefl] | G
+    const size_t d = (size_t)(pmax | 1) * (pmax + 1) + (size_t)(3 + 2 * maxdefl) * pmax + (size_t)maxdefl * maxdefl + 2 + 64;
     return (d + 1) & ~(size_t)1;
 }
 size_t regress_warp_workspace_doubles(int N, int pmax) { return regress_qr_ws_doubles(N, pmax); }
@@ -779,6 +779,8 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
     double *tmp = aux + pmax;
     double *stage = tmp + pmax;                 // 64 doubles of scratch for the tensor-core block products
     double *Zs = stage + 64;                    // deflated right singular vectors (x = R z / s is rebuilt on use)
+    double *Ws = Zs + P.maxdefl * pmax;         // M Z during the block polish
+    double *Gs = Ws + P.maxdefl * pmax;         // Z^T M Z
     const double denom = (double)(N - 1);
     const unsigned nf = (unsigned)(P.f1 - P.f0);
 
@@ -851,7 +853,7 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
             // rank_tol * lower(s_max) the truncation is proven and the vector is iterated to convergence.
             // Returns true with the converged pair, false if the estimate stays above the threshold (the
             // certificate was inconclusive) or the vector does not converge (no gap).
-            auto probe = [&](unsigned seed, Vec<PS> &z) -> bool {
+            auto probe = [&](unsigned seed, Vec<PS> &z, double &zMz, double &Mz2) -> int {
 #pragma unroll
                 for (int t = 0; t < PS; ++t) {
                     const int e = lane + 32 * t;
@@ -882,9 +884,11 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
                         for (int t = 0; t < PS; ++t) zz.v[t] -= pr * zm.v[t];
                     }
                     const double nz = sqrt(vdot<PS>(zz, zz));
+                    zMz = vdot<PS>(zz, z);                         // z^T M z and |M z|^2 of the previous iterate
+                    Mz2 = nz * nz;
                     const double inv = 1.0 / nz;
                     const double s_est = 1.0 / sqrt(nz);
-                    const double sg = vdot<PS>(zz, z) >= 0.0 ? 1.0 : -1.0;
+                    const double sg = zMz >= 0.0 ? 1.0 : -1.0;
                     double dz = 0.0;
 #pragma unroll
                     for (int t = 0; t < PS; ++t) {
@@ -895,22 +899,118 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
                     }
                     dz = sqrt(warp_sum(dz));
                     if (s_est < P.rank_tol * smax_lo) {          // s_next <= s_est < tol * s_max: truncated for sure
-                        if ((dz < 1e-6 && dz > 0.9 * dz_old) || dz < 1e-12) return true;    // at the rounding floor
+                        if ((dz < 1e-6 && dz > 0.9 * dz_old) || dz < 1e-12) return 2;      // at the rounding floor
+                        // slow phase: what still moves is a rotation among close sub-threshold directions --
+                        // hand the vector to the block polish
+                        if (it >= 6 && dz < 1e-2 && dz > 0.4 * dz_old && dz < 0.95 * dz_old) return 1;
                     } else if (it >= 12) {
-                        return false;                            // stays above the threshold: cannot certify here
+                        return 0;                                // stays above the threshold: cannot certify here
                     }
                     dz_old = dz;
                 }
-                return false;
+                return 0;
             };
+            // Block polish of the deflated vectors Z (m columns): subspace iteration Z <- orth(M Z), M = (R^T R)^-1,
+            // until the invariance residual |M Z - Z (Z^T M Z)|_F / |M Z|_F is at the rounding floor.  Returns the
+            // exact deflated sums tr(Z^T M Z), |M Z|_F^2 and checks that every singular value inside span(Z) is
+            // below the threshold (Cholesky test of Z^T M Z - mu I).  0 ok, 1 not converged, 2 a kept direction
+            // (or a near-threshold value) sits in the block.
+            auto polish = [&](double &sum2, double &sum4) -> int {
+                double res_old = 1e300;
+                bool conv = false;
+                for (int round = 0; round < 8 && !conv; ++round) {
+                    double w2 = 0.0, res2 = 0.0;
+                    for (int k = 0; k < m; ++k) {
+                        Vec<PS> w = vload<PS>(Zs + k * pmax, p, lane);
+                        solve_upper_t<PS>(w, W, rinv, ld, p, lane);
+                        solve_upper<PS>(w, W, rinv, ld, p, lane);
+                        vstore<PS>(Ws + k * pmax, w, p, lane);
+                        w2 += vdot<PS>(w, w);
+                    }
+                    __syncwarp();
+                    for (int k = 0; k < m; ++k) {
+                        Vec<PS> r = vload<PS>(Ws + k * pmax, p, lane);
+                        const Vec<PS> w = r;
+                        for (int l = 0; l < m; ++l) {
+                            const Vec<PS> zl = vload<PS>(Zs + l * pmax, p, lane);
+                            const double g = vdot<PS>(zl, w);
+                            if (lane == 0) Gs[l * m + k] = g;
+#pragma unroll
+                            for (int t = 0; t < PS; ++t) r.v[t] -= g * zl.v[t];
+                        }
+                        res2 += vdot<PS>(r, r);
+                    }
+                    __syncwarp();
+                    const double res = sqrt(res2 / w2);
+                    sum4 = w2;
+                    conv = (res < 1e-7 && res > 0.9 * res_old) || res < 1e-11;   // at the rounding floor, not merely slow
+                    res_old = res;
+                    if (conv) break;
+                    for (int k = 0; k < m; ++k) {              // Z <- orth(W), modified Gram-Schmidt
+                        Vec<PS> w = vload<PS>(Ws + k * pmax, p, lane);
+                        for (int l = 0; l < k; ++l) {
+                            const Vec<PS> zl = vload<PS>(Zs + l * pmax, p, lane);
+                            const double g = vdot<PS>(zl, w);
+#pragma unroll
+                            for (int t = 0; t < PS; ++t) w.v[t] -= g * zl.v[t];
+                        }
+                        const double inv = 1.0 / sqrt(vdot<PS>(w, w));
+#pragma unroll
+                        for (int t = 0; t < PS; ++t) w.v[t] *= inv;
+                        vstore<PS>(Zs + k * pmax, w, p, lane);
+                        __syncwarp();
+                    }
+                }
+                if (!conv) return 1;
+                sum2 = 0.0;
+                for (int k = 0; k < m; ++k) sum2 += Gs[k * m + k];
+                // all singular values inside span(Z) below the threshold  <=>  G - mu I positive definite
+                int bad = 0;
+                if (lane == 0) {
+                    const double thr = P.rank_tol * smax_lo * (1.0 - 1e-3);
+                    const double mu = 1.0 / (thr * thr);
+                    for (int a = 0; a < m && !bad; ++a) {
+                        for (int b = 0; b <= a; ++b) {
+                            double v = 0.5 * (Gs[a * m + b] + Gs[b * m + a]) - (a == b ? mu : 0.0);
+                            for (int c = 0; c < b; ++c) v -= Gs[a * m + c] * Gs[b * m + c];   // lower factor overwrites G
+                            if (a == b) { if (!(v > 0.0)) { bad = 1; break; } Gs[a * m + a] = sqrt(v); }
+                            else Gs[a * m + b] = v / Gs[b * m + b];
+                        }
+                    }
+                }
+                bad = __shfl_sync(FULL, bad, 0);
+                return bad ? 2 : 0;
+            };
+
             unsigned seed = (unsigned)q * 7919u;   // independent of the field: stacked fields stay bitwise independent
+            const double T2 = tail2, T4 = tail4;   // totals over all singular values
+            double def2 = 0.0, def4 = 0.0;         // part carried by the deflated block
+            double smin_defl = smax_lo;            // smallest deflated singular value (cancellation guard)
+            bool polished = true;                  // the block spans an invariant subspace to rounding
             for (;;) {
-                const double lb = fmax(ok2 ? 1.0 / sqrt(fmax(tail2, 1e-300)) : 0.0,
-                                       ok4 ? 1.0 / sqrt(sqrt(fmax(tail4, 1e-300))) : 0.0);   // s_next >= lb
-                if (lb >= P.rank_tol * smax_hi * (1.0 + 1e-3)) break;        // nothing (left) to truncate
+                // X carries a relative error of about eps * cond(R); what is left must stay well above it
+                // X carries a relative error of at most about c eps cond(R); add it to what is left, so the bound
+                // stays a lower bound (it merely becomes useless once cancellation has eaten the sums)
+                tail2 = T2 - def2;
+                tail4 = T4 - def4;
+                const double noise = 2.2e-14 * (smax_hi / smin_defl);
+                const double up2 = fmax(tail2, 0.0) + noise * T2, up4 = fmax(tail4, 0.0) + 4.0 * noise * T4;
+                ok2 = tail2 > -noise * T2;                                   // a clearly negative remainder: inconsistent sums
+                ok4 = tail4 > -4.0 * noise * T4;
+                const double lb = fmax(ok2 ? 1.0 / sqrt(up2) : 0.0, ok4 ? 1.0 / sqrt(sqrt(up4)) : 0.0);   // s_next >= lb
+                const bool done = lb >= P.rank_tol * smax_hi * (1.0 + 1e-3);
+                if (done && polished) break;                                 // nothing (left) to truncate
+                if (done || (!polished && m >= P.maxdefl)) {                 // verify / sharpen the block first
+                    const int pr = polish(def2, def4);
+                    if (pr) { fallback = true; why = 5 + pr; break; }
+                    polished = true;
+                    if (!done && m >= P.maxdefl) { fallback = true; why = 3; break; }
+                    continue;
+                }
+                if (m >= P.maxdefl) { fallback = true; why = 3; break; }
                 Vec<PS> z;
-                const bool found = probe(seed++, z);
-                if (found && m >= P.maxdefl) { fallback = true; why = 3; break; }
+                double zMz, Mz2;
+                const int found = probe(seed++, z, zMz, Mz2);
                 if (found) {
                     const Vec<PS> rz = mul_upper<PS>(z, W, ld, p, lane);
                     const double sv = sqrt(vdot<PS>(rz, rz));
@@ -918,17 +1018,21 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
                     vstore<PS>(Zs + m * pmax, z, p, lane);
                     __syncwarp();
                     ++m;
-                    const double i2 = 1.0 / (sv * sv);
-                    const double rest2 = tail2 - i2, rest4 = tail4 - i2 * i2;
-                    // X carries a relative error of about eps * cond(R); what is left must stay well above it
-                    const double noise = 2.2e-14 * (smax_hi / sv);
-                    if (!(rest2 > noise * tail2)) ok2 = false;
-                    if (!(rest4 > 4.0 * noise * tail4)) ok4 = false;
-                    tail2 = rest2;
-                    tail4 = rest4;
+                    smin_defl = fmin(smin_defl, sv);
+                    // triangular solves lose eps * cond digits: beyond cond ~ 5e9 the deflated subspace would be less
+                    // accurate than the reference's SVD -- let the Jacobi SVD handle those rows
+                    if (smax_hi > 5e9 * smin_defl) { fallback = true; why = 5; break; }
+                    if (found == 2 && polished) { const double i2 = 1.0 / (sv * sv); def2 += i2; def4 += i2 * i2; }
+                    else { def2 += zMz; def4 += Mz2; polished = false; }
                     continue;
                 }
-                // inconclusive: maybe only because the bracket [largest column norm, |R|_F] of s_max is wide --
+                if (!polished) {                                             // a loose block can hide what is left
+                    const int pr = polish(def2, def4);
+                    if (pr) { fallback = true; why = 5 + pr; break; }
+                    polished = true;
+                    continue;
+                }
+                // inconclusive: maybe only because the bracket [lower bound, |R|_F] of s_max is wide --
                 // run the power iteration to convergence once and look again
                 if (!refined) {
                     double prev = smax_lo, inc_old = 0.0;
@@ -953,13 +1057,25 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
 
         if (!fallback) {
             if (m > 0) flag |= 1 | 2;
-            Vec<PS> b = vload<PS>(cvec, p, lane);
-            for (int mm = 0; mm < m; ++mm) {         // c -= x (x.c) with x = R z / |R z|
+            // left singular subspace of the truncated values: orthonormal basis of R Z (Z spans the right one)
+            for (int mm = 0; mm < m; ++mm) {
                 const Vec<PS> zm = vload<PS>(Zs + mm * pmax, p, lane);
                 Vec<PS> xm = mul_upper<PS>(zm, W, ld, p, lane);
+                for (int l = 0; l < mm; ++l) {
+                    const Vec<PS> xl = vload<PS>(Ws + l * pmax, p, lane);
+                    const double g = vdot<PS>(xl, xm);
+#pragma unroll
+                    for (int t = 0; t < PS; ++t) xm.v[t] -= g * xl.v[t];
+                }
                 const double inv = 1.0 / sqrt(vdot<PS>(xm, xm));
 #pragma unroll
                 for (int t = 0; t < PS; ++t) xm.v[t] *= inv;
+                vstore<PS>(Ws + mm * pmax, xm, p, lane);
+                __syncwarp();
+            }
+            Vec<PS> b = vload<PS>(cvec, p, lane);
+            for (int mm = 0; mm < m; ++mm) {         // c -= X X^T c
+                const Vec<PS> xm = vload<PS>(Ws + mm * pmax, p, lane);
                 const double pr = vdot<PS>(b, xm);
 #pragma unroll
                 for (int t = 0; t < PS; ++t) b.v[t] -= pr * xm.v[t];
