@@ -142,9 +142,10 @@ int enkfmc_plan_set_tile_range(enkfmc_plan *plan, int64_t tile_begin, int64_t ti
 
 /* Per-stage CUDA-event timing of enkfmc_analysis_device on its launching stream.
  * enable != 0 starts recording (and clears the log); stage_times synchronises and returns the
- * number of recorded calls and the SUMMED milliseconds of K0 centre, K2 regress, K3 solve. */
+ * number of recorded calls and the SUMMED milliseconds of ms4 = {K0 centre, K2a QR, K2b probe/solve,
+ * K3 assemble + local solve} (with field chunking the K2a/K2b split is that of the last chunk). */
 int enkfmc_plan_profile(enkfmc_plan *plan, int enable);
-int enkfmc_plan_stage_times(enkfmc_plan *plan, int64_t *ncalls, double *ms3);
+int enkfmc_plan_stage_times(enkfmc_plan *plan, int64_t *ncalls, double *ms4);
 
 /* Algorithmic work of one analysis with the current tile range (SURVEY 8d definitions):
  * flops2[0] = sum over owned local rows of 2*N*p^2 - (2/3)*p^3 + 4*N*p (Householder-QR least squares),

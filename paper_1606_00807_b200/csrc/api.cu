@@ -205,7 +205,7 @@ int ensure_workspace(enkfmc_plan *p, int64_t nens) {
 }
 
 int do_regress(enkfmc_plan *p, const double *d_U, int64_t nens, double rank_tol, double floor_, double *d_T,
-               double *d_D, int32_t *d_flags, cudaStream_t s) {
+               double *d_D, int32_t *d_flags, cudaStream_t s, cudaEvent_t mid = nullptr) {
     DeviceState *d = p->dev;
     int rc0 = ensure_orders(p);
     if (rc0) return rc0;
@@ -231,7 +231,7 @@ int do_regress(enkfmc_plan *p, const double *d_U, int64_t nens, double rank_tol,
         R.f1 = (int)std::min<int64_t>(p->nfields, f0 + chunk);
         R.nwork = (int64_t)p->work_order.size() * (R.f1 - R.f0);
         if (R.nwork > 0xfffffff0LL) { enkfmc_set_error("too many regressions for one launch"); return ENKFMC_E_CAPACITY; }
-        cudaError_t e = launch_regress(R, d->sm_count, d->smem_limit, s);
+        cudaError_t e = launch_regress(R, d->sm_count, d->smem_limit, s, mid);
         if (e == cudaErrorInvalidConfiguration) {
             enkfmc_set_error("regression workspace (nens=" + std::to_string(nens) + ", predecessors=" +
                              std::to_string(p->max_pred) + ") exceeds shared memory or the 96-predecessor cap");
@@ -334,22 +334,22 @@ extern "C" int enkfmc_analysis_device(enkfmc_plan *p, const double *d_X, const d
     cudaStream_t s = (cudaStream_t)stream;
     cudaEvent_t *ev = nullptr;
     if (p->profile) {
-        while (d->prof.size() < d->prof_used + 4) {
+        while (d->prof.size() < d->prof_used + 5) {
             cudaEvent_t e;
             CK(cudaEventCreate(&e));
             d->prof.push_back(e);
         }
         ev = d->prof.data() + d->prof_used;
-        d->prof_used += 4;
+        d->prof_used += 5;
         CK(cudaEventRecord(ev[0], s));
     }
     CK(launch_center_rows(d_X, d->U, p->nstate2d * p->nfields, (int)nens, s));
     p->counters[0] += 1;
     if (ev) CK(cudaEventRecord(ev[1], s));
-    if ((rc = do_regress(p, d->U, nens, rank_tol, floor_, d->T, d->D, d->flags, s))) return rc;
-    if (ev) CK(cudaEventRecord(ev[2], s));
-    rc = do_solve(p, d_X, d->T, d->D, d_r, d_Ys, nens, d_Xa, d->status, s);
+    if ((rc = do_regress(p, d->U, nens, rank_tol, floor_, d->T, d->D, d->flags, s, ev ? ev[2] : nullptr))) return rc;
     if (ev) CK(cudaEventRecord(ev[3], s));
+    rc = do_solve(p, d_X, d->T, d->D, d_r, d_Ys, nens, d_Xa, d->status, s);
+    if (ev) CK(cudaEventRecord(ev[4], s));
     return rc;
 }
 
@@ -360,13 +360,13 @@ extern "C" int enkfmc_plan_profile(enkfmc_plan *p, int enable) {
 }
 
 extern "C" int enkfmc_plan_stage_times(enkfmc_plan *p, int64_t *ncalls, double *ms3) {
-    ms3[0] = ms3[1] = ms3[2] = 0.0;
+    ms3[0] = ms3[1] = ms3[2] = ms3[3] = 0.0;
     *ncalls = 0;
     if (!p->dev) return ENKFMC_OK;
     DeviceState *d = p->dev;
     CK(cudaDeviceSynchronize());
-    for (size_t k = 0; k + 4 <= d->prof_used; k += 4) {
-        for (int st = 0; st < 3; ++st) {
+    for (size_t k = 0; k + 5 <= d->prof_used; k += 5) {
+        for (int st = 0; st < 4; ++st) {
             float ms = 0.f;
             CK(cudaEventElapsedTime(&ms, d->prof[k + st], d->prof[k + st + 1]));
             ms3[st] += ms;

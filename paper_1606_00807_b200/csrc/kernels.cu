@@ -1138,7 +1138,7 @@ static cudaError_t launch_solve_t(const RegressParams &p, int grid, int warps, s
 }
 
 // Launches K2a + K2b for fields [p.f0, p.f1).  p.counter points at two zero-initialised words.
-cudaError_t launch_regress(const RegressParams &p_in, int sm_count, size_t smem_limit, cudaStream_t s) {
+cudaError_t launch_regress(const RegressParams &p_in, int sm_count, size_t smem_limit, cudaStream_t s, cudaEvent_t mid) {
     if (p_in.nwork == 0) return cudaSuccess;
     if (p_in.pmax > 96) return cudaErrorInvalidConfiguration;
     RegressParams p = p_in;
@@ -1166,6 +1166,7 @@ cudaError_t launch_regress(const RegressParams &p_in, int sm_count, size_t smem_
         }
         if (e != cudaSuccess) return e;
     }
+    if (mid) { e = cudaEventRecord(mid, s); if (e != cudaSuccess) return e; }
     // K2b
     {
         int warps = (int)(smem_limit / (regress_solve_ws_doubles(p.pmax, 1) * sizeof(double)));

@@ -55,7 +55,8 @@ struct SolveParams {
 
 size_t regress_warp_workspace_doubles(int N, int pmax);
 cudaError_t launch_center_rows(const double *X, double *U, int64_t nrows, int N, cudaStream_t s);
-cudaError_t launch_regress(const RegressParams &p, int sm_count, size_t smem_limit, cudaStream_t s);
+// mid (may be null) is recorded between the QR kernel (K2a) and the probe/solve kernel (K2b)
+cudaError_t launch_regress(const RegressParams &p, int sm_count, size_t smem_limit, cudaStream_t s, cudaEvent_t mid);
 // Fills scratch layout fields of p given bmax/nmax; returns doubles per CTA.
 int64_t solve_plan_scratch(SolveParams &p, int64_t nmax, size_t smem_limit);
 cudaError_t launch_assemble_band(const SolveParams &p, int sm_count, cudaStream_t s);

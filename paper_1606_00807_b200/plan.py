@@ -104,9 +104,9 @@ class Plan:
         _lib.check(_lib.lib().enkfmc_plan_profile(self._h, int(enable)))
 
     def stage_times(self):
-        """(ncalls, [ms centre, ms regress, ms solve] summed over the profiled calls)."""
+        """(ncalls, [ms K0 centre, ms K2a QR, ms K2b probe/solve, ms K3 assemble+solve] summed over the profiled calls)."""
         n = C.c_int64(0)
-        ms = np.zeros(3)
+        ms = np.zeros(4)
         _lib.check(_lib.lib().enkfmc_plan_stage_times(self._h, C.addressof(n), _lib.ptr(ms)))
         return int(n.value), ms
 

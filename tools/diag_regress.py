@@ -30,7 +30,7 @@ plan.profile(True)
 for _ in range(a.reps):
     device.analysis_device(plan, dX, dR, dYs, dXa)
 n, ms = plan.stage_times()
-print("stage ms (centre, regress, solve):", ms / n)
+print("stage ms (centre, K2a qr, K2b solve, K3):", ms / n)
 flags = device.workspace_tensor(plan, 3, (plan.nfields * plan.sum_nlocal,), "i32")
 p = np.tile(np.diff(plan.get(ROW_PTR)), plan.nfields)
 print("rows", flags.size, "deflated(bit1&!16)", int(((flags & 2) > 0).sum() - ((flags & 16) > 0).sum()),
@@ -43,4 +43,4 @@ for lo, hi in [(0, 1), (1, 16), (16, 32), (32, 41), (41, 61), (61, 200)]:
               f"fallback {int(((flags[sel] & 16) > 0).sum())}")
 print("fallback reasons (1 zero pivot / p>N, 2 certificate inconclusive, 3 out of deflation slots, 4 refined s above threshold, 5 certificate lost to cancellation, 6 polish not converged, 7 kept direction in block):", np.bincount((flags[(flags & 16) > 0] >> 5) & 7, minlength=8))
 fl = plan.work(w.nens)
-print("algorithmic GF regress/solve:", fl[0] / 1e9, fl[1] / 1e9, " -> TF/s", fl[0] / (ms[1] / n) / 1e9, fl[1] / (ms[2] / n) / 1e9)
+print("algorithmic GF regress/solve:", fl[0] / 1e9, fl[1] / 1e9, " -> TF/s", fl[0] / ((ms[1] + ms[2]) / n) / 1e9, fl[1] / (ms[3] / n) / 1e9)
