@@ -74,13 +74,16 @@ int enkfmc_plan_set_observations(enkfmc_plan *plan, int64_t nobs, const int64_t 
 
 /* Sizes: what = 0 ntiles, 1 sum n_local, 2 nnz(T pattern), 3 sum interior, 4 sum halo,
  * 5 nobs, 6 sum restricted obs, 7 pr, 8 pc, 9 max n_local, 10 max predecessors,
- * 11 max half-bandwidth, 12 nfields, 13 n2d. */
+ * 11 max half-bandwidth, 12 nfields, 13 n2d, 14 distinct regressions among the owned local rows
+ * (halo rows shared by several tiles with the same predecessor list are regressed once and copied),
+ * 15 owned local rows. */
 int64_t enkfmc_plan_size(const enkfmc_plan *plan, int what);
 
 /* Copy-out of the maps (for parity tests / the Python shim).  what = 0 tile_ptr[ntiles+1],
  * 1 local_order, 2 interior_ptr[ntiles+1], 3 interior, 4 interior_pos, 5 halo_ptr, 6 halo,
  * 7 row_ptr[sum n_local + 1], 8 col_idx[nnz] (local positions), 9 obs_ptr[nfields*ntiles+1],
- * 10 obs_pos, 11 obs_row, 12 half-bandwidth per tile, 13 physical order per local row. */
+ * 10 obs_pos, 11 obs_row, 12 half-bandwidth per tile, 13 physical order per local row,
+ * 14 per local row the local row whose regression it shares (itself, or -1 outside the owned tiles). */
 int enkfmc_plan_get(const enkfmc_plan *plan, int what, int64_t *out, int64_t capacity);
 
 /* ---- device-resident stages ------------------------------------------------------ */
@@ -148,10 +151,12 @@ int enkfmc_plan_profile(enkfmc_plan *plan, int enable);
 int enkfmc_plan_stage_times(enkfmc_plan *plan, int64_t *ncalls, double *ms4);
 
 /* Algorithmic work of one analysis with the current tile range (SURVEY 8d definitions):
- * flops2[0] = sum over owned local rows of 2*N*p^2 - (2/3)*p^3 + 4*N*p (Householder-QR least squares),
- * flops2[1] = sum over owned tiles with observations of n*b^2 + 4*n*b*N (banded Cholesky + two sweeps),
+ * flops3[0] = sum over owned local rows of 2*N*p^2 - (2/3)*p^3 + 4*N*p (Householder-QR least squares; the
+ *             reference's work: one regression per local row of every sub-domain),
+ * flops3[1] = sum over owned tiles with observations of n*b^2 + 4*n*b*N (banded Cholesky + two sweeps),
+ * flops3[2] = as [0] over the distinct regressions only: what the regression kernels execute,
  * each times the number of fields. */
-int enkfmc_plan_work(const enkfmc_plan *plan, int64_t nens, double *flops2);
+int enkfmc_plan_work(const enkfmc_plan *plan, int64_t nens, double *flops3);
 
 /* FP64 DFMA peak of the current device, measured with a register-resident FMA-chain kernel
  * (MEASURED_PEAKS.json has no FP64 figure).  Returns TFLOP/s in *tflops. */

@@ -25,14 +25,15 @@ struct DeviceState {
     // maps
     int64_t *tile_ptr = nullptr, *row_ptr = nullptr, *csc_ptr = nullptr, *csc_src = nullptr;
     int32_t *col_idx = nullptr, *csc_row = nullptr, *phys = nullptr, *iphys = nullptr, *bw = nullptr,
-            *state_row = nullptr, *pred_state = nullptr, *work_order = nullptr, *tile_order = nullptr;
+            *state_row = nullptr, *pred_state = nullptr, *work_order = nullptr, *tile_order = nullptr,
+            *regress_order = nullptr, *alias_row = nullptr, *alias_rep = nullptr;
     int64_t *rq_ptr = nullptr, *band_ptr = nullptr;
     int32_t *row_tile = nullptr;
     int64_t band_stride = 0, band_fields = 0;
     double *band = nullptr;
     int64_t rq_stride = 0;
     double *Rq = nullptr;
-    int64_t rq_fields = 0;          // fields the QR scratch holds
+    int64_t rq_alloc = 0;           // doubles the QR scratch holds
     uint8_t *is_interior = nullptr;
     int32_t *obs_slot = nullptr, *tile_nobs = nullptr;
     bool obs_current = false, orders_current = false;
@@ -109,16 +110,6 @@ int ensure_device(enkfmc_plan *p) {
         d->band_stride = bp.back();
         if ((rc = upload(d->band_ptr, bp))) return rc;
     }
-    {   // packed QR block of every local row: R by columns (min(j+1,K) entries), c[K], e2
-        std::vector<int64_t> rq(p->sum_nlocal() + 1, 0);
-        // K depends on the ensemble size; sized for K = p (the largest block), valid for any N
-        for (int64_t q = 0; q < p->sum_nlocal(); ++q) {
-            const int64_t k = p->row_ptr[q + 1] - p->row_ptr[q];
-            rq[q + 1] = rq[q] + k * (k + 1) / 2 + k + 1;
-        }
-        d->rq_stride = rq.back();
-        if ((rc = upload(d->rq_ptr, rq))) return rc;
-    }
     CK(cudaMalloc(&d->counters, 4 * sizeof(unsigned int)));
     CK(cudaMemset(d->counters, 0, 4 * sizeof(unsigned int)));
     for (auto &ev : d->ev) CK(cudaEventCreate(&ev));
@@ -132,6 +123,11 @@ int ensure_orders(enkfmc_plan *p) {
     int rc;
     if ((rc = upload(d->work_order, p->work_order))) return rc;
     if ((rc = upload(d->tile_order, p->tile_order))) return rc;
+    if ((rc = upload(d->regress_order, p->regress_order))) return rc;
+    if ((rc = upload(d->alias_row, p->alias_row))) return rc;
+    if ((rc = upload(d->alias_rep, p->alias_rep))) return rc;
+    if ((rc = upload(d->rq_ptr, p->rq_ptr))) return rc;
+    d->rq_stride = p->rq_ptr.empty() ? 0 : p->rq_ptr.back();
     d->orders_current = true;
     return ENKFMC_OK;
 }
@@ -212,24 +208,24 @@ int do_regress(enkfmc_plan *p, const double *d_U, int64_t nens, double rank_tol,
     RegressParams R{};
     R.U = d_U; R.N = (int)nens; R.ld = (int)nens | 1; R.pmax = (int)std::max<int64_t>(p->max_pred, 1);
     R.nfields = (int)p->nfields; R.nloc = p->sum_nlocal(); R.nnz = p->nnz(); R.nstate2d = p->nstate2d;
-    R.nwork = (int64_t)p->work_order.size() * p->nfields;
-    R.row_ptr = d->row_ptr; R.pred_state = d->pred_state; R.state_row = d->state_row; R.work_order = d->work_order;
+    R.nwork = (int64_t)p->regress_order.size() * p->nfields;
+    R.row_ptr = d->row_ptr; R.pred_state = d->pred_state; R.state_row = d->state_row; R.work_order = d->regress_order;
     R.rank_tol = rank_tol; R.variance_floor = floor_; R.fast_ratio = 1e-6;
     R.T = d_T; R.D = d_D; R.flags = d_flags; R.counter = d->counters;
     R.rq_ptr = d->rq_ptr; R.rq_stride = d->rq_stride;
     // QR scratch: as many fields per launch pair as fit in the budget (default 16 GiB)
     const int64_t budget = (int64_t)16 << 30;
     int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(p->nfields, budget / std::max<int64_t>(8 * d->rq_stride, 1)));
-    if (!d->Rq || d->rq_fields < chunk) {
+    if (!d->Rq || d->rq_alloc < chunk * d->rq_stride) {
         release(d->Rq);
         CK(cudaMalloc(&d->Rq, std::max<size_t>((size_t)chunk * d->rq_stride, 1) * sizeof(double)));
-        d->rq_fields = chunk;
+        d->rq_alloc = chunk * d->rq_stride;
     }
     R.Rq = d->Rq;
     for (int64_t f0 = 0; f0 < p->nfields; f0 += chunk) {
         R.f0 = (int)f0;
         R.f1 = (int)std::min<int64_t>(p->nfields, f0 + chunk);
-        R.nwork = (int64_t)p->work_order.size() * (R.f1 - R.f0);
+        R.nwork = (int64_t)p->regress_order.size() * (R.f1 - R.f0);
         if (R.nwork > 0xfffffff0LL) { enkfmc_set_error("too many regressions for one launch"); return ENKFMC_E_CAPACITY; }
         cudaError_t e = launch_regress(R, d->sm_count, d->smem_limit, s, mid);
         if (e == cudaErrorInvalidConfiguration) {
@@ -239,6 +235,11 @@ int do_regress(enkfmc_plan *p, const double *d_U, int64_t nens, double rank_tol,
         }
         CK(e);
         if (R.nwork > 0) p->counters[0] += 2;
+    }
+    if (!p->alias_row.empty()) {   // copy each distinct regression to the other tiles holding the same row
+        CK(launch_replicate_rows(d->alias_row, d->alias_rep, (int64_t)p->alias_row.size(), d->row_ptr, p->nfields,
+                                 p->nnz(), p->sum_nlocal(), d_T, d_D, d_flags, s));
+        p->counters[0] += 1;
     }
     return ENKFMC_OK;
 }
@@ -289,7 +290,7 @@ void enkfmc_device_release(enkfmc_plan *p) {
     if (!d) return;
     release(d->tile_ptr); release(d->row_ptr); release(d->csc_ptr); release(d->csc_src); release(d->col_idx);
     release(d->csc_row); release(d->phys); release(d->iphys); release(d->bw); release(d->state_row);
-    release(d->pred_state); release(d->work_order); release(d->tile_order); release(d->is_interior);
+    release(d->pred_state); release(d->regress_order); release(d->alias_row); release(d->alias_rep); release(d->work_order); release(d->tile_order); release(d->is_interior);
     release(d->obs_slot); release(d->tile_nobs); release(d->U); release(d->T); release(d->D); release(d->scratch);
     release(d->flags); release(d->status); release(d->counters); release(d->rq_ptr); release(d->Rq); release(d->band_ptr); release(d->band); release(d->row_tile); release(d->dX); release(d->dXa); release(d->dR);
     release(d->dYs);

@@ -982,7 +982,8 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
                 return bad ? 2 : 0;
             };
 
-            unsigned seed = (unsigned)q * 7919u;   // independent of the field: stacked fields stay bitwise independent
+            // depends on the regression only (not on the field, nor on which tile's copy of the row is computed)
+            unsigned seed = (unsigned)P.state_row[q] * 7919u + (unsigned)p * 104729u;
             const double T2 = tail2, T4 = tail4;   // totals over all singular values
             double def2 = 0.0, def4 = 0.0;         // part carried by the deflated block
             double smin_defl = smax_lo;            // smallest deflated singular value (cancellation guard)
@@ -1191,6 +1192,37 @@ cudaError_t launch_regress(const RegressParams &p_in, int sm_count, size_t smem_
         else e = launch_solve_t<3>(p, (int)grid, warps, ws * warps, s);
     }
     return e;
+}
+
+// Copies a finished regression to its aliases: one warp per (alias row, field).
+__global__ void __launch_bounds__(256) replicate_rows_kernel(const int32_t *__restrict__ alias_row,
+                                                             const int32_t *__restrict__ alias_rep, int64_t naliases,
+                                                             const int64_t *__restrict__ row_ptr, int64_t nfields,
+                                                             int64_t nnz, int64_t nloc, double *__restrict__ T,
+                                                             double *__restrict__ D, int32_t *__restrict__ flags) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (w >= naliases * nfields) return;
+    const int64_t a = w % naliases, f = w / naliases;
+    const int q = alias_row[a], r = alias_rep[a];
+    const int64_t dst = row_ptr[q], src = row_ptr[r];
+    const int p = (int)(row_ptr[q + 1] - dst);
+    double *Tf = T + f * nnz;
+    for (int j = lane; j < p; j += 32) Tf[dst + j] = Tf[src + j];
+    if (lane == 0) {
+        D[f * nloc + q] = D[f * nloc + r];
+        if (flags) flags[f * nloc + q] = flags[f * nloc + r];
+    }
+}
+
+cudaError_t launch_replicate_rows(const int32_t *alias_row, const int32_t *alias_rep, int64_t naliases,
+                                  const int64_t *row_ptr, int64_t nfields, int64_t nnz, int64_t nloc, double *T,
+                                  double *D, int32_t *flags, cudaStream_t s) {
+    const int64_t warps = naliases * nfields;
+    if (warps == 0) return cudaSuccess;
+    replicate_rows_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(alias_row, alias_rep, naliases, row_ptr, nfields,
+                                                                       nnz, nloc, T, D, flags);
+    return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------------------------------

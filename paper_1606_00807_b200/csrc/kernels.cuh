@@ -14,7 +14,7 @@ struct RegressParams {
     const int64_t *row_ptr;    // [nloc + 1]
     const int32_t *pred_state; // [nnz] state row of each predecessor
     const int32_t *state_row;  // [nloc]
-    const int32_t *work_order; // [nloc] rows, most predecessors first
+    const int32_t *work_order; // distinct regressions (plan.h regress_order), most predecessors first
     double rank_tol, variance_floor, fast_ratio;
     double *T;                 // [nfields][nnz]  (-beta)
     double *D;                 // [nfields][nloc] floored
@@ -57,6 +57,10 @@ size_t regress_warp_workspace_doubles(int N, int pmax);
 cudaError_t launch_center_rows(const double *X, double *U, int64_t nrows, int N, cudaStream_t s);
 // mid (may be null) is recorded between the QR kernel (K2a) and the probe/solve kernel (K2b)
 cudaError_t launch_regress(const RegressParams &p, int sm_count, size_t smem_limit, cudaStream_t s, cudaEvent_t mid);
+// T, D, flags of row alias_row[a] := those of alias_rep[a] (same regression), every field
+cudaError_t launch_replicate_rows(const int32_t *alias_row, const int32_t *alias_rep, int64_t naliases,
+                                  const int64_t *row_ptr, int64_t nfields, int64_t nnz, int64_t nloc, double *T,
+                                  double *D, int32_t *flags, cudaStream_t s);
 // Fills scratch layout fields of p given bmax/nmax; returns doubles per CTA.
 int64_t solve_plan_scratch(SolveParams &p, int64_t nmax, size_t smem_limit);
 cudaError_t launch_assemble_band(const SolveParams &p, int sm_count, cudaStream_t s);

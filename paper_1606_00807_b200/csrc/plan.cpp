@@ -15,6 +15,7 @@
 #include <cstring>
 #include <numeric>
 #include <string>
+#include <unordered_map>
 
 #include "plan.h"
 
@@ -241,13 +242,57 @@ int validate_increasing(const int64_t *a, int64_t n, const char *name) {
 void enkfmc_build_orders(enkfmc_plan &p) {
     p.work_order.clear();
     p.tile_order.clear();
+    p.regress_order.clear();
+    p.alias_row.clear();
+    p.alias_rep.clear();
+    // identical regressions (same state row, same predecessor list) among the owned rows
+    std::unordered_map<uint64_t, std::vector<int32_t>> seen;
+    auto row_hash = [&](int64_t q) {
+        uint64_t h = 1469598103934665603ull ^ (uint64_t)(uint32_t)p.state_row[q];
+        for (int64_t e = p.row_ptr[q]; e < p.row_ptr[q + 1]; ++e) {
+            h ^= (uint64_t)(uint32_t)p.pred_state[e];
+            h *= 1099511628211ull;
+        }
+        return h;
+    };
+    auto same_row = [&](int64_t a, int64_t b) {
+        const int64_t n = p.row_ptr[a + 1] - p.row_ptr[a];
+        if (p.state_row[a] != p.state_row[b] || n != p.row_ptr[b + 1] - p.row_ptr[b]) return false;
+        return std::equal(p.pred_state.begin() + p.row_ptr[a], p.pred_state.begin() + p.row_ptr[a] + n,
+                          p.pred_state.begin() + p.row_ptr[b]);
+    };
     for (int64_t t = p.tile_begin; t < p.tile_end; ++t) {
         p.tile_order.push_back((int32_t)t);
-        for (int64_t q = p.tile_ptr[t]; q < p.tile_ptr[t + 1]; ++q) p.work_order.push_back((int32_t)q);
+        for (int64_t q = p.tile_ptr[t]; q < p.tile_ptr[t + 1]; ++q) {
+            p.work_order.push_back((int32_t)q);
+            auto &bucket = seen[row_hash(q)];
+            int32_t rep = -1;
+            for (int32_t c : bucket) if (same_row(c, q)) { rep = c; break; }
+            if (rep < 0) {
+                bucket.push_back((int32_t)q);
+                p.regress_order.push_back((int32_t)q);
+            } else {
+                p.alias_row.push_back((int32_t)q);
+                p.alias_rep.push_back(rep);
+            }
+        }
     }
-    std::stable_sort(p.work_order.begin(), p.work_order.end(), [&](int32_t a, int32_t b) {
+    auto more_preds = [&](int32_t a, int32_t b) {
         return (p.row_ptr[a + 1] - p.row_ptr[a]) > (p.row_ptr[b + 1] - p.row_ptr[b]);
-    });
+    };
+    std::stable_sort(p.work_order.begin(), p.work_order.end(), more_preds);
+    std::stable_sort(p.regress_order.begin(), p.regress_order.end(), more_preds);
+    // packed QR block of every representative: R by columns (min(j+1,K) entries), c[K], e2; sized for
+    // K = p (the largest block), valid for any ensemble size
+    p.rq_ptr.assign((size_t)p.sum_nlocal() + 1, 0);
+    {
+        std::vector<uint8_t> is_rep((size_t)p.sum_nlocal(), 0);
+        for (int32_t q : p.regress_order) is_rep[q] = 1;
+        for (int64_t q = 0; q < p.sum_nlocal(); ++q) {
+            const int64_t k = p.row_ptr[q + 1] - p.row_ptr[q];
+            p.rq_ptr[q + 1] = p.rq_ptr[q] + (is_rep[q] ? k * (k + 1) / 2 + k + 1 : 0);
+        }
+    }
     std::stable_sort(p.tile_order.begin(), p.tile_order.end(), [&](int32_t a, int32_t b) {
         auto cost = [&](int32_t t) {
             double n = (double)(p.tile_ptr[t + 1] - p.tile_ptr[t]), w = (double)p.bw[t] + 1.0;
@@ -270,16 +315,15 @@ extern "C" int enkfmc_plan_set_tile_range(enkfmc_plan *p, int64_t t0, int64_t t1
     return ENKFMC_OK;
 }
 
-extern "C" int enkfmc_plan_work(const enkfmc_plan *p, int64_t nens, double *flops2) {
+extern "C" int enkfmc_plan_work(const enkfmc_plan *p, int64_t nens, double *flops3) {
     const double N = (double)nens;
-    double reg = 0.0, sol = 0.0;
-    for (int64_t t = p->tile_begin; t < p->tile_end; ++t) {
-        for (int64_t q = p->tile_ptr[t]; q < p->tile_ptr[t + 1]; ++q) {
-            const double k = (double)(p->row_ptr[q + 1] - p->row_ptr[q]);
-            reg += 2.0 * N * k * k - (2.0 / 3.0) * k * k * k + 4.0 * N * k;
-        }
-    }
-    reg *= (double)p->nfields;
+    auto qr_flops = [&](int64_t q) {
+        const double k = (double)(p->row_ptr[q + 1] - p->row_ptr[q]);
+        return 2.0 * N * k * k - (2.0 / 3.0) * k * k * k + 4.0 * N * k;
+    };
+    double reg = 0.0, sol = 0.0, reg_distinct = 0.0;
+    for (int32_t q : p->work_order) reg += qr_flops(q);
+    for (int32_t q : p->regress_order) reg_distinct += qr_flops(q);
     for (int64_t f = 0; f < p->nfields; ++f) {
         for (int64_t t = p->tile_begin; t < p->tile_end; ++t) {
             if (p->have_obs && p->tile_nobs[(size_t)(f * p->ntiles + t)] == 0) continue;
@@ -287,8 +331,9 @@ extern "C" int enkfmc_plan_work(const enkfmc_plan *p, int64_t nens, double *flop
             sol += n * b * b + 4.0 * n * b * N;
         }
     }
-    flops2[0] = reg;
-    flops2[1] = sol;
+    flops3[0] = reg * (double)p->nfields;
+    flops3[1] = sol;
+    flops3[2] = reg_distinct * (double)p->nfields;
     return ENKFMC_OK;
 }
 
@@ -553,6 +598,8 @@ extern "C" int64_t enkfmc_plan_size(const enkfmc_plan *p, int what) {
         case 11: return p->max_bw;
         case 12: return p->nfields;
         case 13: return p->n2d;
+        case 14: return (int64_t)p->regress_order.size();   // distinct regressions among the owned rows
+        case 15: return (int64_t)p->work_order.size();      // owned local rows
         default: return -1;
     }
 }
@@ -582,6 +629,12 @@ extern "C" int enkfmc_plan_get(const enkfmc_plan *p, int what, int64_t *out, int
         case 11: return copy_out(p->obs_row, out, cap);
         case 12: return copy_out(p->bw, out, cap);
         case 13: return copy_out(p->phys, out, cap);
+        case 14: {   // per local row: the row whose regression it shares (itself for a representative, -1 if not owned)
+            std::vector<int64_t> rep((size_t)p->sum_nlocal(), -1);
+            for (int32_t q : p->regress_order) rep[q] = q;
+            for (size_t a = 0; a < p->alias_row.size(); ++a) rep[p->alias_row[a]] = p->alias_rep[a];
+            return copy_out(rep, out, cap);
+        }
         default: enkfmc_set_error("unknown map id"); return ENKFMC_E_VALUE;
     }
 }

@@ -30,7 +30,13 @@ struct enkfmc_plan {
     std::vector<int64_t> csc_ptr;       // per local row + 1: column lists of T (global offsets)
     std::vector<int32_t> csc_row;       // local row j holding the entry
     std::vector<int64_t> csc_src;       // offset of the entry in the CSR value array
-    std::vector<int32_t> work_order;    // local rows sorted by predecessor count, descending
+    std::vector<int32_t> work_order;    // owned local rows sorted by predecessor count, descending
+    // Halo rows are regressed once per tile holding them (estimator.py:123-159 runs per sub-domain), but two
+    // local rows with the same state row and the same predecessor list are the same regression: it is
+    // computed once (regress_order, the representatives) and copied to its aliases.
+    std::vector<int32_t> regress_order; // representatives among the owned rows, most predecessors first
+    std::vector<int32_t> alias_row, alias_rep;   // owned non-representative rows and their representatives
+    std::vector<int64_t> rq_ptr;        // per local row + 1: offset of the packed QR block (representatives only)
     std::vector<int32_t> tile_order;    // tiles sorted by solve cost, descending
     int64_t max_nlocal = 0, max_pred = 0, max_bw = 0;
 

@@ -11,10 +11,10 @@ import numpy as np
 from . import _lib
 
 (TILE_PTR, LOCAL_ORDER, INTERIOR_PTR, INTERIOR, INTERIOR_POS, HALO_PTR, HALO, ROW_PTR, COL_IDX, OBS_PTR, OBS_POS,
- OBS_ROW, BANDWIDTH, PHYS) = range(14)
+ OBS_ROW, BANDWIDTH, PHYS, REGRESSION_OF) = range(15)
 _SIZE_OF = {TILE_PTR: (0, 1), LOCAL_ORDER: (1, 0), INTERIOR_PTR: (0, 1), INTERIOR: (3, 0), INTERIOR_POS: (3, 0),
             HALO_PTR: (0, 1), HALO: (4, 0), ROW_PTR: (1, 1), COL_IDX: (2, 0), OBS_POS: (6, 0), OBS_ROW: (6, 0),
-            BANDWIDTH: (0, 0), PHYS: (1, 0)}
+            BANDWIDTH: (0, 0), PHYS: (1, 0), REGRESSION_OF: (1, 0)}
 
 
 class Plan:
@@ -73,6 +73,8 @@ class Plan:
     max_nlocal = property(lambda self: self.size(9))
     max_pred = property(lambda self: self.size(10))
     max_bw = property(lambda self: self.size(11))
+    n_regressions = property(lambda self: self.size(14))   # distinct regressions among the owned rows
+    n_owned_rows = property(lambda self: self.size(15))
     nfields = property(lambda self: self.size(12))
 
     def get(self, what: int) -> np.ndarray:
@@ -111,10 +113,11 @@ class Plan:
         return int(n.value), ms
 
     def work(self, nens: int):
-        """Algorithmic flops (regress, solve) of one analysis over the owned tiles."""
-        fl = np.zeros(2)
+        """Algorithmic flops of one analysis over the owned tiles: (regressions as the reference
+        runs them, local solves, regressions executed = distinct ones only)."""
+        fl = np.zeros(3)
         _lib.check(_lib.lib().enkfmc_plan_work(self._h, int(nens), _lib.ptr(fl)))
-        return float(fl[0]), float(fl[1])
+        return float(fl[0]), float(fl[1]), float(fl[2])
 
     def subdomains(self):
         """list[Subdomain] exactly as decompose returns them (geometry.py:204-221)."""

@@ -86,13 +86,15 @@ def test_restrict_observations_per_field_tile():
 def test_work_counts_match_survey_and_tile_ranges():
     g = _geo(192, 96, nfields=29)
     pl = Plan.decomposed(g, 256, 4)
-    reg, sol = pl.work(80)
+    reg, sol, reg_distinct = pl.work(80)
     assert reg == pytest.approx(2.86e11, rel=0.01) and sol == pytest.approx(6.48e10, rel=0.01)
+    assert 0.6 * reg < reg_distinct < 0.7 * reg          # halo rows shared between tiles are regressed once
     pl.set_tile_range(0, 128)
-    r0, _ = pl.work(80)
+    r0, _, d0 = pl.work(80)
     pl.set_tile_range(128, 256)
-    r1, _ = pl.work(80)
+    r1, _, d1 = pl.work(80)
     assert r0 + r1 == pytest.approx(reg, rel=1e-12)
+    assert d0 + d1 > reg_distinct                        # rows straddling the cut are regressed by both ranks
     with pytest.raises(ValueError):
         pl.set_tile_range(10, 300)
 
@@ -130,3 +132,33 @@ def test_perturb_observations_is_the_reference_stream(golden_analysis):
     A = golden_analysis
     net = mck.ObservationNetwork(A["a0_obs"], A["a0_r"], A["a0_y"])
     assert np.array_equal(mck.perturb_observations(net, int(A["a0_params"][3]), 11, 0).Ys, A["a0_Ys"])
+
+
+def test_shared_regressions_are_identical_problems():
+    """Halo rows regressed by several tiles: rows mapped onto one regression must have the same state
+    row and the same predecessor list (estimator.py:123-131), and every distinct problem is kept once."""
+    from paper_1606_00807_b200 import plan as planmod
+    geo = mck.GridGeometry("grid2d", 24, 18)
+    for periodic in (False, True):
+        geo = mck.GridGeometry("grid2d", 24, 18, boundary="periodic" if periodic else "clipped")
+        plan = planmod.Plan.decomposed(geo, 12, 2)
+        tile_ptr, local_order = plan.get(planmod.TILE_PTR), plan.get(planmod.LOCAL_ORDER)
+        row_ptr, col_idx = plan.get(planmod.ROW_PTR), plan.get(planmod.COL_IDX)
+        rep = plan.get(planmod.REGRESSION_OF)
+        tile_of = np.repeat(np.arange(plan.ntiles), np.diff(tile_ptr))
+
+        def problem(q):
+            base = tile_ptr[tile_of[q]]
+            return (int(local_order[q]), tuple(local_order[base + col_idx[row_ptr[q]:row_ptr[q + 1]]].tolist()))
+
+        problems = [problem(q) for q in range(len(rep))]
+        assert all(problems[q] == problems[rep[q]] for q in range(len(rep)))
+        assert all(rep[rep[q]] == rep[q] for q in range(len(rep)))
+        assert plan.n_regressions == len(set(problems)) == len(set(rep.tolist()))
+        assert plan.n_regressions < plan.n_owned_rows == len(rep)
+        # one rank's share: only owned rows are mapped, and only onto owned rows
+        plan.set_tile_range(2, 5)
+        rep = plan.get(planmod.REGRESSION_OF)
+        owned = (tile_of >= 2) & (tile_of < 5)
+        assert np.all(rep[~owned] == -1) and np.all(owned[rep[owned]])
+        assert plan.n_owned_rows == int(owned.sum())

@@ -43,4 +43,4 @@ for lo, hi in [(0, 1), (1, 16), (16, 32), (32, 41), (41, 61), (61, 200)]:
               f"fallback {int(((flags[sel] & 16) > 0).sum())}")
 print("fallback reasons (1 zero pivot / p>N, 2 certificate inconclusive, 3 out of deflation slots, 4 refined s above threshold, 5 certificate lost to cancellation, 6 polish not converged, 7 kept direction in block):", np.bincount((flags[(flags & 16) > 0] >> 5) & 7, minlength=8))
 fl = plan.work(w.nens)
-print("algorithmic GF regress/solve:", fl[0] / 1e9, fl[1] / 1e9, " -> TF/s", fl[0] / ((ms[1] + ms[2]) / n) / 1e9, fl[1] / (ms[3] / n) / 1e9)
+print("algorithmic GF regress/solve:", fl[2] / 1e9, fl[1] / 1e9, " -> TF/s", fl[2] / ((ms[1] + ms[2]) / n) / 1e9, fl[1] / (ms[3] / n) / 1e9)

@@ -54,7 +54,7 @@ def run(name, w, oracle_fields):
     nrow = flags.size
     print(f"| {name} | {w.nstate} | {w.nens} | {w.zeta} | {'yes' if maps_ok else 'NO'} | {terr:.1e} | {derr:.1e} | {xerr:.1e} | "
           f"{100 * ((flags & 2) > 0).sum() / nrow:.1f} | {100 * ((flags & 16) > 0).sum() / nrow:.2f} | {100 * ((flags & 8) > 0).sum() / nrow:.1f} | "
-          f"{ms[1] + ms[2]:.2f} | {ms[3]:.2f} | {w.nstate / (ms.sum() * 1e-3) / 1e6:.2f} | {fl[0] / (ms[1] + ms[2]) / 1e9:.2f} | {fl[1] / ms[3] / 1e9:.2f} | "
+          f"{ms[1] + ms[2]:.2f} | {ms[3]:.2f} | {w.nstate / (ms.sum() * 1e-3) / 1e6:.2f} | {fl[2] / (ms[1] + ms[2]) / 1e9:.2f} | {fl[1] / ms[3] / 1e9:.2f} | "
           f"{len(oracle_fields)} field(s), {t_cpu:.1f} s |", flush=True)
 
 
