@@ -261,6 +261,10 @@ int do_solve(enkfmc_plan *p, const double *d_X, const double *d_T, const double 
     S.is_interior = d->is_interior; S.scratch = d->scratch; S.status = d_status; S.counter = d->counters + 2;
     S.band_ptr = d->band_ptr; S.band_stride = d->band_stride; S.row_tile = d->row_tile; S.work_order = d->work_order;
     S.nrows_owned = (int64_t)p->work_order.size();
+    S.asm_nmax = (int)p->max_nlocal;
+    S.asm_nnzmax = 0;
+    for (int64_t t = 0; t < p->ntiles; ++t)
+        S.asm_nnzmax = std::max<int>(S.asm_nnzmax, (int)(p->row_ptr[p->tile_ptr[t + 1]] - p->row_ptr[p->tile_ptr[t]]));
     int rc2 = ensure_band(p);
     if (rc2) return rc2;
     S.band = d->band;
@@ -268,7 +272,7 @@ int do_solve(enkfmc_plan *p, const double *d_X, const double *d_T, const double 
     for (int64_t f0 = 0; f0 < p->nfields; f0 += d->band_fields) {
         S.f0 = (int)f0;
         S.f1 = (int)std::min<int64_t>(p->nfields, f0 + d->band_fields);
-        CK(launch_assemble_band(S, d->sm_count, s));
+        CK(launch_assemble_band(S, d->sm_count, d->smem_limit, s));
         cudaError_t e = launch_local_solve(S, d->solve_grid, d->smem_limit, s);
         if (e == cudaErrorInvalidConfiguration) {
             enkfmc_set_error("local-solve window (half-bandwidth " + std::to_string(p->max_bw) + ") exceeds shared memory");
@@ -548,7 +552,8 @@ extern "C" int enkfmc_assemble_band(enkfmc_plan *p, const double *d_T, const dou
     S.band_ptr = d->band_ptr; S.band_stride = d->band_stride; S.row_tile = d->row_tile; S.work_order = d->work_order;
     S.nrows_owned = (int64_t)p->work_order.size();
     S.assemble_only = 1; S.f0 = 0; S.f1 = 1; S.band = d_band;
-    CK(launch_assemble_band(S, d->sm_count, (cudaStream_t)stream));
+    S.tile_order = d->tile_order; S.asm_nmax = (int)p->max_nlocal; S.asm_nnzmax = (int)std::min<int64_t>(p->nnz(), 1 << 30);
+    CK(launch_assemble_band(S, d->sm_count, d->smem_limit, (cudaStream_t)stream));
     p->counters[0] += 1;
     return ENKFMC_OK;
 }

@@ -1300,6 +1300,89 @@ __global__ void __launch_bounds__(ASM_WARPS * 32) assemble_band_kernel(const Sol
     }
 }
 
+// Tile-cooperative form of K3a: one CTA per (field, tile).  The tile's T values, the physical column of every
+// entry, D and the row pointers are staged in shared memory once, so the index chase of every row of A runs at
+// shared-memory latency; each warp then assembles rows exactly as assemble_band_kernel does (same order of
+// additions, bitwise the same band).  Used whenever the staging fits (launch_assemble_band decides).
+#define ASMT_THREADS 512
+
+__host__ __device__ inline size_t asm_tile_smem_bytes(int nmax, int nnzmax, int bmax) {
+    size_t b = (size_t)nnzmax * 8 + (size_t)nmax * 8 + (size_t)(ASMT_THREADS / 32) * 8 * (solve_wb(bmax) + 1) * 8;
+    b += (size_t)(nmax + 1) * 4;
+    b += (size_t)nnzmax * 2 + (size_t)nmax * 2;
+    return (b + 15) & ~(size_t)15;
+}
+
+__global__ void __launch_bounds__(ASMT_THREADS) assemble_band_tile_kernel(const SolveParams P) {
+    extern __shared__ double smem[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nf = P.f1 - P.f0;
+    const int t = P.tile_order[blockIdx.x / nf];
+    const int fl = (int)(blockIdx.x % nf), f = P.f0 + fl;
+    if (!P.assemble_only && P.tile_nobs[(int64_t)f * P.ntiles + t] == 0) return;
+    const int64_t base = P.tile_ptr[t];
+    const int n = (int)(P.tile_ptr[t + 1] - base);
+    const int64_t e0 = P.row_ptr[base];
+    const int nz = (int)(P.row_ptr[base + n] - e0);
+    const int Wb = solve_wb(P.bw[t]), Wr = 8 * (Wb + 1);
+    const int accw = 8 * (solve_wb(P.bmax) + 1);
+
+    double *sT = smem;
+    double *sD = sT + P.asm_nnzmax;
+    double *accs = sD + P.asm_nmax;
+    int32_t *sRow = reinterpret_cast<int32_t *>(accs + (size_t)(ASMT_THREADS / 32) * accw);
+    uint16_t *sK = reinterpret_cast<uint16_t *>(sRow + P.asm_nmax + 1);
+    uint16_t *sPhys = sK + P.asm_nnzmax;
+
+    const double *Tf = P.T + (int64_t)f * P.nnz + e0;
+    const double *Df = P.D + (int64_t)f * P.nloc + base;
+    const int32_t *phys = P.phys + base;
+    for (int i = tid; i < n; i += ASMT_THREADS) { sD[i] = Df[i]; sPhys[i] = (uint16_t)phys[i]; }
+    for (int i = tid; i <= n; i += ASMT_THREADS) sRow[i] = (int32_t)(P.row_ptr[base + i] - e0);
+    for (int e = tid; e < nz; e += ASMT_THREADS) { sT[e] = Tf[e]; sK[e] = (uint16_t)phys[P.col_idx[e0 + e]]; }
+    __syncthreads();
+
+    double *acc = accs + (size_t)warp * accw;
+    for (int i = warp; i < n; i += ASMT_THREADS / 32) {
+        const int I = sPhys[i];
+        const int col0 = 8 * ((I >> 3) - Wb);
+        for (int e = lane; e < Wr; e += 32) acc[e] = 0.0;
+        const int64_t c0 = P.csc_ptr[base + i];
+        const int ncsc = (int)(P.csc_ptr[base + i + 1] - c0);
+        __syncwarp();
+        // rows j > i holding column i: lists are short (<= 96), fetched 32 at a time and broadcast by shuffle
+        for (int eb = -1; eb < ncsc; eb = (eb < 0 ? 0 : eb + 32)) {
+            int jl = 0, sl = 0, cnt_e = 1;
+            if (eb >= 0) {
+                cnt_e = ncsc - eb < 32 ? ncsc - eb : 32;
+                if (lane < cnt_e) { jl = P.csc_row[c0 + eb + lane]; sl = (int)(P.csc_src[c0 + eb + lane] - e0); }
+            }
+            for (int ee = 0; ee < cnt_e; ++ee) {
+                int j; double tji;
+                if (eb < 0) { j = i; tji = 1.0; }
+                else { j = __shfl_sync(FULL, jl, ee); tji = sT[__shfl_sync(FULL, sl, ee)]; }
+                const double sc = tji / sD[j];
+                const int q0 = sRow[j];
+                const int cnt = sRow[j + 1] - q0;
+                for (int m = lane - 1; m < cnt; m += 32) {
+                    int Kp; double tjk;
+                    if (m < 0) { Kp = sPhys[j]; tjk = 1.0; } else { Kp = sK[q0 + m]; tjk = sT[q0 + m]; }
+                    if (Kp <= I) acc[Kp - col0] += sc * tjk;
+                }
+                __syncwarp();
+            }
+        }
+        if (lane == 0 && !P.assemble_only) {
+            const int sl = P.obs_slot[(int64_t)f * P.nloc + base + i];
+            if (sl >= 0) acc[I - col0] += 1.0 / P.rdiag[sl];
+        }
+        __syncwarp();
+        double *dst = P.band + (int64_t)fl * P.band_stride + P.band_ptr[t] + (int64_t)I * Wr;
+        for (int e = lane; e < Wr; e += 32) dst[e] = acc[e];
+        __syncwarp();
+    }
+}
+
 __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveParams P) {
     extern __shared__ double smem[];
     __shared__ unsigned int s_item;
@@ -1614,9 +1697,17 @@ int solve_grid_size(int sm_count, const SolveParams &p, size_t smem_limit) {
     return (int)(grid < 1 ? 1 : grid);
 }
 
-cudaError_t launch_assemble_band(const SolveParams &p, int sm_count, cudaStream_t s) {
+cudaError_t launch_assemble_band(const SolveParams &p, int sm_count, size_t smem_limit, cudaStream_t s) {
     const int64_t total = p.nrows_owned * (p.f1 - p.f0);
     if (total == 0) return cudaSuccess;
+    const size_t tile_smem = asm_tile_smem_bytes(p.asm_nmax, p.asm_nnzmax, p.bmax);
+    if (p.asm_nmax > 0 && p.asm_nmax < 65536 && p.asm_nnzmax < 65536 && tile_smem <= smem_limit) {
+        cudaError_t e = cudaFuncSetAttribute(assemble_band_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)tile_smem);
+        if (e != cudaSuccess) return e;
+        assemble_band_tile_kernel<<<(unsigned)((int64_t)p.ntiles_owned * (p.f1 - p.f0)), ASMT_THREADS, tile_smem, s>>>(p);
+        return cudaGetLastError();
+    }
     int64_t grid = (total + ASM_WARPS - 1) / ASM_WARPS;
     if (grid > (int64_t)sm_count * 8) grid = (int64_t)sm_count * 8;
     const size_t smem = (size_t)ASM_WARPS * 8 * (solve_wb(p.bmax) + 1) * sizeof(double);

@@ -51,6 +51,7 @@ struct SolveParams {
     const int32_t *row_tile;   // [nloc]
     const int32_t *work_order; // owned local rows
     int64_t nrows_owned;
+    int asm_nmax, asm_nnzmax;  // largest tile (rows, T entries): shared-memory staging of the tile-cooperative K3a
 };
 
 size_t regress_warp_workspace_doubles(int N, int pmax);
@@ -63,7 +64,7 @@ cudaError_t launch_replicate_rows(const int32_t *alias_row, const int32_t *alias
                                   double *D, int32_t *flags, cudaStream_t s);
 // Fills scratch layout fields of p given bmax/nmax; returns doubles per CTA.
 int64_t solve_plan_scratch(SolveParams &p, int64_t nmax, size_t smem_limit);
-cudaError_t launch_assemble_band(const SolveParams &p, int sm_count, cudaStream_t s);
+cudaError_t launch_assemble_band(const SolveParams &p, int sm_count, size_t smem_limit, cudaStream_t s);
 int solve_grid_size(int sm_count, const SolveParams &p, size_t smem_limit);
 cudaError_t launch_local_solve(const SolveParams &p, int grid, size_t smem_limit, cudaStream_t s);
 cudaError_t launch_scatter_rows(double *dst, const int64_t *dst_rows, const double *src, const int64_t *src_rows,
