@@ -1383,6 +1383,9 @@ __global__ void __launch_bounds__(ASMT_THREADS) assemble_band_tile_kernel(const 
     }
 }
 
+__host__ __device__ inline size_t solve_strip_doubles(int Wb) { return (((4 * (size_t)Wb * (Wb + 1) * 2 + 7) / 8 + 1) & ~(size_t)1); }
+__host__ __device__ inline size_t solve_rowsrc_doubles(int rows) { return ((3 * (size_t)rows * 4 + 15) / 16) * 2; }
+
 __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveParams P) {
     extern __shared__ double smem[];
     __shared__ unsigned int s_item;
@@ -1392,20 +1395,28 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
     const int N = P.N;
     double *scr = P.scratch + (int64_t)blockIdx.x * P.scratch_stride;
     double *Z = scr + P.off_z;                 // [nbp][N] forward-substituted right-hand sides
-    // shared layout: Lp[2][WrMax][LP_PITCH] | Zb[8][N] | invd[8] | strips | window A | window RHS
-    const int WbMax = solve_wb(P.bmax), WrMax = 8 * (WbMax + 1), PitchMax = WrMax + 2;
+    // shared layout: Lp[2][WrMax][LP_PITCH] | Zb[8][N] | invd[2][8] | rinv[2][8] | strips | row sources | window A | window RHS
+    const int WbMax = solve_wb(P.bmax), WrMax = 8 * (WbMax + 1);
     double *Lp0 = smem;
     double *Zb = Lp0 + 2 * (size_t)WrMax * LP_PITCH;
-    double *invd = Zb + 8 * (size_t)N;
-    unsigned short *strips = reinterpret_cast<unsigned short *>(invd + 8);
-    double *sm_rest = invd + 8 + (((4 * WbMax * (WbMax + 1) * 2 + 7) / 8 + 1) & ~1);
+    double *invd0 = Zb + 8 * (size_t)N;
+    double *rinv0 = invd0 + 16;
+    unsigned short *strips = reinterpret_cast<unsigned short *>(rinv0 + 16);
+    int32_t *rsl = reinterpret_cast<int32_t *>(rinv0 + 16 + solve_strip_doubles(WbMax));   // [nmax8] obs slot or -1
+    int32_t *rxr = rsl + P.rows_smem;                                                      // [nmax8] state row
+    int32_t *rxi = rxr + P.rows_smem;                                                      // [nmax8] state row if interior, else -1
+    double *sm_rest = rinv0 + 16 + solve_strip_doubles(WbMax) + solve_rowsrc_doubles(P.rows_smem);
     double *Aw = P.a_in_smem ? sm_rest : scr + P.off_win_a;
     double *Rw = P.r_in_smem ? (P.a_in_smem ? sm_rest + P.a_doubles : sm_rest) : scr + P.off_win_r;
-    (void)PitchMax;
     const unsigned nf = (unsigned)(P.f1 - P.f0);
     const int total_items = (int)nf * P.ntiles_owned;
-    const int G = nthreads / N > 0 ? nthreads / N : 1;     // row groups for the per-member updates
-    const int m_f = tid % N, g_f = tid / N;
+    // per-member updates: G row groups of N threads; warp 0 is kept free of them when the remaining threads hold
+    // as many groups (it factors the next diagonal block meanwhile)
+    const int G0 = nthreads / N > 0 ? nthreads / N : 1;
+    const int goff = (nthreads - 32) / N >= G0 ? 32 : 0;
+    const int G = G0;
+    const int m_f = (tid - goff) % N, g_f = tid >= goff ? (tid - goff) / N : G;
+    const int zoff = nthreads >= 256 ? 128 : 0;               // the threads solving the right-hand sides in (b)
 
     for (;;) {
         __syncthreads();
@@ -1443,73 +1454,128 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
             while (rem >= 8 * (Wb - q)) { rem -= 8 * (Wb - q); ++q; }
             strips[s] = (unsigned short)((q << 10) | (8 * q + rem));
         }
-        // load block row R (8 rows of A and of the right-hand side) into its window slot
-        auto load_block_row = [&](int R) {
+        // where each physical row's right-hand side and analysis row live (resolves the index chain once)
+        const bool rows_cached = 8 * nb <= P.rows_smem;
+        if (rows_cached) {
+            for (int i = tid; i < 8 * nb; i += nthreads) {
+                int sl = -1, xr = 0, xi = -1;
+                if (i < n) {
+                    const int il = iphys[i];
+                    sl = slotf[il]; xr = srow[il]; xi = inter[il] ? xr : -1;
+                }
+                rsl[i] = sl; rxr[i] = xr; rxi[i] = xi;
+            }
+            __syncthreads();
+        }
+        // block row R (8 rows of A and of the right-hand side): fetch into registers, commit to its window slot
+        const bool pf = rows_cached && 8 * Wr <= 2 * nthreads && 8 * N <= 2 * nthreads;
+        double fa[2], fy[2], fx[2], fr[2];
+        auto rhs_value = [&](int i, int m) {
+            double v = 0.0;
+            if (i < n) {
+                const int il = iphys[i];
+                const int sl = slotf[il];
+                if (sl >= 0) v = (P.Ys[(int64_t)sl * N + m] - Xf[(int64_t)srow[il] * N + m]) * (1.0 / P.rdiag[sl]);
+            }
+            return v;
+        };
+        auto fetch_block_row = [&](int R) {
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const int e = tid + k * nthreads;
+                fa[k] = 0.0; fy[k] = 0.0; fx[k] = 0.0; fr[k] = 0.0;
+                if (e < 8 * Wr) {
+                    const int rr = e / Wr, ee = e - rr * Wr, i = 8 * R + rr;
+                    fa[k] = (i < n) ? band[(int64_t)i * Wr + ee] : ((ee == 8 * Wb + rr) ? 1.0 : 0.0);   // padding row: identity
+                }
+                if (e < 8 * N) {
+                    const int rr = e / N, m = e - rr * N, i = 8 * R + rr;
+                    const int sl = rsl[i];
+                    if (sl >= 0) { fy[k] = P.Ys[(int64_t)sl * N + m]; fx[k] = Xf[(int64_t)rxr[i] * N + m]; fr[k] = P.rdiag[sl]; }
+                }
+            }
+        };
+        auto commit_block_row = [&](int R) {
             const int rs = (R % nslot) * 8;
             const int rot = (((R - Wb) % nslot) + nslot) % nslot * 8;   // window column of band entry 0
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const int e = tid + k * nthreads;
+                if (e < 8 * Wr) {
+                    const int rr = e / Wr, ee = e - rr * Wr;
+                    int cc = rot + ee; if (cc >= Wr) cc -= Wr;
+                    Aw[(size_t)(rs + rr) * pitch + cc] = fa[k];
+                }
+                if (e < 8 * N) {
+                    const int rr = e / N, m = e - rr * N;
+                    Rw[(size_t)(rs + rr) * N + m] = (fr[k] != 0.0) ? (fy[k] - fx[k]) * (1.0 / fr[k]) : 0.0;
+                }
+            }
+        };
+        auto load_block_row = [&](int R) {
+            if (pf) { fetch_block_row(R); commit_block_row(R); return; }
+            const int rs = (R % nslot) * 8;
+            const int rot = (((R - Wb) % nslot) + nslot) % nslot * 8;
             for (int e = tid; e < 8 * Wr; e += nthreads) {
                 const int rr = e / Wr, ee = e - rr * Wr, i = 8 * R + rr;
-                double v;
-                if (i < n) v = band[(int64_t)i * Wr + ee];
-                else v = (ee == 8 * Wb + rr) ? 1.0 : 0.0;              // padding row: identity
+                const double v = (i < n) ? band[(int64_t)i * Wr + ee] : ((ee == 8 * Wb + rr) ? 1.0 : 0.0);
                 int cc = rot + ee; if (cc >= Wr) cc -= Wr;
                 Aw[(size_t)(rs + rr) * pitch + cc] = v;
             }
             for (int e = tid; e < 8 * N; e += nthreads) {
-                const int rr = e / N, m = e - rr * N, i = 8 * R + rr;
-                double v = 0.0;
-                if (i < n) {
-                    const int il = iphys[i];
-                    const int sl = slotf[il];
-                    if (sl >= 0) v = (P.Ys[(int64_t)sl * N + m] - Xf[(int64_t)srow[il] * N + m]) * (1.0 / P.rdiag[sl]);
-                }
-                Rw[(size_t)(rs + rr) * N + m] = v;
+                const int rr = e / N, m = e - rr * N;
+                Rw[(size_t)(rs + rr) * N + m] = rhs_value(8 * R + rr, m);
             }
         };
         for (int R = 0; R <= Wb && R < nb; ++R) load_block_row(R);
         __syncthreads();
 
         // ---- forward: blocked Cholesky + forward substitution --------------------------------
-        double *Lp = Lp0;
         double pivmax = 0.0;                         // largest pivot so far (warp 0 tracks it redundantly per lane)
+        // 8x8 Cholesky of diagonal block J (warp 0): L_JJ into rows 0..7 of panel buffer J & 1, 1/diag into invd
+        auto factor_diag = [&](int J) {
+            const int sJ = (J % nslot) * 8;
+            double *Lp = Lp0 + (size_t)(J & 1) * WrMax * LP_PITCH;
+            double *invd = invd0 + 8 * (J & 1);
+            double *Dg = Aw + (size_t)sJ * pitch + sJ;
+            for (int c = 0; c < 8; ++c) {
+                double piv = Dg[(size_t)c * pitch + c];
+                // A = T~^T D^-1 T~ + H^T R^-1 H is positive semi-definite by construction, so a pivot at
+                // or below the rounding level of the largest pivot seen is cancellation noise, not
+                // indefiniteness: clamp it (counted) instead of failing.  NaN / inf still fail.
+                if (!(piv == piv) || !(fabs(piv) < DBL_MAX)) { if (lane == 0) s_fail = 2; }
+                else if (!(piv > 1e-13 * pivmax)) {
+                    if (pivmax == 0.0) { if (lane == 0) s_fail = 1; }           // non-positive leading entry
+                    else { piv = 1e-13 * pivmax; if (lane == 0) atomicAdd(P.counter + 1, 1u); }
+                }
+                pivmax = fmax(pivmax, piv);
+                const double inv = 1.0 / sqrt(piv);
+                __syncwarp();
+                if (lane > c && lane < 8) Dg[(size_t)lane * pitch + c] *= inv;
+                if (lane == c) { Dg[(size_t)c * pitch + c] = piv * inv; invd[c] = inv; }
+                __syncwarp();
+                // rank-1 update of the remaining lower triangle: element (r, c2), c < c2 <= r < 8
+                for (int e = lane; e < 64; e += 32) {
+                    const int r = e >> 3, c2 = e & 7;
+                    if (c2 > c && c2 <= r) Dg[(size_t)r * pitch + c2] -= Dg[(size_t)r * pitch + c] * Dg[(size_t)c2 * pitch + c];
+                }
+                __syncwarp();
+            }
+            for (int e = lane; e < 64; e += 32) {
+                const int r = e >> 3, c = e & 7;
+                Lp[r * LP_PITCH + c] = (c <= r) ? Dg[(size_t)r * pitch + c] : 0.0;
+            }
+        };
+        if (tid < 32) factor_diag(0);
+        __syncthreads();
         for (int J = 0; J < nb; ++J) {
+            if (s_fail) break;
+            double *Lp = Lp0 + (size_t)(J & 1) * WrMax * LP_PITCH;
+            const double *invd = invd0 + 8 * (J & 1);
             const int sJ = (J % nslot) * 8;
             const int s1 = ((J + 1) % nslot) * 8;      // window row of panel row r is wrap(s1 + r)
             const int below = (nb - 1 - J < Wb ? nb - 1 - J : Wb) * 8;     // panel rows under the diagonal block
-            // (a) 8x8 Cholesky of the diagonal block, warp 0, result in Lp rows 0..7
-            if (tid < 32) {
-                double *Dg = Aw + (size_t)sJ * pitch + sJ;
-                for (int c = 0; c < 8; ++c) {
-                    double piv = Dg[(size_t)c * pitch + c];
-                    // A = T~^T D^-1 T~ + H^T R^-1 H is positive semi-definite by construction, so a pivot at
-                    // or below the rounding level of the largest pivot seen is cancellation noise, not
-                    // indefiniteness: clamp it (counted) instead of failing.  NaN / inf still fail.
-                    if (!(piv == piv) || !(fabs(piv) < DBL_MAX)) { if (lane == 0) s_fail = 2; }
-                    else if (!(piv > 1e-13 * pivmax)) {
-                        if (pivmax == 0.0) { if (lane == 0) s_fail = 1; }           // non-positive leading entry
-                        else { piv = 1e-13 * pivmax; if (lane == 0) atomicAdd(P.counter + 1, 1u); }
-                    }
-                    pivmax = fmax(pivmax, piv);
-                    const double inv = 1.0 / sqrt(piv);
-                    __syncwarp();
-                    if (lane > c && lane < 8) Dg[(size_t)lane * pitch + c] *= inv;
-                    if (lane == c) { Dg[(size_t)c * pitch + c] = piv * inv; invd[c] = inv; }
-                    __syncwarp();
-                    // rank-1 update of the remaining lower triangle: element (r, c2), c < c2 <= r < 8
-                    for (int e = lane; e < 64; e += 32) {
-                        const int r = e >> 3, c2 = e & 7;
-                        if (c2 > c && c2 <= r) Dg[(size_t)r * pitch + c2] -= Dg[(size_t)r * pitch + c] * Dg[(size_t)c2 * pitch + c];
-                    }
-                    __syncwarp();
-                }
-                for (int e = lane; e < 64; e += 32) {
-                    const int r = e >> 3, c = e & 7;
-                    Lp[r * LP_PITCH + c] = (c <= r) ? Dg[(size_t)r * pitch + c] : 0.0;
-                }
-            }
-            __syncthreads();
-            if (s_fail) break;
-            // (b) panel rows: x L_JJ^T = a ; right-hand sides: L_JJ z = b
+            // (b) panel rows: x L_JJ^T = a ; right-hand sides: L_JJ z = b (another set of threads)
             for (int r = tid; r < below; r += nthreads) {
                 int wr = s1 + r; if (wr >= Wr) wr -= Wr;
                 const double *arow = Aw + (size_t)wr * pitch + sJ;
@@ -1524,7 +1590,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
 #pragma unroll
                 for (int c = 0; c < 8; ++c) Lp[(8 + r) * LP_PITCH + c] = x[c];
             }
-            for (int m = tid; m < N; m += nthreads) {
+            for (int m = tid >= zoff ? tid - zoff : tid + nthreads - zoff; m < N; m += nthreads) {
                 double z[8];
 #pragma unroll
                 for (int c = 0; c < 8; ++c) {
@@ -1537,15 +1603,18 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
                 }
             }
             __syncthreads();
+            // (e) the next block row goes into the slot of block row J (retired by the barrier above): the
+            // global loads are issued here and land behind the updates below
+            const bool more = J + Wb + 1 < nb;
+            if (more && pf) fetch_block_row(J + Wb + 1);
             // L block -> global (overwrites the A rows of block J, already consumed)
             for (int e = tid; e < (8 + below) * 8; e += nthreads)
                 band[(int64_t)8 * J * Wr + e] = Lp[(e >> 3) * LP_PITCH + (e & 7)];
-            // (c) trailing update, 1x8 strips: A[i, 8q..8q+7] -= L[i,:] . L[8q..8q+7,:]^T
-            const int ns_live = 4 * (below >> 3) * ((below >> 3) + 1);
-            for (int s = tid; s < nstrips; s += nthreads) {
+            // (c) trailing update, 1x8 strips: A[i, 8q..8q+7] -= L[i,:] . L[8q..8q+7,:]^T.  Strips beyond the first
+            // round go to the last threads, so warp 0 (which owns the next diagonal block) finishes first.
+            for (int s = tid, round = 0; s < nstrips; ++round, s = round * nthreads + (nthreads - 1 - tid)) {
                 const int q = strips[s] >> 10, r = strips[s] & 1023;
                 if (r >= below) continue;
-                (void)ns_live;
                 const double2 *li2 = reinterpret_cast<const double2 *>(Lp + (8 + r) * LP_PITCH);
                 const double2 l01 = li2[0], l23 = li2[1], l45 = li2[2], l67 = li2[3];
                 int wr = s1 + r; if (wr >= Wr) wr -= Wr;
@@ -1567,6 +1636,9 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
                 a2[0] = make_double2(acc[0], acc[1]); a2[1] = make_double2(acc[2], acc[3]);
                 a2[2] = make_double2(acc[4], acc[5]); a2[3] = make_double2(acc[6], acc[7]);
             }
+            // (a) warp 0 owns the strips of the next diagonal block (q = 0, r < 8): it factors that block now,
+            // while the other warps update the right-hand sides
+            if (tid < 32 && J + 1 < nb) { __syncwarp(); factor_diag(J + 1); }
             // (d) right-hand sides of the rows below: one member per thread, rows strided by G
             if (g_f < G) {
                 double z[8];
@@ -1583,8 +1655,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
                     *bp = d;
                 }
             }
-            // (e) bring in the next block row (its slot held block row J, now retired)
-            if (J + Wb + 1 < nb) load_block_row(J + Wb + 1);
+            if (more) { if (pf) commit_block_row(J + Wb + 1); else load_block_row(J + Wb + 1); }
             __syncthreads();
         }
         if (s_fail) {
@@ -1594,18 +1665,53 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
 
         // ---- backward: L^T x = z blockwise, Xa = Xb + dx on interior rows --------------------
         double *red = Aw;                       // [G][8][N] partial sums (the A window is dead now)
-        auto load_panel = [&](int J, double *dst) {
+        const bool pfb = 8 * Wr <= 2 * nthreads;
+        double fl2[2];
+        auto fetch_panel = [&](int J) {
             const int below = (nb - 1 - J < Wb ? nb - 1 - J : Wb) * 8;
-            for (int e = tid; e < (8 + below) * 8; e += nthreads)
-                dst[(e >> 3) * LP_PITCH + (e & 7)] = band[(int64_t)8 * J * Wr + e];
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const int e = tid + k * nthreads;
+                fl2[k] = (e < (8 + below) * 8) ? band[(int64_t)8 * J * Wr + e] : 0.0;
+            }
         };
-        load_panel(nb - 1, Lp0);
+        auto commit_panel = [&](int J, double *dst, double *rinv) {
+            const int below = (nb - 1 - J < Wb ? nb - 1 - J : Wb) * 8;
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const int e = tid + k * nthreads;
+                if (e < (8 + below) * 8) {
+                    dst[(e >> 3) * LP_PITCH + (e & 7)] = fl2[k];
+                    if (e < 64 && (e >> 3) == (e & 7)) rinv[e & 7] = 1.0 / fl2[k];
+                }
+            }
+        };
+        auto load_panel = [&](int J, double *dst, double *rinv) {
+            if (pfb) { fetch_panel(J); commit_panel(J, dst, rinv); return; }
+            const int below = (nb - 1 - J < Wb ? nb - 1 - J : Wb) * 8;
+            for (int e = tid; e < (8 + below) * 8; e += nthreads) {
+                const double v = band[(int64_t)8 * J * Wr + e];
+                dst[(e >> 3) * LP_PITCH + (e & 7)] = v;
+                if (e < 64 && (e >> 3) == (e & 7)) rinv[e & 7] = 1.0 / v;
+            }
+        };
+        load_panel(nb - 1, Lp0, rinv0);
         __syncthreads();
         for (int J = nb - 1; J >= 0; --J) {
-            const double *Lc = Lp0 + (size_t)((nb - 1 - J) & 1) * WrMax * LP_PITCH;
-            double *Ln = Lp0 + (size_t)((nb - J) & 1) * WrMax * LP_PITCH;
+            const int cur = (nb - 1 - J) & 1;
+            const double *Lc = Lp0 + (size_t)cur * WrMax * LP_PITCH;
+            const double *rinvc = rinv0 + 8 * cur;
+            double *Ln = Lp0 + (size_t)(cur ^ 1) * WrMax * LP_PITCH;
             const int below = (nb - 1 - J < Wb ? nb - 1 - J : Wb) * 8;
             const int s1 = ((J + 1) % nslot) * 8;
+            // this block's forward-substituted right-hand sides and the next panel: issued now, used after the sums
+            const int mz = tid >= zoff ? tid - zoff : tid + nthreads - zoff;
+            double zreg[8];
+            if (mz < N) {
+#pragma unroll
+                for (int c = 0; c < 8; ++c) zreg[c] = Z[(int64_t)(8 * J + c) * N + mz];
+            }
+            if (J > 0 && pfb) fetch_panel(J - 1);
             if (g_f < G) {
                 double acc[8];
 #pragma unroll
@@ -1622,21 +1728,24 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
 #pragma unroll
                 for (int c = 0; c < 8; ++c) red[((size_t)g_f * 8 + c) * N + m_f] = acc[c];
             }
-            if (J > 0) load_panel(J - 1, Ln);
+            if (J > 0) { if (pfb) commit_panel(J - 1, Ln, rinv0 + 8 * (cur ^ 1)); else load_panel(J - 1, Ln, rinv0 + 8 * (cur ^ 1)); }
             __syncthreads();
-            for (int m = tid; m < N; m += nthreads) {
+            for (int m = mz; m < N; m += nthreads) {
                 double x[8];
 #pragma unroll
                 for (int c = 7; c >= 0; --c) {
-                    double s = Z[(int64_t)(8 * J + c) * N + m];
+                    double s = (m == mz) ? zreg[c] : Z[(int64_t)(8 * J + c) * N + m];
                     for (int g = 0; g < G; ++g) s -= red[((size_t)g * 8 + c) * N + m];
 #pragma unroll
                     for (int c2 = c + 1; c2 < 8; ++c2) s -= Lc[c2 * LP_PITCH + c] * x[c2];
-                    x[c] = s / Lc[c * LP_PITCH + c];
+                    x[c] = s * rinvc[c];
                     if (!(fabs(x[c]) < DBL_MAX)) s_fail = 2;        // non-finite analysis increment (benign race)
                     const int i = 8 * J + c;
                     Rw[(size_t)((J % nslot) * 8 + c) * N + m] = x[c];
-                    if (i < n) {
+                    if (rows_cached) {
+                        const int xi = rxi[i];
+                        if (xi >= 0) { const int64_t gidx = (int64_t)xi * N + m; Xaf[gidx] = Xf[gidx] + x[c]; }
+                    } else if (i < n) {
                         const int il = iphys[i];
                         if (inter[il]) {
                             const int64_t gidx = (int64_t)srow[il] * N + m;
@@ -1654,12 +1763,14 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
 // Scratch / shared-memory layout chosen on the host.
 static size_t solve_fixed_doubles(const SolveParams &p) {
     const int Wb = solve_wb(p.bmax), Wr = 8 * (Wb + 1);
-    return 2 * (size_t)Wr * LP_PITCH + 8 * (size_t)p.N + 8 + (((4 * (size_t)Wb * (Wb + 1) * 2 + 7) / 8 + 1) & ~(size_t)1);
+    return 2 * (size_t)Wr * LP_PITCH + 8 * (size_t)p.N + 32 + solve_strip_doubles(Wb) + solve_rowsrc_doubles(p.rows_smem);
 }
 
 int64_t solve_plan_scratch(SolveParams &p, int64_t nmax, size_t smem_limit) {
     const int64_t Wb = solve_wb(p.bmax), Wr = 8 * (Wb + 1), pitch = Wr + 2;
     const int G = SOLVE_THREADS / p.N > 0 ? SOLVE_THREADS / p.N : 1;
+    // per-row source tables in shared memory (3 x int32 per row) for tiles of up to 4096 rows
+    p.rows_smem = nmax <= 4096 ? (int)((nmax + 7) / 8 * 8) : 0;
     const size_t fixed = solve_fixed_doubles(p) * sizeof(double) + 64;
     // the A window doubles as the [G][8][N] reduction buffer of the backward pass
     const size_t a_doubles = std::max<size_t>((size_t)(Wr * pitch), (size_t)G * 8 * p.N);
