@@ -1302,8 +1302,8 @@ __global__ void __launch_bounds__(ASM_WARPS * 32) assemble_band_kernel(const Sol
 
 // Tile-cooperative form of K3a: one CTA per (field, tile).  The tile's T values, the physical column of every
 // entry, D and the row pointers are staged in shared memory once, so the index chase of every row of A runs at
-// shared-memory latency; each warp then assembles rows exactly as assemble_band_kernel does (same order of
-// additions, bitwise the same band).  Used whenever the staging fits (launch_assemble_band decides).
+// shared-memory latency; each warp then assembles rows as assemble_band_kernel does (same order of additions; 1/D is
+// formed once per row instead of one division per term).  Used whenever the staging fits (launch_assemble_band decides).
 #define ASMT_THREADS 512
 
 __host__ __device__ inline size_t asm_tile_smem_bytes(int nmax, int nnzmax, int bmax) {
@@ -1337,7 +1337,7 @@ __global__ void __launch_bounds__(ASMT_THREADS) assemble_band_tile_kernel(const 
     const double *Tf = P.T + (int64_t)f * P.nnz + e0;
     const double *Df = P.D + (int64_t)f * P.nloc + base;
     const int32_t *phys = P.phys + base;
-    for (int i = tid; i < n; i += ASMT_THREADS) { sD[i] = Df[i]; sPhys[i] = (uint16_t)phys[i]; }
+    for (int i = tid; i < n; i += ASMT_THREADS) { sD[i] = 1.0 / Df[i]; sPhys[i] = (uint16_t)phys[i]; }
     for (int i = tid; i <= n; i += ASMT_THREADS) sRow[i] = (int32_t)(P.row_ptr[base + i] - e0);
     for (int e = tid; e < nz; e += ASMT_THREADS) { sT[e] = Tf[e]; sK[e] = (uint16_t)phys[P.col_idx[e0 + e]]; }
     __syncthreads();
@@ -1361,7 +1361,7 @@ __global__ void __launch_bounds__(ASMT_THREADS) assemble_band_tile_kernel(const 
                 int j; double tji;
                 if (eb < 0) { j = i; tji = 1.0; }
                 else { j = __shfl_sync(FULL, jl, ee); tji = sT[__shfl_sync(FULL, sl, ee)]; }
-                const double sc = tji / sD[j];
+                const double sc = tji * sD[j];
                 const int q0 = sRow[j];
                 const int cnt = sRow[j + 1] - q0;
                 for (int m = lane - 1; m < cnt; m += 32) {
@@ -1397,9 +1397,10 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
     double *Z = scr + P.off_z;                 // [nbp][N] forward-substituted right-hand sides
     // shared layout: Lp[2][WrMax][LP_PITCH] | Zb[8][N] | invd[2][8] | rinv[2][8] | strips | row sources | window A | window RHS
     const int WbMax = solve_wb(P.bmax), WrMax = 8 * (WbMax + 1);
+    const int NR = P.nr_pitch;                 // member pitch of Zb / the RHS window / red: >= 8 ceil(N/8), = 8 mod 16
     double *Lp0 = smem;
     double *Zb = Lp0 + 2 * (size_t)WrMax * LP_PITCH;
-    double *invd0 = Zb + 8 * (size_t)N;
+    double *invd0 = Zb + 8 * (size_t)NR;
     double *rinv0 = invd0 + 16;
     unsigned short *strips = reinterpret_cast<unsigned short *>(rinv0 + 16);
     int32_t *rsl = reinterpret_cast<int32_t *>(rinv0 + 16 + solve_strip_doubles(WbMax));   // [nmax8] obs slot or -1
@@ -1410,12 +1411,9 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
     double *Rw = P.r_in_smem ? (P.a_in_smem ? sm_rest + P.a_doubles : sm_rest) : scr + P.off_win_r;
     const unsigned nf = (unsigned)(P.f1 - P.f0);
     const int total_items = (int)nf * P.ntiles_owned;
-    // per-member updates: G row groups of N threads; warp 0 is kept free of them when the remaining threads hold
-    // as many groups (it factors the next diagonal block meanwhile)
-    const int G0 = nthreads / N > 0 ? nthreads / N : 1;
-    const int goff = (nthreads - 32) / N >= G0 ? 32 : 0;
-    const int G = G0;
-    const int m_f = (tid - goff) % N, g_f = tid >= goff ? (tid - goff) / N : G;
+    const int warp = tid >> 5, nwarps = nthreads >> 5;
+    const int g8 = lane >> 2, t4 = lane & 3;                  // mma.m8n8k4 fragment coordinates of this lane
+    const int nct = (N + 7) >> 3;                             // 8-member column tiles
     const int zoff = nthreads >= 256 ? 128 : 0;               // the threads solving the right-hand sides in (b)
 
     for (;;) {
@@ -1447,12 +1445,11 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
             continue;
         }
 
-        // strips of the trailing update: (block column q, panel row r >= 8 q), ordered by q then r
-        const int nstrips = 4 * Wb * (Wb + 1);
-        for (int s = tid; s < nstrips; s += nthreads) {
-            int q = 0, rem = s;
-            while (rem >= 8 * (Wb - q)) { rem -= 8 * (Wb - q); ++q; }
-            strips[s] = (unsigned short)((q << 10) | (8 * q + rem));
+        // 8x8 tiles (rb, cb <= rb) of the trailing update, ordered by rb: the live ones are a prefix
+        for (int s = tid; s < Wb * (Wb + 1) / 2; s += nthreads) {
+            int rb = 0, rem = s;
+            while (rem > rb) { rem -= rb + 1; ++rb; }
+            strips[s] = (unsigned short)((rb << 8) | rem);
         }
         // where each physical row's right-hand side and analysis row live (resolves the index chain once)
         const bool rows_cached = 8 * nb <= P.rows_smem;
@@ -1508,7 +1505,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
                 }
                 if (e < 8 * N) {
                     const int rr = e / N, m = e - rr * N;
-                    Rw[(size_t)(rs + rr) * N + m] = (fr[k] != 0.0) ? (fy[k] - fx[k]) * (1.0 / fr[k]) : 0.0;
+                    Rw[(size_t)(rs + rr) * NR + m] = (fr[k] != 0.0) ? (fy[k] - fx[k]) * (1.0 / fr[k]) : 0.0;
                 }
             }
         };
@@ -1524,7 +1521,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
             }
             for (int e = tid; e < 8 * N; e += nthreads) {
                 const int rr = e / N, m = e - rr * N;
-                Rw[(size_t)(rs + rr) * N + m] = rhs_value(8 * R + rr, m);
+                Rw[(size_t)(rs + rr) * NR + m] = rhs_value(8 * R + rr, m);
             }
         };
         for (int R = 0; R <= Wb && R < nb; ++R) load_block_row(R);
@@ -1594,11 +1591,11 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
                 double z[8];
 #pragma unroll
                 for (int c = 0; c < 8; ++c) {
-                    double s = Rw[(size_t)(sJ + c) * N + m];
+                    double s = Rw[(size_t)(sJ + c) * NR + m];
 #pragma unroll
                     for (int c2 = 0; c2 < c; ++c2) s -= z[c2] * Lp[c * LP_PITCH + c2];
                     z[c] = s * invd[c];
-                    Zb[c * N + m] = z[c];
+                    Zb[c * NR + m] = z[c];
                     Z[(int64_t)(8 * J + c) * N + m] = z[c];
                 }
             }
@@ -1610,49 +1607,48 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
             // L block -> global (overwrites the A rows of block J, already consumed)
             for (int e = tid; e < (8 + below) * 8; e += nthreads)
                 band[(int64_t)8 * J * Wr + e] = Lp[(e >> 3) * LP_PITCH + (e & 7)];
-            // (c) trailing update, 1x8 strips: A[i, 8q..8q+7] -= L[i,:] . L[8q..8q+7,:]^T.  Strips beyond the first
-            // round go to the last threads, so warp 0 (which owns the next diagonal block) finishes first.
-            for (int s = tid, round = 0; s < nstrips; ++round, s = round * nthreads + (nthreads - 1 - tid)) {
-                const int q = strips[s] >> 10, r = strips[s] & 1023;
-                if (r >= below) continue;
-                const double2 *li2 = reinterpret_cast<const double2 *>(Lp + (8 + r) * LP_PITCH);
-                const double2 l01 = li2[0], l23 = li2[1], l45 = li2[2], l67 = li2[3];
-                int wr = s1 + r; if (wr >= Wr) wr -= Wr;
-                int wc = s1 + 8 * q; if (wc >= Wr) wc -= Wr;
-                double *arow = Aw + (size_t)wr * pitch + wc;
-                double2 *a2 = reinterpret_cast<double2 *>(arow);
-                double acc[8];
-                { const double2 t0 = a2[0], t1 = a2[1], t2 = a2[2], t3 = a2[3];
-                  acc[0] = t0.x; acc[1] = t0.y; acc[2] = t1.x; acc[3] = t1.y; acc[4] = t2.x; acc[5] = t2.y; acc[6] = t3.x; acc[7] = t3.y; }
-#pragma unroll
-                for (int jj = 0; jj < 8; ++jj) {
-                    const double2 *lj2 = reinterpret_cast<const double2 *>(Lp + (8 + 8 * q + jj) * LP_PITCH);
-                    const double2 m01 = lj2[0], m23 = lj2[1], m45 = lj2[2], m67 = lj2[3];
-                    double d = acc[jj];
-                    d = fma(-l01.x, m01.x, d); d = fma(-l01.y, m01.y, d); d = fma(-l23.x, m23.x, d); d = fma(-l23.y, m23.y, d);
-                    d = fma(-l45.x, m45.x, d); d = fma(-l45.y, m45.y, d); d = fma(-l67.x, m67.x, d); d = fma(-l67.y, m67.y, d);
-                    acc[jj] = d;
-                }
-                a2[0] = make_double2(acc[0], acc[1]); a2[1] = make_double2(acc[2], acc[3]);
-                a2[2] = make_double2(acc[4], acc[5]); a2[3] = make_double2(acc[6], acc[7]);
-            }
-            // (a) warp 0 owns the strips of the next diagonal block (q = 0, r < 8): it factors that block now,
-            // while the other warps update the right-hand sides
-            if (tid < 32 && J + 1 < nb) { __syncwarp(); factor_diag(J + 1); }
-            // (d) right-hand sides of the rows below: one member per thread, rows strided by G
-            if (g_f < G) {
-                double z[8];
-#pragma unroll
-                for (int c = 0; c < 8; ++c) z[c] = Zb[c * N + m_f];
-                for (int r = g_f; r < below; r += G) {
-                    const double2 *li2 = reinterpret_cast<const double2 *>(Lp + (8 + r) * LP_PITCH);
-                    const double2 l01 = li2[0], l23 = li2[1], l45 = li2[2], l67 = li2[3];
-                    int wr = s1 + r; if (wr >= Wr) wr -= Wr;
-                    double *bp = Rw + (size_t)wr * N + m_f;
-                    double d = *bp;
-                    d = fma(-l01.x, z[0], d); d = fma(-l01.y, z[1], d); d = fma(-l23.x, z[2], d); d = fma(-l23.y, z[3], d);
-                    d = fma(-l45.x, z[4], d); d = fma(-l45.y, z[5], d); d = fma(-l67.x, z[6], d); d = fma(-l67.y, z[7], d);
-                    *bp = d;
+            // (c) trailing update A[rb, cb] -= L_rb L_cb^T and (d) right-hand sides B[rb, :] -= L_rb Z_J, by 8x8 tiles on
+            // the FP64 tensor cores (mma.m8n8k4: two k-steps per tile).  Warp 0 owns tile (0, 0) = the next diagonal
+            // block and (a) factors it right away, while the other warps share the remaining tiles.
+            {
+                const int nbl = below >> 3;
+                const int nC = nbl * (nbl + 1) / 2;
+                auto l_frag = [&](int blk, double &a0, double &a1) {
+                    const double *l = Lp + (8 + 8 * blk + g8) * LP_PITCH + t4;
+                    a0 = l[0]; a1 = l[4];
+                };
+                auto c_tile = [&](int rb, int cb) {
+                    double a0, a1, b0, b1;
+                    l_frag(rb, a0, a1);
+                    l_frag(cb, b0, b1);
+                    int wr0 = s1 + 8 * rb; if (wr0 >= Wr) wr0 -= Wr;
+                    int wc0 = s1 + 8 * cb; if (wc0 >= Wr) wc0 -= Wr;
+                    double2 *cp = reinterpret_cast<double2 *>(Aw + (size_t)(wr0 + g8) * pitch + wc0 + 2 * t4);
+                    double2 c = *cp;
+                    mma_f64(c.x, c.y, -a0, b0);
+                    mma_f64(c.x, c.y, -a1, b1);
+                    *cp = c;
+                };
+                if (warp == 0) {
+                    if (nbl > 0) c_tile(0, 0);
+                    if (J + 1 < nb) { __syncwarp(); factor_diag(J + 1); }
+                } else {
+                    for (int u = warp; u < nC + nbl * nct; u += nwarps - 1) {
+                        if (u < nC) {
+                            const int rc = strips[u];
+                            c_tile(rc >> 8, rc & 255);
+                        } else {
+                            const int rb = (u - nC) / nct, ct = (u - nC) - rb * nct;
+                            double a0, a1;
+                            l_frag(rb, a0, a1);
+                            int wr0 = s1 + 8 * rb; if (wr0 >= Wr) wr0 -= Wr;
+                            double2 *cp = reinterpret_cast<double2 *>(Rw + (size_t)(wr0 + g8) * NR + 8 * ct + 2 * t4);
+                            double2 c = *cp;
+                            mma_f64(c.x, c.y, -a0, Zb[(size_t)t4 * NR + 8 * ct + g8]);
+                            mma_f64(c.x, c.y, -a1, Zb[(size_t)(4 + t4) * NR + 8 * ct + g8]);
+                            *cp = c;
+                        }
+                    }
                 }
             }
             if (more) { if (pf) commit_block_row(J + Wb + 1); else load_block_row(J + Wb + 1); }
@@ -1664,7 +1660,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
         }
 
         // ---- backward: L^T x = z blockwise, Xa = Xb + dx on interior rows --------------------
-        double *red = Aw;                       // [G][8][N] partial sums (the A window is dead now)
+        double *red = Aw;                       // [8][NR]: L_below^T x of the current block (the A window is dead now)
         const bool pfb = 8 * Wr <= 2 * nthreads;
         double fl2[2];
         auto fetch_panel = [&](int J) {
@@ -1712,21 +1708,18 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
                 for (int c = 0; c < 8; ++c) zreg[c] = Z[(int64_t)(8 * J + c) * N + mz];
             }
             if (J > 0 && pfb) fetch_panel(J - 1);
-            if (g_f < G) {
-                double acc[8];
-#pragma unroll
-                for (int c = 0; c < 8; ++c) acc[c] = 0.0;
-                for (int r = g_f; r < below; r += G) {
-                    const double2 *li2 = reinterpret_cast<const double2 *>(Lc + (8 + r) * LP_PITCH);
-                    const double2 l01 = li2[0], l23 = li2[1], l45 = li2[2], l67 = li2[3];
-                    int wr = s1 + r; if (wr >= Wr) wr -= Wr;
-                    const double x = Rw[(size_t)wr * N + m_f];
-                    acc[0] = fma(l01.x, x, acc[0]); acc[1] = fma(l01.y, x, acc[1]); acc[2] = fma(l23.x, x, acc[2]);
-                    acc[3] = fma(l23.y, x, acc[3]); acc[4] = fma(l45.x, x, acc[4]); acc[5] = fma(l45.y, x, acc[5]);
-                    acc[6] = fma(l67.x, x, acc[6]); acc[7] = fma(l67.y, x, acc[7]);
+            // S[c][m] = sum_r L[r][c] x[r][m] over the rows below, one 8-member column tile per warp on the tensor
+            // cores (two independent accumulators over alternate k-steps)
+            for (int ct = warp; ct < nct; ct += nwarps) {
+                double p0 = 0.0, p1 = 0.0, q0 = 0.0, q1 = 0.0;
+                for (int k0 = 0; k0 < below; k0 += 8) {
+                    int w = s1 + k0; if (w >= Wr) w -= Wr;
+                    const double *lk = Lc + (8 + k0 + t4) * LP_PITCH + g8;
+                    const double *xk = Rw + (size_t)(w + t4) * NR + 8 * ct + g8;
+                    mma_f64(p0, p1, lk[0], xk[0]);
+                    mma_f64(q0, q1, lk[4 * LP_PITCH], xk[(size_t)4 * NR]);
                 }
-#pragma unroll
-                for (int c = 0; c < 8; ++c) red[((size_t)g_f * 8 + c) * N + m_f] = acc[c];
+                *reinterpret_cast<double2 *>(red + (size_t)g8 * NR + 8 * ct + 2 * t4) = make_double2(p0 + q0, p1 + q1);
             }
             if (J > 0) { if (pfb) commit_panel(J - 1, Ln, rinv0 + 8 * (cur ^ 1)); else load_panel(J - 1, Ln, rinv0 + 8 * (cur ^ 1)); }
             __syncthreads();
@@ -1735,13 +1728,13 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
 #pragma unroll
                 for (int c = 7; c >= 0; --c) {
                     double s = (m == mz) ? zreg[c] : Z[(int64_t)(8 * J + c) * N + m];
-                    for (int g = 0; g < G; ++g) s -= red[((size_t)g * 8 + c) * N + m];
+                    s -= red[(size_t)c * NR + m];
 #pragma unroll
                     for (int c2 = c + 1; c2 < 8; ++c2) s -= Lc[c2 * LP_PITCH + c] * x[c2];
                     x[c] = s * rinvc[c];
                     if (!(fabs(x[c]) < DBL_MAX)) s_fail = 2;        // non-finite analysis increment (benign race)
                     const int i = 8 * J + c;
-                    Rw[(size_t)((J % nslot) * 8 + c) * N + m] = x[c];
+                    Rw[(size_t)((J % nslot) * 8 + c) * NR + m] = x[c];
                     if (rows_cached) {
                         const int xi = rxi[i];
                         if (xi >= 0) { const int64_t gidx = (int64_t)xi * N + m; Xaf[gidx] = Xf[gidx] + x[c]; }
@@ -1763,25 +1756,28 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
 // Scratch / shared-memory layout chosen on the host.
 static size_t solve_fixed_doubles(const SolveParams &p) {
     const int Wb = solve_wb(p.bmax), Wr = 8 * (Wb + 1);
-    return 2 * (size_t)Wr * LP_PITCH + 8 * (size_t)p.N + 32 + solve_strip_doubles(Wb) + solve_rowsrc_doubles(p.rows_smem);
+    return 2 * (size_t)Wr * LP_PITCH + 8 * (size_t)p.nr_pitch + 32 + solve_strip_doubles(Wb) + solve_rowsrc_doubles(p.rows_smem);
 }
 
 int64_t solve_plan_scratch(SolveParams &p, int64_t nmax, size_t smem_limit) {
     const int64_t Wb = solve_wb(p.bmax), Wr = 8 * (Wb + 1), pitch = Wr + 2;
-    const int G = SOLVE_THREADS / p.N > 0 ? SOLVE_THREADS / p.N : 1;
+    // member pitch: covers the padded 8-member tiles and is 8 mod 16, so fragment loads of consecutive rows fall
+    // into different bank halves
+    p.nr_pitch = (p.N + 7) / 8 * 8;
+    if (p.nr_pitch % 16 == 0) p.nr_pitch += 8;
     // per-row source tables in shared memory (3 x int32 per row) for tiles of up to 4096 rows
     p.rows_smem = nmax <= 4096 ? (int)((nmax + 7) / 8 * 8) : 0;
     const size_t fixed = solve_fixed_doubles(p) * sizeof(double) + 64;
-    // the A window doubles as the [G][8][N] reduction buffer of the backward pass
-    const size_t a_doubles = std::max<size_t>((size_t)(Wr * pitch), (size_t)G * 8 * p.N);
-    const size_t r_bytes = (size_t)(Wr * p.N) * sizeof(double);
+    // the A window doubles as the [8][nr_pitch] buffer of the backward pass
+    const size_t a_doubles = std::max<size_t>((size_t)(Wr * pitch), (size_t)8 * p.nr_pitch);
+    const size_t r_bytes = (size_t)(Wr * p.nr_pitch) * sizeof(double);
     p.a_doubles = (int64_t)a_doubles;
     p.a_in_smem = fixed + a_doubles * sizeof(double) <= smem_limit;
     p.r_in_smem = fixed + (p.a_in_smem ? a_doubles * sizeof(double) : 0) + r_bytes <= smem_limit;
     int64_t off = 0;
     p.off_z = off; off += ((nmax + 7) / 8 * 8) * p.N;
     p.off_win_a = off; if (!p.a_in_smem) off += (int64_t)a_doubles;
-    p.off_win_r = off; if (!p.r_in_smem) off += Wr * p.N;
+    p.off_win_r = off; if (!p.r_in_smem) off += Wr * p.nr_pitch;
     off = (off + 15) & ~(int64_t)15;
     p.scratch_stride = off;
     return off;
@@ -1789,11 +1785,10 @@ int64_t solve_plan_scratch(SolveParams &p, int64_t nmax, size_t smem_limit) {
 
 static size_t solve_smem_bytes(const SolveParams &p) {
     const int64_t Wb = solve_wb(p.bmax), Wr = 8 * (Wb + 1), pitch = Wr + 2;
-    const int G = SOLVE_THREADS / p.N > 0 ? SOLVE_THREADS / p.N : 1;
     size_t rest = 0;
     if (p.a_in_smem) rest += (size_t)p.a_doubles;
-    if (p.r_in_smem) rest += (size_t)(Wr * p.N);
-    (void)G; (void)pitch;
+    if (p.r_in_smem) rest += (size_t)(Wr * p.nr_pitch);
+    (void)pitch;
     return (solve_fixed_doubles(p) + rest) * sizeof(double);
 }
 

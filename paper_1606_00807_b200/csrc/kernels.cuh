@@ -42,6 +42,7 @@ struct SolveParams {
     int a_in_smem, r_in_smem;  // window placement
     int64_t a_doubles;         // size of the A window / backward reduction buffer
     int rows_smem;             // rows the per-row source tables in shared memory hold (0: none)
+    int nr_pitch;              // member pitch of the right-hand-side window (see solve_plan_scratch)
     int32_t *status;           // [nfields * ntiles]
     unsigned int *counter;
     int assemble_only;         // 1: K3a writes T^T D^-1 T without the observation term, for every owned tile
