@@ -1414,7 +1414,6 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
     const int warp = tid >> 5, nwarps = nthreads >> 5;
     const int g8 = lane >> 2, t4 = lane & 3;                  // mma.m8n8k4 fragment coordinates of this lane
     const int nct = (N + 7) >> 3;                             // 8-member column tiles
-    const int zoff = nthreads >= 256 ? 128 : 0;               // the threads solving the right-hand sides in (b)
 
     for (;;) {
         __syncthreads();
@@ -1467,6 +1466,13 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
         // block row R (8 rows of A and of the right-hand side): fetch into registers, commit to its window slot
         const bool pf = rows_cached && 8 * Wr <= 2 * nthreads && 8 * N <= 2 * nthreads;
         double fa[2], fy[2], fx[2], fr[2];
+        int ea_r[2], ea_e[2], er_r[2], er_m[2];     // this thread's (row, entry) of the A part and (row, member) of the RHS part
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int e = tid + k * nthreads;
+            ea_r[k] = e / Wr; ea_e[k] = e - ea_r[k] * Wr;
+            er_r[k] = e / N; er_m[k] = e - er_r[k] * N;
+        }
         auto rhs_value = [&](int i, int m) {
             double v = 0.0;
             if (i < n) {
@@ -1479,40 +1485,36 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
         auto fetch_block_row = [&](int R) {
 #pragma unroll
             for (int k = 0; k < 2; ++k) {
-                const int e = tid + k * nthreads;
                 fa[k] = 0.0; fy[k] = 0.0; fx[k] = 0.0; fr[k] = 0.0;
-                if (e < 8 * Wr) {
-                    const int rr = e / Wr, ee = e - rr * Wr, i = 8 * R + rr;
-                    fa[k] = (i < n) ? band[(int64_t)i * Wr + ee] : ((ee == 8 * Wb + rr) ? 1.0 : 0.0);   // padding row: identity
+                if (ea_r[k] < 8) {
+                    const int i = 8 * R + ea_r[k];
+                    fa[k] = (i < n) ? band[(int64_t)i * Wr + ea_e[k]] : ((ea_e[k] == 8 * Wb + ea_r[k]) ? 1.0 : 0.0);   // padding row: identity
                 }
-                if (e < 8 * N) {
-                    const int rr = e / N, m = e - rr * N, i = 8 * R + rr;
+                if (er_r[k] < 8) {
+                    const int i = 8 * R + er_r[k];
                     const int sl = rsl[i];
-                    if (sl >= 0) { fy[k] = P.Ys[(int64_t)sl * N + m]; fx[k] = Xf[(int64_t)rxr[i] * N + m]; fr[k] = P.rdiag[sl]; }
+                    if (sl >= 0) {
+                        fy[k] = P.Ys[(int64_t)sl * N + er_m[k]]; fx[k] = Xf[(int64_t)rxr[i] * N + er_m[k]]; fr[k] = P.rdiag[sl];
+                    }
                 }
             }
         };
-        auto commit_block_row = [&](int R) {
-            const int rs = (R % nslot) * 8;
-            const int rot = (((R - Wb) % nslot) + nslot) % nslot * 8;   // window column of band entry 0
+        // rs: window slot (row offset) of block row R; rot: window column of its band entry 0
+        auto commit_block_row = [&](int rs, int rot) {
 #pragma unroll
             for (int k = 0; k < 2; ++k) {
-                const int e = tid + k * nthreads;
-                if (e < 8 * Wr) {
-                    const int rr = e / Wr, ee = e - rr * Wr;
-                    int cc = rot + ee; if (cc >= Wr) cc -= Wr;
-                    Aw[(size_t)(rs + rr) * pitch + cc] = fa[k];
+                if (ea_r[k] < 8) {
+                    int cc = rot + ea_e[k]; if (cc >= Wr) cc -= Wr;
+                    Aw[(size_t)(rs + ea_r[k]) * pitch + cc] = fa[k];
                 }
-                if (e < 8 * N) {
-                    const int rr = e / N, m = e - rr * N;
-                    Rw[(size_t)(rs + rr) * NR + m] = (fr[k] != 0.0) ? (fy[k] - fx[k]) * (1.0 / fr[k]) : 0.0;
-                }
+                if (er_r[k] < 8)
+                    Rw[(size_t)(rs + er_r[k]) * NR + er_m[k]] = (fr[k] != 0.0) ? (fy[k] - fx[k]) * (1.0 / fr[k]) : 0.0;
             }
         };
         auto load_block_row = [&](int R) {
-            if (pf) { fetch_block_row(R); commit_block_row(R); return; }
             const int rs = (R % nslot) * 8;
             const int rot = (((R - Wb) % nslot) + nslot) % nslot * 8;
+            if (pf) { fetch_block_row(R); commit_block_row(rs, rot); return; }
             for (int e = tid; e < 8 * Wr; e += nthreads) {
                 const int rr = e / Wr, ee = e - rr * Wr, i = 8 * R + rr;
                 const double v = (i < n) ? band[(int64_t)i * Wr + ee] : ((ee == 8 * Wb + rr) ? 1.0 : 0.0);
@@ -1528,15 +1530,23 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
         __syncthreads();
 
         // ---- forward: blocked Cholesky + forward substitution --------------------------------
+        // Everything but the 8x8 diagonal factorisation runs as 8x8 tiles on the FP64 tensor cores (mma.m8n8k4, two
+        // k-steps per tile).  Panel buffer J & 1 holds, in rows 0..7, L_JJ (lower) and the strict lower part of
+        // L_JJ^-1 transposed into the upper triangle (diagonal of the inverse in invd); rows 8.. hold the panel.
         double pivmax = 0.0;                         // largest pivot so far (warp 0 tracks it redundantly per lane)
-        // 8x8 Cholesky of diagonal block J (warp 0): L_JJ into rows 0..7 of panel buffer J & 1, 1/diag into invd
-        auto factor_diag = [&](int J) {
-            const int sJ = (J % nslot) * 8;
-            double *Lp = Lp0 + (size_t)(J & 1) * WrMax * LP_PITCH;
-            double *invd = invd0 + 8 * (J & 1);
-            double *Dg = Aw + (size_t)sJ * pitch + sJ;
+        // Diagonal block J (warp 0): lane r (mod 8) keeps row r of the block and of the running inverse in registers;
+        // right-looking Cholesky with the same eliminations applied to the identity.
+        auto factor_diag = [&](int sJ, int buf) {
+            double *Lp = Lp0 + (size_t)buf * WrMax * LP_PITCH;
+            double *invd = invd0 + 8 * buf;
+            const double *Dg = Aw + (size_t)sJ * pitch + sJ;
+            const int r = lane & 7;
+            double a[8], v[8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) { a[c] = (c <= r) ? Dg[(size_t)r * pitch + c] : 0.0; v[c] = (c == r) ? 1.0 : 0.0; }
+#pragma unroll
             for (int c = 0; c < 8; ++c) {
-                double piv = Dg[(size_t)c * pitch + c];
+                double piv = __shfl_sync(FULL, a[c], c);
                 // A = T~^T D^-1 T~ + H^T R^-1 H is positive semi-definite by construction, so a pivot at
                 // or below the rounding level of the largest pivot seen is cancellation noise, not
                 // indefiniteness: clamp it (counted) instead of failing.  NaN / inf still fail.
@@ -1546,57 +1556,67 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
                     else { piv = 1e-13 * pivmax; if (lane == 0) atomicAdd(P.counter + 1, 1u); }
                 }
                 pivmax = fmax(pivmax, piv);
-                const double inv = 1.0 / sqrt(piv);
-                __syncwarp();
-                if (lane > c && lane < 8) Dg[(size_t)lane * pitch + c] *= inv;
-                if (lane == c) { Dg[(size_t)c * pitch + c] = piv * inv; invd[c] = inv; }
-                __syncwarp();
-                // rank-1 update of the remaining lower triangle: element (r, c2), c < c2 <= r < 8
-                for (int e = lane; e < 64; e += 32) {
-                    const int r = e >> 3, c2 = e & 7;
-                    if (c2 > c && c2 <= r) Dg[(size_t)r * pitch + c2] -= Dg[(size_t)r * pitch + c] * Dg[(size_t)c2 * pitch + c];
+                const double inv = rsqrt(piv);
+                a[c] = (r == c) ? piv * inv : a[c] * inv;             // column c of L
+#pragma unroll
+                for (int k = 0; k <= c; ++k) if (r == c) v[k] *= inv; // row c of L^-1 is final
+#pragma unroll
+                for (int c2 = c + 1; c2 < 8; ++c2) {
+                    const double lc2 = __shfl_sync(FULL, a[c], c2);
+                    if (r >= c2) a[c2] -= a[c] * lc2;
                 }
-                __syncwarp();
+#pragma unroll
+                for (int k = 0; k <= c; ++k) {
+                    const double vk = __shfl_sync(FULL, v[k], c);
+                    if (r > c) v[k] -= a[c] * vk;
+                }
             }
-            for (int e = lane; e < 64; e += 32) {
-                const int r = e >> 3, c = e & 7;
-                Lp[r * LP_PITCH + c] = (c <= r) ? Dg[(size_t)r * pitch + c] : 0.0;
+            if (lane < 8) {
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    if (c <= r) Lp[r * LP_PITCH + c] = a[c];          // L[r][c]
+                    if (c < r) Lp[c * LP_PITCH + r] = v[c];           // (L^-1)[r][c] at the transposed place
+                }
+                invd[r] = v[r];
             }
         };
-        if (tid < 32) factor_diag(0);
+        // (L_JJ^-1)[i][j] from a panel buffer
+        auto linv = [&](const double *Lp, const double *dg, int i, int j) {
+            return i == j ? dg[i] : (i > j ? Lp[j * LP_PITCH + i] : 0.0);
+        };
+        if (warp == 0) factor_diag(0, 0);
         __syncthreads();
+        int sJ = 0;                                    // window slot of block row J
         for (int J = 0; J < nb; ++J) {
             if (s_fail) break;
             double *Lp = Lp0 + (size_t)(J & 1) * WrMax * LP_PITCH;
             const double *invd = invd0 + 8 * (J & 1);
-            const int sJ = (J % nslot) * 8;
-            const int s1 = ((J + 1) % nslot) * 8;      // window row of panel row r is wrap(s1 + r)
+            int s1 = sJ + 8; if (s1 >= Wr) s1 = 0;     // window row of panel row r is wrap(s1 + r)
             const int below = (nb - 1 - J < Wb ? nb - 1 - J : Wb) * 8;     // panel rows under the diagonal block
-            // (b) panel rows: x L_JJ^T = a ; right-hand sides: L_JJ z = b (another set of threads)
-            for (int r = tid; r < below; r += nthreads) {
-                int wr = s1 + r; if (wr >= Wr) wr -= Wr;
-                const double *arow = Aw + (size_t)wr * pitch + sJ;
-                double x[8];
-#pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                    double s = arow[c];
-#pragma unroll
-                    for (int c2 = 0; c2 < c; ++c2) s -= x[c2] * Lp[c * LP_PITCH + c2];
-                    x[c] = s * invd[c];
-                }
-#pragma unroll
-                for (int c = 0; c < 8; ++c) Lp[(8 + r) * LP_PITCH + c] = x[c];
-            }
-            for (int m = tid >= zoff ? tid - zoff : tid + nthreads - zoff; m < N; m += nthreads) {
-                double z[8];
-#pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                    double s = Rw[(size_t)(sJ + c) * NR + m];
-#pragma unroll
-                    for (int c2 = 0; c2 < c; ++c2) s -= z[c2] * Lp[c * LP_PITCH + c2];
-                    z[c] = s * invd[c];
-                    Zb[c * NR + m] = z[c];
-                    Z[(int64_t)(8 * J + c) * N + m] = z[c];
+            const int nbl = below >> 3;
+            // (b) panel X = A_panel L_JJ^-T (one 8-row block per unit) and right-hand sides Z_J = L_JJ^-1 B_J (one
+            // 8-member tile per unit)
+            {
+                const double li0 = linv(Lp, invd, g8, t4), li1 = linv(Lp, invd, g8, 4 + t4);
+                for (int u = warp; u < nbl + nct; u += nwarps) {
+                    double c0 = 0.0, c1 = 0.0;
+                    if (u < nbl) {
+                        int wr0 = s1 + 8 * u; if (wr0 >= Wr) wr0 -= Wr;
+                        const double *ar = Aw + (size_t)(wr0 + g8) * pitch + sJ + t4;
+                        mma_f64(c0, c1, ar[0], li0);
+                        mma_f64(c0, c1, ar[4], li1);
+                        *reinterpret_cast<double2 *>(Lp + (8 + 8 * u + g8) * LP_PITCH + 2 * t4) = make_double2(c0, c1);
+                    } else {
+                        const int ct = u - nbl;
+                        const double *br = Rw + (size_t)(sJ + t4) * NR + 8 * ct + g8;
+                        mma_f64(c0, c1, li0, br[0]);
+                        mma_f64(c0, c1, li1, br[(size_t)4 * NR]);
+                        const int col = 8 * ct + 2 * t4;
+                        *reinterpret_cast<double2 *>(Zb + (size_t)g8 * NR + col) = make_double2(c0, c1);
+                        double *zg = Z + (int64_t)(8 * J + g8) * N + col;
+                        if (col < N) zg[0] = c0;
+                        if (col + 1 < N) zg[1] = c1;
+                    }
                 }
             }
             __syncthreads();
@@ -1607,11 +1627,9 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
             // L block -> global (overwrites the A rows of block J, already consumed)
             for (int e = tid; e < (8 + below) * 8; e += nthreads)
                 band[(int64_t)8 * J * Wr + e] = Lp[(e >> 3) * LP_PITCH + (e & 7)];
-            // (c) trailing update A[rb, cb] -= L_rb L_cb^T and (d) right-hand sides B[rb, :] -= L_rb Z_J, by 8x8 tiles on
-            // the FP64 tensor cores (mma.m8n8k4: two k-steps per tile).  Warp 0 owns tile (0, 0) = the next diagonal
-            // block and (a) factors it right away, while the other warps share the remaining tiles.
+            // (c) trailing update A[rb, cb] -= L_rb L_cb^T and (d) right-hand sides B[rb, :] -= L_rb Z_J.  Warp 0 owns
+            // tile (0, 0) = the next diagonal block and (a) factors it right away; the other warps share the rest.
             {
-                const int nbl = below >> 3;
                 const int nC = nbl * (nbl + 1) / 2;
                 auto l_frag = [&](int blk, double &a0, double &a1) {
                     const double *l = Lp + (8 + 8 * blk + g8) * LP_PITCH + t4;
@@ -1631,28 +1649,35 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
                 };
                 if (warp == 0) {
                     if (nbl > 0) c_tile(0, 0);
-                    if (J + 1 < nb) { __syncwarp(); factor_diag(J + 1); }
+                    if (J + 1 < nb) { __syncwarp(); factor_diag(s1, (J + 1) & 1); }
                 } else {
-                    for (int u = warp; u < nC + nbl * nct; u += nwarps - 1) {
-                        if (u < nC) {
-                            const int rc = strips[u];
-                            c_tile(rc >> 8, rc & 255);
-                        } else {
-                            const int rb = (u - nC) / nct, ct = (u - nC) - rb * nct;
-                            double a0, a1;
-                            l_frag(rb, a0, a1);
-                            int wr0 = s1 + 8 * rb; if (wr0 >= Wr) wr0 -= Wr;
-                            double2 *cp = reinterpret_cast<double2 *>(Rw + (size_t)(wr0 + g8) * NR + 8 * ct + 2 * t4);
-                            double2 c = *cp;
-                            mma_f64(c.x, c.y, -a0, Zb[(size_t)t4 * NR + 8 * ct + g8]);
-                            mma_f64(c.x, c.y, -a1, Zb[(size_t)(4 + t4) * NR + 8 * ct + g8]);
-                            *cp = c;
-                        }
+                    for (int u = warp; u < nC; u += nwarps - 1) {
+                        const int rc = strips[u];
+                        c_tile(rc >> 8, rc & 255);
+                    }
+                    // (d): units (rb, ct), rb-major, continuing the round-robin where (c) stopped
+                    int u = warp - 1 - (nC - 1) % (nwarps - 1);
+                    if (nC == 0) u = warp - 1;
+                    if (u < 0) u += nwarps - 1;
+                    int rb = 0, ct = u;
+                    while (ct >= nct) { ct -= nct; ++rb; }
+                    while (rb < nbl) {
+                        double a0, a1;
+                        l_frag(rb, a0, a1);
+                        int wr0 = s1 + 8 * rb; if (wr0 >= Wr) wr0 -= Wr;
+                        double2 *cp = reinterpret_cast<double2 *>(Rw + (size_t)(wr0 + g8) * NR + 8 * ct + 2 * t4);
+                        double2 c = *cp;
+                        mma_f64(c.x, c.y, -a0, Zb[(size_t)t4 * NR + 8 * ct + g8]);
+                        mma_f64(c.x, c.y, -a1, Zb[(size_t)(4 + t4) * NR + 8 * ct + g8]);
+                        *cp = c;
+                        ct += nwarps - 1;
+                        while (ct >= nct) { ct -= nct; ++rb; }
                     }
                 }
             }
-            if (more) { if (pf) commit_block_row(J + Wb + 1); else load_block_row(J + Wb + 1); }
+            if (more) { if (pf) commit_block_row(sJ, s1); else load_block_row(J + Wb + 1); }
             __syncthreads();
+            sJ = s1;
         }
         if (s_fail) {
             if (tid == 0) P.status[(int64_t)f * P.ntiles + t] = s_fail;
@@ -1660,7 +1685,9 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
         }
 
         // ---- backward: L^T x = z blockwise, Xa = Xb + dx on interior rows --------------------
-        double *red = Aw;                       // [8][NR]: L_below^T x of the current block (the A window is dead now)
+        // One warp per 8-member tile: S = L_below^T x (chain of tensor-core products over the rows below), then
+        // x_J = L_JJ^-T (z_J - S) with the stored inverse; one barrier per block.
+        double *red = Aw;                       // [8][NR] staging of z_J - S (the A window is dead now)
         const bool pfb = 8 * Wr <= 2 * nthreads;
         double fl2[2];
         auto fetch_panel = [&](int J) {
@@ -1693,23 +1720,22 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
         };
         load_panel(nb - 1, Lp0, rinv0);
         __syncthreads();
+        int sB = ((nb - 1) % nslot) * 8;                // window slot of block row J
         for (int J = nb - 1; J >= 0; --J) {
             const int cur = (nb - 1 - J) & 1;
             const double *Lc = Lp0 + (size_t)cur * WrMax * LP_PITCH;
             const double *rinvc = rinv0 + 8 * cur;
             double *Ln = Lp0 + (size_t)(cur ^ 1) * WrMax * LP_PITCH;
             const int below = (nb - 1 - J < Wb ? nb - 1 - J : Wb) * 8;
-            const int s1 = ((J + 1) % nslot) * 8;
-            // this block's forward-substituted right-hand sides and the next panel: issued now, used after the sums
-            const int mz = tid >= zoff ? tid - zoff : tid + nthreads - zoff;
-            double zreg[8];
-            if (mz < N) {
-#pragma unroll
-                for (int c = 0; c < 8; ++c) zreg[c] = Z[(int64_t)(8 * J + c) * N + mz];
+            int s1 = sB + 8; if (s1 >= Wr) s1 = 0;
+            // this warp's first tile of z_J (B-fragment layout) and the next panel: issued now, used after the sums
+            double zf0 = 0.0, zf1 = 0.0;
+            if (warp < nct) {
+                const int col = 8 * warp + g8;
+                if (col < N) { zf0 = Z[(int64_t)(8 * J + t4) * N + col]; zf1 = Z[(int64_t)(8 * J + 4 + t4) * N + col]; }
             }
             if (J > 0 && pfb) fetch_panel(J - 1);
-            // S[c][m] = sum_r L[r][c] x[r][m] over the rows below, one 8-member column tile per warp on the tensor
-            // cores (two independent accumulators over alternate k-steps)
+            const double lt0 = linv(Lc, rinvc, t4, g8), lt1 = linv(Lc, rinvc, 4 + t4, g8);   // (L_JJ^-T)[g8][k]
             for (int ct = warp; ct < nct; ct += nwarps) {
                 double p0 = 0.0, p1 = 0.0, q0 = 0.0, q1 = 0.0;
                 for (int k0 = 0; k0 < below; k0 += 8) {
@@ -1719,35 +1745,36 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
                     mma_f64(p0, p1, lk[0], xk[0]);
                     mma_f64(q0, q1, lk[4 * LP_PITCH], xk[(size_t)4 * NR]);
                 }
-                *reinterpret_cast<double2 *>(red + (size_t)g8 * NR + 8 * ct + 2 * t4) = make_double2(p0 + q0, p1 + q1);
+                // S (C-fragment layout) -> shared -> B fragments of z_J - S, within the warp
+                double *rd = red + 8 * ct;
+                *reinterpret_cast<double2 *>(rd + (size_t)g8 * NR + 2 * t4) = make_double2(p0 + q0, p1 + q1);
+                __syncwarp();
+                if (ct != warp) {
+                    const int col = 8 * ct + g8;
+                    zf0 = zf1 = 0.0;
+                    if (col < N) { zf0 = Z[(int64_t)(8 * J + t4) * N + col]; zf1 = Z[(int64_t)(8 * J + 4 + t4) * N + col]; }
+                }
+                const double w0 = zf0 - rd[(size_t)t4 * NR + g8], w1 = zf1 - rd[(size_t)(4 + t4) * NR + g8];
+                double x0 = 0.0, x1 = 0.0;
+                mma_f64(x0, x1, lt0, w0);
+                mma_f64(x0, x1, lt1, w1);
+                const int col = 8 * ct + 2 * t4;
+                if (col < N && (!(fabs(x0) < DBL_MAX) || (col + 1 < N && !(fabs(x1) < DBL_MAX)))) s_fail = 2;   // benign race
+                *reinterpret_cast<double2 *>(Rw + (size_t)(sB + g8) * NR + col) = make_double2(x0, x1);
+                const int i = 8 * J + g8;
+                int xi = -1;
+                if (rows_cached) xi = rxi[i];
+                else if (i < n) { const int il = iphys[i]; if (inter[il]) xi = srow[il]; }
+                if (xi >= 0) {
+                    const int64_t gidx = (int64_t)xi * N + col;
+                    if (col < N) Xaf[gidx] = Xf[gidx] + x0;
+                    if (col + 1 < N) Xaf[gidx + 1] = Xf[gidx + 1] + x1;
+                }
+                __syncwarp();
             }
             if (J > 0) { if (pfb) commit_panel(J - 1, Ln, rinv0 + 8 * (cur ^ 1)); else load_panel(J - 1, Ln, rinv0 + 8 * (cur ^ 1)); }
             __syncthreads();
-            for (int m = mz; m < N; m += nthreads) {
-                double x[8];
-#pragma unroll
-                for (int c = 7; c >= 0; --c) {
-                    double s = (m == mz) ? zreg[c] : Z[(int64_t)(8 * J + c) * N + m];
-                    s -= red[(size_t)c * NR + m];
-#pragma unroll
-                    for (int c2 = c + 1; c2 < 8; ++c2) s -= Lc[c2 * LP_PITCH + c] * x[c2];
-                    x[c] = s * rinvc[c];
-                    if (!(fabs(x[c]) < DBL_MAX)) s_fail = 2;        // non-finite analysis increment (benign race)
-                    const int i = 8 * J + c;
-                    Rw[(size_t)((J % nslot) * 8 + c) * NR + m] = x[c];
-                    if (rows_cached) {
-                        const int xi = rxi[i];
-                        if (xi >= 0) { const int64_t gidx = (int64_t)xi * N + m; Xaf[gidx] = Xf[gidx] + x[c]; }
-                    } else if (i < n) {
-                        const int il = iphys[i];
-                        if (inter[il]) {
-                            const int64_t gidx = (int64_t)srow[il] * N + m;
-                            Xaf[gidx] = Xf[gidx] + x[c];
-                        }
-                    }
-                }
-            }
-            __syncthreads();
+            sB = sB == 0 ? Wr - 8 : sB - 8;
         }
         if (tid == 0) P.status[(int64_t)f * P.ntiles + t] = s_fail;
     }
