@@ -767,6 +767,234 @@ __global__ void __launch_bounds__(256, 1) regress_qr_kernel(const RegressParams 
     }
 }
 
+// ---- K2a, register-panel form ----------------------------------------------------------------
+// Left-looking blocked Householder QR of [A^T | y] (N x (p + 1)): eight columns at a time live in registers
+// (lane <-> rows lane + 32 s), gathered straight from the anomaly rows in global memory.  Every earlier
+// reflector is applied to the block from shared memory, two at a time (one pass of 16 dot products with the
+// transposing warp reduction), then the block is factored in registers and its R columns go straight to the
+// packed output.  Shared memory holds only the reflectors that later blocks still need (all but those of the
+// last block), so ten regressions are resident per SM instead of eight and the matrix itself never touches
+// shared memory.  The first block takes the (p + 1) mod 8 odd columns: it has no earlier reflectors to apply.
+#define QRP_NB 8
+
+__host__ __device__ inline size_t regress_qrp_ws_doubles(int N, int pmax) {
+    const int vcols = pmax - (QRP_NB - 1) > 1 ? pmax - (QRP_NB - 1) : 1;
+    const size_t d = (size_t)N * vcols + (size_t)pmax + (size_t)(pmax / 2 + 1);   // V | tau | g of the pairs
+    return (d + 1) & ~(size_t)1;
+}
+
+// c <- H2 H1 c for the eight block columns: c' = c - w1 v1, w1 = tau1 v1.c ; c'' = c' - w2 v2, w2 = tau2 (v2.c - w1 v2.v1)
+template <int S, int S0>
+__device__ __forceinline__ void qrp_apply2(double (&c)[QRP_NB][S], const double *V1, const double *V2, int N, double tau1,
+                                           double tau2, double g, int lane) {
+    double v1[S], v2[S], d1[QRP_NB], d2[QRP_NB];
+#pragma unroll
+    for (int s = S0; s < S; ++s) {
+        const int i = lane + 32 * s;
+        v1[s] = i < N ? V1[i] : 0.0;
+        v2[s] = i < N ? V2[i] : 0.0;
+    }
+#pragma unroll
+    for (int b = 0; b < QRP_NB; ++b) {
+        d1[b] = 0.0; d2[b] = 0.0;
+#pragma unroll
+        for (int s = S0; s < S; ++s) { d1[b] += v1[s] * c[b][s]; d2[b] += v2[s] * c[b][s]; }
+    }
+#pragma unroll
+    for (int b = 0; b < QRP_NB; b += 4) {
+        warp_sum4(d1[b], d1[b + 1], d1[b + 2], d1[b + 3], lane);
+        warp_sum4(d2[b], d2[b + 1], d2[b + 2], d2[b + 3], lane);
+    }
+#pragma unroll
+    for (int b = 0; b < QRP_NB; ++b) {
+        const double w1 = d1[b] * tau1;
+        const double w2 = (d2[b] - w1 * g) * tau2;
+#pragma unroll
+        for (int s = S0; s < S; ++s) c[b][s] -= w1 * v1[s] + w2 * v2[s];
+    }
+}
+
+template <int S, int S0>
+__device__ __forceinline__ void qrp_apply1(double (&c)[QRP_NB][S], const double *V1, int N, double tau1, int lane) {
+    double v1[S], d1[QRP_NB];
+#pragma unroll
+    for (int s = S0; s < S; ++s) { const int i = lane + 32 * s; v1[s] = i < N ? V1[i] : 0.0; }
+#pragma unroll
+    for (int b = 0; b < QRP_NB; ++b) {
+        d1[b] = 0.0;
+#pragma unroll
+        for (int s = S0; s < S; ++s) d1[b] += v1[s] * c[b][s];
+    }
+#pragma unroll
+    for (int b = 0; b < QRP_NB; b += 4) warp_sum4(d1[b], d1[b + 1], d1[b + 2], d1[b + 3], lane);
+#pragma unroll
+    for (int b = 0; b < QRP_NB; ++b) {
+        const double w1 = d1[b] * tau1;
+#pragma unroll
+        for (int s = S0; s < S; ++s) c[b][s] -= w1 * v1[s];
+    }
+}
+
+// Reflectors [k0, k1) from shared memory onto the block; slots below 32 S0 hold only zeros of v and are skipped.
+template <int S, int S0>
+__device__ __forceinline__ void qrp_apply_range(double (&c)[QRP_NB][S], const double *V, const double *tau, const double *gp,
+                                                int N, int k0, int k1, int lane) {
+    int k = k0;
+    if ((k & 1) && k < k1) { qrp_apply1<S, S0>(c, V + (size_t)k * N, N, tau[k], lane); ++k; }
+    for (; k + 1 < k1; k += 2)
+        qrp_apply2<S, S0>(c, V + (size_t)k * N, V + (size_t)(k + 1) * N, N, tau[k], tau[k + 1], gp[k >> 1], lane);
+    if (k < k1) qrp_apply1<S, S0>(c, V + (size_t)k * N, N, tau[k], lane);
+}
+
+template <int S>
+__global__ void __launch_bounds__(320, 1) regress_qr_panel_kernel(const RegressParams P) {
+    extern __shared__ double smem[];
+    const int lane = threadIdx.x & 31;
+    const int N = P.N, pmax = P.pmax;
+    double *V = smem + (size_t)(threadIdx.x >> 5) * regress_qrp_ws_doubles(N, pmax);
+    const int vcols = pmax - (QRP_NB - 1) > 1 ? pmax - (QRP_NB - 1) : 1;
+    double *tau = V + (size_t)N * vcols;
+    double *gp = tau + pmax;
+    const double denom = (double)(N - 1);
+    const unsigned nf = (unsigned)(P.f1 - P.f0);
+
+    for (;;) {
+        unsigned int wk = 0;
+        if (lane == 0) wk = atomicAdd(P.counter, 1u);
+        wk = __shfl_sync(FULL, wk, 0);
+        if ((int64_t)wk >= P.nwork) break;
+        const int q = P.work_order[wk / nf];
+        const int fl = (int)(wk % nf), f = P.f0 + fl;
+        const int64_t r0 = P.row_ptr[q];
+        const int p = (int)(P.row_ptr[q + 1] - r0);
+        const double *Uf = P.U + (int64_t)f * P.nstate2d * N;
+        const double *yrow = Uf + (int64_t)P.state_row[q] * N;
+        const int32_t *pred = P.pred_state + r0;
+
+        if (p == 0) {  // estimator.py:139-144
+            double s = 0.0;
+            for (int i = lane; i < N; i += 32) { const double v = yrow[i]; s += v * v; }
+            s = warp_sum(s) / denom;
+            if (lane == 0) {
+                P.D[(int64_t)f * P.nloc + q] = fmax(s, P.variance_floor);
+                if (P.flags) P.flags[(int64_t)f * P.nloc + q] = (s < P.variance_floor) ? 8 : 0;
+            }
+            continue;
+        }
+        const int K = p < N ? p : N;                     // reflectors
+        const int ncols = p + 1;                         // the last column is y
+        const int nstore = ncols - QRP_NB;               // reflectors j < nstore are applied to later blocks
+        double *out = P.Rq + (int64_t)fl * P.rq_stride + P.rq_ptr[q];
+
+        for (int o = 0; o < ncols;) {
+            const int nbc = (o == 0) ? ((ncols - 1) & (QRP_NB - 1)) + 1 : QRP_NB;
+            double c[QRP_NB][S];
+#pragma unroll
+            for (int b = 0; b < QRP_NB; ++b) {
+                const int j = o + b;
+                const double *src = (j < p) ? Uf + (int64_t)pred[j < p ? j : 0] * N : yrow;
+#pragma unroll
+                for (int s = 0; s < S; ++s) {
+                    const int i = lane + 32 * s;
+                    c[b][s] = (b < nbc && i < N) ? src[i] : 0.0;
+                }
+            }
+            // earlier reflectors, by ranges of dead slots
+            {
+                const int kprev = o < K ? o : K;
+                if (kprev > 0) {
+                    qrp_apply_range<S, 0>(c, V, tau, gp, N, 0, kprev < 32 ? kprev : 32, lane);
+                    if constexpr (S > 1) if (kprev > 32) qrp_apply_range<S, 1>(c, V, tau, gp, N, 32, kprev < 64 ? kprev : 64, lane);
+                    if constexpr (S > 2) if (kprev > 64) qrp_apply_range<S, 2>(c, V, tau, gp, N, 64, kprev < 96 ? kprev : 96, lane);
+                    if constexpr (S > 3) if (kprev > 96) qrp_apply_range<S, (S > 3 ? 3 : 0)>(c, V, tau, gp, N, 96, kprev, lane);
+                }
+            }
+            // factor the block in registers
+            double vp[S];                                   // reflector j - 1 (for the pair's v_j . v_{j-1})
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                const int i = lane + 32 * s;
+                vp[s] = (o > 0 && (o & 1) && o - 1 < K && i < N) ? V[(size_t)(o - 1) * N + i] : 0.0;
+            }
+#pragma unroll
+            for (int jj = 0; jj < QRP_NB; ++jj) {
+                const int j = o + jj;
+                if (jj < nbc && j < p && j < K) {
+                    // one batched reduction: |v|^2, x0, (v.v_prev, v_prev[j]), and per later column (v.c_b, c_b[j]);
+                    // the dots use the raw column and are corrected for v[j] = x0 - alpha afterwards
+                    double vr[S];
+                    double r[4 + 2 * (QRP_NB - 1)];
+#pragma unroll
+                    for (int e = 0; e < 4 + 2 * (QRP_NB - 1); ++e) r[e] = 0.0;
+#pragma unroll
+                    for (int s = 0; s < S; ++s) {
+                        const int i = lane + 32 * s;
+                        vr[s] = (i >= j) ? c[jj][s] : 0.0;
+                        r[0] += vr[s] * vr[s];
+                        r[2] += vr[s] * vp[s];
+                        if (i == j) { r[1] = vr[s]; r[3] = vp[s]; }
+#pragma unroll
+                        for (int b = jj + 1; b < QRP_NB; ++b) {
+                            r[4 + 2 * (b - jj - 1)] += vr[s] * c[b][s];
+                            if (i == j) r[5 + 2 * (b - jj - 1)] = c[b][s];
+                        }
+                    }
+#pragma unroll
+                    for (int e = 0; e < 4 + 2 * (QRP_NB - 1 - jj); e += 4) warp_sum4(r[e], r[e + 1], r[e + 2], r[e + 3], lane);
+                    const double x0 = r[1];
+                    const double nrm = sqrt(r[0]);
+                    const double alpha = nrm == 0.0 ? 0.0 : ((x0 >= 0.0) ? -nrm : nrm);
+                    const double tj = nrm == 0.0 ? 0.0 : 1.0 / (nrm * (nrm + fabs(x0)));   // 2 / v^T v
+#pragma unroll
+                    for (int s = 0; s < S; ++s) {
+                        const int i = lane + 32 * s;
+                        if (i == j) { vr[s] = x0 - alpha; c[jj][s] = alpha; }               // R[j][j]
+                    }
+#pragma unroll
+                    for (int b = jj + 1; b < QRP_NB; ++b) {
+                        const double w = (r[4 + 2 * (b - jj - 1)] - alpha * r[5 + 2 * (b - jj - 1)]) * tj;
+#pragma unroll
+                        for (int s = 0; s < S; ++s) c[b][s] -= w * vr[s];
+                    }
+                    if (j < nstore) {
+#pragma unroll
+                        for (int s = 0; s < S; ++s) { const int i = lane + 32 * s; if (i < N) V[(size_t)j * N + i] = vr[s]; }
+                        if (lane == 0) {
+                            tau[j] = tj;
+                            if (j & 1) gp[j >> 1] = r[2] - alpha * r[3];                    // v_j . v_{j-1} with the final v_j[j]
+                        }
+                    }
+#pragma unroll
+                    for (int s = 0; s < S; ++s) vp[s] = vr[s];
+                }
+            }
+            // finished columns -> packed output: R by columns (min(j + 1, K) entries), then c[0:K] and e2 for y
+#pragma unroll
+            for (int b = 0; b < QRP_NB; ++b) {
+                const int j = o + b;
+                if (b >= nbc) continue;
+                double *dst = out + packed_col_offset(j, K);
+                if (j < p) {
+                    const int h = j + 1 < K ? j + 1 : K;
+#pragma unroll
+                    for (int s = 0; s < S; ++s) { const int i = lane + 32 * s; if (i < h) dst[i] = c[b][s]; }
+                } else {
+                    double e2 = 0.0;
+#pragma unroll
+                    for (int s = 0; s < S; ++s) {
+                        const int i = lane + 32 * s;
+                        if (i < K) dst[i] = c[b][s]; else e2 += c[b][s] * c[b][s];       // rows >= N hold zeros
+                    }
+                    e2 = warp_sum(e2);
+                    if (lane == 0) dst[K] = e2;
+                }
+            }
+            __syncwarp();
+            o += nbc;
+        }
+    }
+}
+
 // ---- K2b: truncation probes + solve --------------------------------------------------------
 template <int PS>
 __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressParams P) {
@@ -1130,6 +1358,14 @@ static cudaError_t launch_qr_t(const RegressParams &p, int grid, int warps, size
     return cudaGetLastError();
 }
 
+template <int S>
+static cudaError_t launch_qrp_t(const RegressParams &p, int grid, int warps, size_t smem, cudaStream_t s) {
+    cudaError_t e = cudaFuncSetAttribute(regress_qr_panel_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    regress_qr_panel_kernel<S><<<grid, warps * 32, smem, s>>>(p);
+    return cudaGetLastError();
+}
+
 template <int PS>
 static cudaError_t launch_solve_t(const RegressParams &p, int grid, int warps, size_t smem, cudaStream_t s) {
     cudaError_t e = cudaFuncSetAttribute(regress_solve_kernel<PS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1146,7 +1382,23 @@ cudaError_t launch_regress(const RegressParams &p_in, int sm_count, size_t smem_
     cudaError_t e = cudaMemsetAsync(p.counter, 0, 2 * sizeof(unsigned int), s);
     if (e != cudaSuccess) return e;
     // K2a
-    {
+    const int S = (p.N + 31) / 32;
+    if (S <= 4 && !getenv("ENKFMC_QR_SMEM")) {
+        const size_t ws = regress_qrp_ws_doubles(p.N, p.pmax) * sizeof(double);
+        int warps = (int)(smem_limit / ws);
+        if (warps < 1) return cudaErrorInvalidConfiguration;
+        if (warps > 10) warps = 10;                    // <= 320 threads: up to 204 registers per thread
+        int64_t grid = sm_count;
+        const int64_t need = (p.nwork + warps - 1) / warps;
+        if (grid > need) grid = need;
+        switch (S) {
+            case 1: e = launch_qrp_t<1>(p, (int)grid, warps, ws * warps, s); break;
+            case 2: e = launch_qrp_t<2>(p, (int)grid, warps, ws * warps, s); break;
+            case 3: e = launch_qrp_t<3>(p, (int)grid, warps, ws * warps, s); break;
+            default: e = launch_qrp_t<4>(p, (int)grid, warps, ws * warps, s); break;
+        }
+        if (e != cudaSuccess) return e;
+    } else {
         const size_t ws = regress_qr_ws_doubles(p.N, p.pmax) * sizeof(double);
         int warps = (int)(smem_limit / ws);
         if (warps < 1) return cudaErrorInvalidConfiguration;
@@ -1157,7 +1409,6 @@ cudaError_t launch_regress(const RegressParams &p_in, int sm_count, size_t smem_
         int64_t grid = (int64_t)sm_count * ctas;
         const int64_t need = (p.nwork + warps - 1) / warps;
         if (grid > need) grid = need;
-        const int S = (p.N + 31) / 32;
         switch (S) {
             case 1: e = launch_qr_t<1>(p, (int)grid, warps, ws * warps, s); break;
             case 2: e = launch_qr_t<2>(p, (int)grid, warps, ws * warps, s); break;
