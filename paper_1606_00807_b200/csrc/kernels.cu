@@ -995,6 +995,231 @@ __global__ void __launch_bounds__(320, 1) regress_qr_panel_kernel(const RegressP
     }
 }
 
+// ---- K2a, tensor-core form ---------------------------------------------------------------------
+// Blocked Householder QR of [A^T | y] with the block of eight columns in registers in mma.m8n8k4 fragment
+// layout: lane (g8, t4) = (lane >> 2, lane & 3) owns column g8 of the block and the rows 8 mt + 4 u + t4
+// (m-tile mt, u in {0, 1}).  Earlier reflectors are applied eight at a time in compact WY form,
+//     C <- C - V T^T (V^T C),
+// as three chains of FP64 tensor-core products whose operands are the column registers themselves and
+// fragments of V (reflectors, shared memory) and T (8 x 8 per block, shared memory): with the row <-> n and
+// reflector <-> k index maps chosen below, the accumulator fragment of each product is exactly the A fragment
+// of the next, so no shuffles or transposes are needed.  The block itself is then factored in registers:
+// each reflector is broadcast by shuffles within the lanes sharing t4, one dot product per lane group gives
+// the column updates (groups right of the pivot) and the V^T V entries of the T recurrence (groups left of it).
+#define QRM_TP 12      // pitch of a T block: B-fragment loads (2 t4 + h) * 12 + g8 are conflict-free
+
+__host__ __device__ constexpr int qrm_vp(int N) {            // reflector pitch: >= 8 ceil(N / 8), = 4 mod 16
+    int v = (N + 7) / 8 * 8;
+    while (v % 16 != 4) ++v;
+    return v;
+}
+__host__ __device__ inline size_t regress_qrm_ws_doubles(int N, int pmax) {
+    const int nblk = pmax / 8 > 0 ? pmax / 8 : 1;         // reflector blocks that a later column block can need
+    return (size_t)nblk * 8 * qrm_vp(N) + (size_t)nblk * 8 * QRM_TP;
+}
+
+template <int NT>
+__global__ void __launch_bounds__(256, 1) regress_qr_mma_kernel(const RegressParams P) {
+    extern __shared__ double smem[];
+    const int lane = threadIdx.x & 31, g8 = lane >> 2, t4 = lane & 3;
+    const int N = P.N, pmax = P.pmax;
+    constexpr int VP = qrm_vp(8 * NT);                     // rows are padded to 8 NT (zeros beyond N)
+    const int nblk_cap = pmax / 8 > 0 ? pmax / 8 : 1;
+    double *Vs = smem + (size_t)(threadIdx.x >> 5) * regress_qrm_ws_doubles(8 * NT, pmax);
+    double *Ts = Vs + (size_t)nblk_cap * 8 * VP;
+    const double denom = (double)(N - 1);
+    const unsigned nf = (unsigned)(P.f1 - P.f0);
+    const int pig = 4 * (g8 & 1) + (g8 >> 1);              // row (within an m-tile) of accumulator column n = g8
+
+    for (;;) {
+        unsigned int wk = 0;
+        if (lane == 0) wk = atomicAdd(P.counter, 1u);
+        wk = __shfl_sync(FULL, wk, 0);
+        if ((int64_t)wk >= P.nwork) break;
+        const int q = P.work_order[wk / nf];
+        const int fl = (int)(wk % nf), f = P.f0 + fl;
+        const int64_t r0 = P.row_ptr[q];
+        const int p = (int)(P.row_ptr[q + 1] - r0);
+        const double *Uf = P.U + (int64_t)f * P.nstate2d * N;
+        const double *yrow = Uf + (int64_t)P.state_row[q] * N;
+        const int32_t *pred = P.pred_state + r0;
+
+        if (p == 0) {  // estimator.py:139-144
+            double s = 0.0;
+            for (int i = lane; i < N; i += 32) { const double v = yrow[i]; s += v * v; }
+            s = warp_sum(s) / denom;
+            if (lane == 0) {
+                P.D[(int64_t)f * P.nloc + q] = fmax(s, P.variance_floor);
+                if (P.flags) P.flags[(int64_t)f * P.nloc + q] = (s < P.variance_floor) ? 8 : 0;
+            }
+            continue;
+        }
+        const int K = p < N ? p : N;                     // reflectors
+        const int ncols = p + 1;                         // the last column is y
+        double *out = P.Rq + (int64_t)fl * P.rq_stride + P.rq_ptr[q];
+        double *yout = out + packed_col_offset(p, K);
+
+        for (int o = 0; o < ncols; o += 8) {
+            const int m0 = o >> 3;                       // m-tile holding the diagonal rows of this block
+            const bool stored = o + 8 < ncols;           // a later block will need these reflectors
+            const int j_own = o + g8;                    // this lane group's column
+            const bool isy = j_own == p;
+            double *dst = out + packed_col_offset(j_own < p ? j_own : p, K);
+            const int h = j_own < p ? (j_own + 1 < K ? j_own + 1 : K) : 0;    // R entries of my column (0: y or padding)
+            double c[NT][2];
+            {
+                const double *src = j_own < p ? Uf + (int64_t)pred[j_own < p ? j_own : 0] * N : yrow;
+#pragma unroll
+                for (int mt = 0; mt < NT; ++mt) {
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        const int row = 8 * mt + 4 * u + t4;
+                        c[mt][u] = (j_own < ncols && row < N) ? src[row] : 0.0;
+                    }
+                }
+            }
+            // ---- earlier reflector blocks: C <- C - V T^T (V^T C) ----
+            for (int ob = 0; ob < o && ob < K; ob += 8) {
+                const int mb = ob >> 3;
+                const double *Vb = Vs + (size_t)(ob + g8) * VP + t4;
+                double wa0 = 0.0, wa1 = 0.0, wb0 = 0.0, wb1 = 0.0, wc0 = 0.0, wc1 = 0.0, wd0 = 0.0, wd1 = 0.0;
+#pragma unroll
+                for (int mt = 0; mt < NT; ++mt) {
+                    if (mt >= mb) {
+                        if (mt & 1) { mma_f64(wc0, wc1, c[mt][0], Vb[8 * mt]); mma_f64(wd0, wd1, c[mt][1], Vb[8 * mt + 4]); }
+                        else { mma_f64(wa0, wa1, c[mt][0], Vb[8 * mt]); mma_f64(wb0, wb1, c[mt][1], Vb[8 * mt + 4]); }
+                    }
+                }
+                const double w0 = (wa0 + wb0) + (wc0 + wd0), w1 = (wa1 + wb1) + (wc1 + wd1);   // (C^T V)[g8][2 t4 + {0, 1}]
+                const double *Tb = Ts + (size_t)mb * 8 * QRM_TP;
+                double z0 = 0.0, z1 = 0.0;                                                    // (C^T V T)[g8][2 t4 + {0, 1}]
+                mma_f64(z0, z1, w0, Tb[(2 * t4) * QRM_TP + g8]);
+                mma_f64(z0, z1, w1, Tb[(2 * t4 + 1) * QRM_TP + g8]);
+                const double *V3 = Vs + (size_t)(ob + 2 * t4) * VP + pig;
+                z0 = -z0; z1 = -z1;
+#pragma unroll
+                for (int mt = 0; mt < NT; ++mt) {
+                    if (mt >= mb) {
+                        mma_f64(c[mt][0], c[mt][1], z0, V3[8 * mt]);
+                        mma_f64(c[mt][0], c[mt][1], z1, V3[VP + 8 * mt]);
+                    }
+                }
+            }
+            // ---- rows above the block are final: write them out and clear them, so that the panel below runs over
+            //      all m-tiles without masks (cleared rows contribute nothing) ----
+            double dt[2] = {0.0, 0.0};                   // the diagonal m-tile of this lane's column
+#pragma unroll
+            for (int mt = 0; mt < NT; ++mt) {
+                if (mt < m0) {
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        const int row = 8 * mt + 4 * u + t4;
+                        if (row < h) dst[row] = c[mt][u];
+                        if (isy && row < K) yout[row] = c[mt][u];
+                        c[mt][u] = 0.0;
+                    }
+                } else if (mt == m0) { dt[0] = c[mt][0]; dt[1] = c[mt][1]; c[mt][0] = 0.0; c[mt][1] = 0.0; }
+            }
+            // ---- factor the block in registers ----
+            double Trow[8];                              // row g8 of the block's T
+#pragma unroll
+            for (int k = 0; k < 8; ++k) Trow[k] = 0.0;
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) {
+                const int j = o + jj;
+                if (j < p && j < K) {                    // warp-uniform
+                    const int src = 4 * jj + t4;
+                    double vd[2], vv[NT][2];
+                    const double s0 = (t4 >= jj) ? dt[0] : 0.0;                // rows o + t4 and o + 4 + t4 against row j = o + jj
+                    const double s1 = (4 + t4 >= jj) ? dt[1] : 0.0;
+                    vd[0] = __shfl_sync(FULL, s0, src);
+                    vd[1] = __shfl_sync(FULL, s1, src);
+#pragma unroll
+                    for (int mt = 0; mt < NT; ++mt) {
+                        vv[mt][0] = __shfl_sync(FULL, c[mt][0], src);
+                        vv[mt][1] = __shfl_sync(FULL, c[mt][1], src);
+                    }
+                    double a0 = vd[0] * dt[0], a1 = vd[1] * dt[1], a2 = 0.0, a3 = 0.0;
+#pragma unroll
+                    for (int mt = 0; mt < NT; ++mt) {
+                        if (mt & 1) { a2 = fma(vv[mt][0], c[mt][0], a2); a3 = fma(vv[mt][1], c[mt][1], a3); }
+                        else { a0 = fma(vv[mt][0], c[mt][0], a0); a1 = fma(vv[mt][1], c[mt][1], a1); }
+                    }
+                    double d = (a0 + a1) + (a2 + a3);                          // raw v . (my column), over my rows
+                    d += __shfl_xor_sync(FULL, d, 1);
+                    d += __shfl_xor_sync(FULL, d, 2);
+                    const double ss = __shfl_sync(FULL, d, 4 * jj);            // |raw v|^2
+                    const double x0 = __shfl_sync(FULL, dt[jj >> 2], 4 * jj + (jj & 3));
+                    const double cj = __shfl_sync(FULL, dt[jj >> 2], (lane & ~3) | (jj & 3));   // my column at row j
+                    // nrm = sqrt(ss), tau = 2 / v^T v = 1 / (ss + nrm |x0|): rsqrt + reciprocal instead of sqrt + division
+                    const bool zero = !(ss > 0.0);
+                    const double nrm = zero ? 0.0 : ss * rsqrt(ss);
+                    const double alpha = (x0 >= 0.0) ? -nrm : nrm;
+                    const double tj = zero ? 0.0 : __drcp_rn(fma(nrm, fabs(x0), ss));
+                    const double gfin = d - alpha * cj;                        // v . (my column) with v[j] = x0 - alpha
+                    if (t4 == (jj & 3)) vd[jj >> 2] = x0 - alpha;
+                    const double w = (g8 > jj) ? gfin * tj : 0.0;
+                    dt[0] = fma(-w, vd[0], dt[0]);
+                    dt[1] = fma(-w, vd[1], dt[1]);
+#pragma unroll
+                    for (int mt = 0; mt < NT; ++mt) { c[mt][0] = fma(-w, vv[mt][0], c[mt][0]); c[mt][1] = fma(-w, vv[mt][1], c[mt][1]); }
+                    if (g8 == jj && t4 == (jj & 3)) dt[jj >> 2] = alpha;      // R[j][j]; the rows below keep v
+                    // T[:, jj] = -tau T[:, :jj] (V^T v)[:jj], T[jj][jj] = tau; (V^T v)[k] sits in lane group k
+                    {
+                        double sA = 0.0, sB = 0.0;
+#pragma unroll
+                        for (int k = 0; k < jj; ++k) {
+                            const double gk = __shfl_sync(FULL, gfin, 4 * k);
+                            if (k & 1) sB = fma(Trow[k], gk, sB); else sA = fma(Trow[k], gk, sA);
+                        }
+                        Trow[jj] = (g8 < jj) ? -tj * (sA + sB) : (g8 == jj ? tj : 0.0);
+                    }
+                    if (stored && g8 == jj) {
+                        double *vdst = Vs + (size_t)j * VP + t4;
+#pragma unroll
+                        for (int mt = 0; mt < NT; ++mt) { vdst[8 * mt] = vv[mt][0]; vdst[8 * mt + 4] = vv[mt][1]; }
+                        vdst[8 * m0] = vd[0];
+                        vdst[8 * m0 + 4] = vd[1];
+                    }
+                } else if (stored && g8 == jj) {         // no reflector from this column (p > N): an identity factor
+                    double *vdst = Vs + (size_t)j * VP + t4;
+#pragma unroll
+                    for (int mt = 0; mt < NT; ++mt) { vdst[8 * mt] = 0.0; vdst[8 * mt + 4] = 0.0; }
+                }
+            }
+            if (stored && t4 == 0) {
+                double *tdst = Ts + (size_t)m0 * 8 * QRM_TP + g8 * QRM_TP;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) tdst[k] = Trow[k];
+            }
+            // ---- the block's own rows of R; for y: rows < K are Q^T y, the rest gives e2 ----
+            {
+                double e2 = 0.0;
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int row = o + 4 * u + t4;
+                    if (row < h) dst[row] = dt[u];
+                    if (isy) { if (row < K) yout[row] = dt[u]; else e2 = fma(dt[u], dt[u], e2); }
+                }
+                if (o + 8 >= ncols) {                    // last block (uniform): the y column is here
+#pragma unroll
+                    for (int mt = 0; mt < NT; ++mt) {
+#pragma unroll
+                        for (int u = 0; u < 2; ++u) {
+                            const int row = 8 * mt + 4 * u + t4;
+                            if (isy && mt > m0) { if (row < K) yout[row] = c[mt][u]; else e2 = fma(c[mt][u], c[mt][u], e2); }
+                        }
+                    }
+                    e2 += __shfl_xor_sync(FULL, e2, 1);
+                    e2 += __shfl_xor_sync(FULL, e2, 2);
+                    if (isy && t4 == 0) yout[K] = e2;
+                }
+            }
+            __syncwarp();
+        }
+    }
+}
+
 // ---- K2b: truncation probes + solve --------------------------------------------------------
 template <int PS>
 __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressParams P) {
@@ -1366,6 +1591,14 @@ static cudaError_t launch_qrp_t(const RegressParams &p, int grid, int warps, siz
     return cudaGetLastError();
 }
 
+template <int NT>
+static cudaError_t launch_qrm_t(const RegressParams &p, int grid, int warps, size_t smem, cudaStream_t s) {
+    cudaError_t e = cudaFuncSetAttribute(regress_qr_mma_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    regress_qr_mma_kernel<NT><<<grid, warps * 32, smem, s>>>(p);
+    return cudaGetLastError();
+}
+
 template <int PS>
 static cudaError_t launch_solve_t(const RegressParams &p, int grid, int warps, size_t smem, cudaStream_t s) {
     cudaError_t e = cudaFuncSetAttribute(regress_solve_kernel<PS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1383,7 +1616,23 @@ cudaError_t launch_regress(const RegressParams &p_in, int sm_count, size_t smem_
     if (e != cudaSuccess) return e;
     // K2a
     const int S = (p.N + 31) / 32;
-    if (S <= 4 && !getenv("ENKFMC_QR_SMEM")) {
+    const char *qr_sel = getenv("ENKFMC_QR");
+    if (p.N <= 128 && !qr_sel) {
+        const int nt = (p.N + 7) / 8;
+        const int NTc = nt <= 4 ? 4 : nt <= 6 ? 6 : nt <= 10 ? 10 : 16;      // the instantiation used below
+        const size_t ws = regress_qrm_ws_doubles(8 * NTc, p.pmax) * sizeof(double);
+        int warps = (int)(smem_limit / ws);
+        if (warps < 1) return cudaErrorInvalidConfiguration;
+        if (warps > 8) warps = 8;
+        int64_t grid = sm_count;
+        const int64_t need = (p.nwork + warps - 1) / warps;
+        if (grid > need) grid = need;
+        if (nt <= 4) e = launch_qrm_t<4>(p, (int)grid, warps, ws * warps, s);
+        else if (nt <= 6) e = launch_qrm_t<6>(p, (int)grid, warps, ws * warps, s);
+        else if (nt <= 10) e = launch_qrm_t<10>(p, (int)grid, warps, ws * warps, s);
+        else e = launch_qrm_t<16>(p, (int)grid, warps, ws * warps, s);
+        if (e != cudaSuccess) return e;
+    } else if (S <= 4 && !(qr_sel && qr_sel[0] == 's')) {
         const size_t ws = regress_qrp_ws_doubles(p.N, p.pmax) * sizeof(double);
         int warps = (int)(smem_limit / ws);
         if (warps < 1) return cudaErrorInvalidConfiguration;
