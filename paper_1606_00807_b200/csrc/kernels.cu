@@ -767,234 +767,6 @@ __global__ void __launch_bounds__(256, 1) regress_qr_kernel(const RegressParams 
     }
 }
 
-// ---- K2a, register-panel form ----------------------------------------------------------------
-// Left-looking blocked Householder QR of [A^T | y] (N x (p + 1)): eight columns at a time live in registers
-// (lane <-> rows lane + 32 s), gathered straight from the anomaly rows in global memory.  Every earlier
-// reflector is applied to the block from shared memory, two at a time (one pass of 16 dot products with the
-// transposing warp reduction), then the block is factored in registers and its R columns go straight to the
-// packed output.  Shared memory holds only the reflectors that later blocks still need (all but those of the
-// last block), so ten regressions are resident per SM instead of eight and the matrix itself never touches
-// shared memory.  The first block takes the (p + 1) mod 8 odd columns: it has no earlier reflectors to apply.
-#define QRP_NB 8
-
-__host__ __device__ inline size_t regress_qrp_ws_doubles(int N, int pmax) {
-    const int vcols = pmax - (QRP_NB - 1) > 1 ? pmax - (QRP_NB - 1) : 1;
-    const size_t d = (size_t)N * vcols + (size_t)pmax + (size_t)(pmax / 2 + 1);   // V | tau | g of the pairs
-    return (d + 1) & ~(size_t)1;
-}
-
-// c <- H2 H1 c for the eight block columns: c' = c - w1 v1, w1 = tau1 v1.c ; c'' = c' - w2 v2, w2 = tau2 (v2.c - w1 v2.v1)
-template <int S, int S0>
-__device__ __forceinline__ void qrp_apply2(double (&c)[QRP_NB][S], const double *V1, const double *V2, int N, double tau1,
-                                           double tau2, double g, int lane) {
-    double v1[S], v2[S], d1[QRP_NB], d2[QRP_NB];
-#pragma unroll
-    for (int s = S0; s < S; ++s) {
-        const int i = lane + 32 * s;
-        v1[s] = i < N ? V1[i] : 0.0;
-        v2[s] = i < N ? V2[i] : 0.0;
-    }
-#pragma unroll
-    for (int b = 0; b < QRP_NB; ++b) {
-        d1[b] = 0.0; d2[b] = 0.0;
-#pragma unroll
-        for (int s = S0; s < S; ++s) { d1[b] += v1[s] * c[b][s]; d2[b] += v2[s] * c[b][s]; }
-    }
-#pragma unroll
-    for (int b = 0; b < QRP_NB; b += 4) {
-        warp_sum4(d1[b], d1[b + 1], d1[b + 2], d1[b + 3], lane);
-        warp_sum4(d2[b], d2[b + 1], d2[b + 2], d2[b + 3], lane);
-    }
-#pragma unroll
-    for (int b = 0; b < QRP_NB; ++b) {
-        const double w1 = d1[b] * tau1;
-        const double w2 = (d2[b] - w1 * g) * tau2;
-#pragma unroll
-        for (int s = S0; s < S; ++s) c[b][s] -= w1 * v1[s] + w2 * v2[s];
-    }
-}
-
-template <int S, int S0>
-__device__ __forceinline__ void qrp_apply1(double (&c)[QRP_NB][S], const double *V1, int N, double tau1, int lane) {
-    double v1[S], d1[QRP_NB];
-#pragma unroll
-    for (int s = S0; s < S; ++s) { const int i = lane + 32 * s; v1[s] = i < N ? V1[i] : 0.0; }
-#pragma unroll
-    for (int b = 0; b < QRP_NB; ++b) {
-        d1[b] = 0.0;
-#pragma unroll
-        for (int s = S0; s < S; ++s) d1[b] += v1[s] * c[b][s];
-    }
-#pragma unroll
-    for (int b = 0; b < QRP_NB; b += 4) warp_sum4(d1[b], d1[b + 1], d1[b + 2], d1[b + 3], lane);
-#pragma unroll
-    for (int b = 0; b < QRP_NB; ++b) {
-        const double w1 = d1[b] * tau1;
-#pragma unroll
-        for (int s = S0; s < S; ++s) c[b][s] -= w1 * v1[s];
-    }
-}
-
-// Reflectors [k0, k1) from shared memory onto the block; slots below 32 S0 hold only zeros of v and are skipped.
-template <int S, int S0>
-__device__ __forceinline__ void qrp_apply_range(double (&c)[QRP_NB][S], const double *V, const double *tau, const double *gp,
-                                                int N, int k0, int k1, int lane) {
-    int k = k0;
-    if ((k & 1) && k < k1) { qrp_apply1<S, S0>(c, V + (size_t)k * N, N, tau[k], lane); ++k; }
-    for (; k + 1 < k1; k += 2)
-        qrp_apply2<S, S0>(c, V + (size_t)k * N, V + (size_t)(k + 1) * N, N, tau[k], tau[k + 1], gp[k >> 1], lane);
-    if (k < k1) qrp_apply1<S, S0>(c, V + (size_t)k * N, N, tau[k], lane);
-}
-
-template <int S>
-__global__ void __launch_bounds__(320, 1) regress_qr_panel_kernel(const RegressParams P) {
-    extern __shared__ double smem[];
-    const int lane = threadIdx.x & 31;
-    const int N = P.N, pmax = P.pmax;
-    double *V = smem + (size_t)(threadIdx.x >> 5) * regress_qrp_ws_doubles(N, pmax);
-    const int vcols = pmax - (QRP_NB - 1) > 1 ? pmax - (QRP_NB - 1) : 1;
-    double *tau = V + (size_t)N * vcols;
-    double *gp = tau + pmax;
-    const double denom = (double)(N - 1);
-    const unsigned nf = (unsigned)(P.f1 - P.f0);
-
-    for (;;) {
-        unsigned int wk = 0;
-        if (lane == 0) wk = atomicAdd(P.counter, 1u);
-        wk = __shfl_sync(FULL, wk, 0);
-        if ((int64_t)wk >= P.nwork) break;
-        const int q = P.work_order[wk / nf];
-        const int fl = (int)(wk % nf), f = P.f0 + fl;
-        const int64_t r0 = P.row_ptr[q];
-        const int p = (int)(P.row_ptr[q + 1] - r0);
-        const double *Uf = P.U + (int64_t)f * P.nstate2d * N;
-        const double *yrow = Uf + (int64_t)P.state_row[q] * N;
-        const int32_t *pred = P.pred_state + r0;
-
-        if (p == 0) {  // estimator.py:139-144
-            double s = 0.0;
-            for (int i = lane; i < N; i += 32) { const double v = yrow[i]; s += v * v; }
-            s = warp_sum(s) / denom;
-            if (lane == 0) {
-                P.D[(int64_t)f * P.nloc + q] = fmax(s, P.variance_floor);
-                if (P.flags) P.flags[(int64_t)f * P.nloc + q] = (s < P.variance_floor) ? 8 : 0;
-            }
-            continue;
-        }
-        const int K = p < N ? p : N;                     // reflectors
-        const int ncols = p + 1;                         // the last column is y
-        const int nstore = ncols - QRP_NB;               // reflectors j < nstore are applied to later blocks
-        double *out = P.Rq + (int64_t)fl * P.rq_stride + P.rq_ptr[q];
-
-        for (int o = 0; o < ncols;) {
-            const int nbc = (o == 0) ? ((ncols - 1) & (QRP_NB - 1)) + 1 : QRP_NB;
-            double c[QRP_NB][S];
-#pragma unroll
-            for (int b = 0; b < QRP_NB; ++b) {
-                const int j = o + b;
-                const double *src = (j < p) ? Uf + (int64_t)pred[j < p ? j : 0] * N : yrow;
-#pragma unroll
-                for (int s = 0; s < S; ++s) {
-                    const int i = lane + 32 * s;
-                    c[b][s] = (b < nbc && i < N) ? src[i] : 0.0;
-                }
-            }
-            // earlier reflectors, by ranges of dead slots
-            {
-                const int kprev = o < K ? o : K;
-                if (kprev > 0) {
-                    qrp_apply_range<S, 0>(c, V, tau, gp, N, 0, kprev < 32 ? kprev : 32, lane);
-                    if constexpr (S > 1) if (kprev > 32) qrp_apply_range<S, 1>(c, V, tau, gp, N, 32, kprev < 64 ? kprev : 64, lane);
-                    if constexpr (S > 2) if (kprev > 64) qrp_apply_range<S, 2>(c, V, tau, gp, N, 64, kprev < 96 ? kprev : 96, lane);
-                    if constexpr (S > 3) if (kprev > 96) qrp_apply_range<S, (S > 3 ? 3 : 0)>(c, V, tau, gp, N, 96, kprev, lane);
-                }
-            }
-            // factor the block in registers
-            double vp[S];                                   // reflector j - 1 (for the pair's v_j . v_{j-1})
-#pragma unroll
-            for (int s = 0; s < S; ++s) {
-                const int i = lane + 32 * s;
-                vp[s] = (o > 0 && (o & 1) && o - 1 < K && i < N) ? V[(size_t)(o - 1) * N + i] : 0.0;
-            }
-#pragma unroll
-            for (int jj = 0; jj < QRP_NB; ++jj) {
-                const int j = o + jj;
-                if (jj < nbc && j < p && j < K) {
-                    // one batched reduction: |v|^2, x0, (v.v_prev, v_prev[j]), and per later column (v.c_b, c_b[j]);
-                    // the dots use the raw column and are corrected for v[j] = x0 - alpha afterwards
-                    double vr[S];
-                    double r[4 + 2 * (QRP_NB - 1)];
-#pragma unroll
-                    for (int e = 0; e < 4 + 2 * (QRP_NB - 1); ++e) r[e] = 0.0;
-#pragma unroll
-                    for (int s = 0; s < S; ++s) {
-                        const int i = lane + 32 * s;
-                        vr[s] = (i >= j) ? c[jj][s] : 0.0;
-                        r[0] += vr[s] * vr[s];
-                        r[2] += vr[s] * vp[s];
-                        if (i == j) { r[1] = vr[s]; r[3] = vp[s]; }
-#pragma unroll
-                        for (int b = jj + 1; b < QRP_NB; ++b) {
-                            r[4 + 2 * (b - jj - 1)] += vr[s] * c[b][s];
-                            if (i == j) r[5 + 2 * (b - jj - 1)] = c[b][s];
-                        }
-                    }
-#pragma unroll
-                    for (int e = 0; e < 4 + 2 * (QRP_NB - 1 - jj); e += 4) warp_sum4(r[e], r[e + 1], r[e + 2], r[e + 3], lane);
-                    const double x0 = r[1];
-                    const double nrm = sqrt(r[0]);
-                    const double alpha = nrm == 0.0 ? 0.0 : ((x0 >= 0.0) ? -nrm : nrm);
-                    const double tj = nrm == 0.0 ? 0.0 : 1.0 / (nrm * (nrm + fabs(x0)));   // 2 / v^T v
-#pragma unroll
-                    for (int s = 0; s < S; ++s) {
-                        const int i = lane + 32 * s;
-                        if (i == j) { vr[s] = x0 - alpha; c[jj][s] = alpha; }               // R[j][j]
-                    }
-#pragma unroll
-                    for (int b = jj + 1; b < QRP_NB; ++b) {
-                        const double w = (r[4 + 2 * (b - jj - 1)] - alpha * r[5 + 2 * (b - jj - 1)]) * tj;
-#pragma unroll
-                        for (int s = 0; s < S; ++s) c[b][s] -= w * vr[s];
-                    }
-                    if (j < nstore) {
-#pragma unroll
-                        for (int s = 0; s < S; ++s) { const int i = lane + 32 * s; if (i < N) V[(size_t)j * N + i] = vr[s]; }
-                        if (lane == 0) {
-                            tau[j] = tj;
-                            if (j & 1) gp[j >> 1] = r[2] - alpha * r[3];                    // v_j . v_{j-1} with the final v_j[j]
-                        }
-                    }
-#pragma unroll
-                    for (int s = 0; s < S; ++s) vp[s] = vr[s];
-                }
-            }
-            // finished columns -> packed output: R by columns (min(j + 1, K) entries), then c[0:K] and e2 for y
-#pragma unroll
-            for (int b = 0; b < QRP_NB; ++b) {
-                const int j = o + b;
-                if (b >= nbc) continue;
-                double *dst = out + packed_col_offset(j, K);
-                if (j < p) {
-                    const int h = j + 1 < K ? j + 1 : K;
-#pragma unroll
-                    for (int s = 0; s < S; ++s) { const int i = lane + 32 * s; if (i < h) dst[i] = c[b][s]; }
-                } else {
-                    double e2 = 0.0;
-#pragma unroll
-                    for (int s = 0; s < S; ++s) {
-                        const int i = lane + 32 * s;
-                        if (i < K) dst[i] = c[b][s]; else e2 += c[b][s] * c[b][s];       // rows >= N hold zeros
-                    }
-                    e2 = warp_sum(e2);
-                    if (lane == 0) dst[K] = e2;
-                }
-            }
-            __syncwarp();
-            o += nbc;
-        }
-    }
-}
-
 // ---- K2a, tensor-core form ---------------------------------------------------------------------
 // Blocked Householder QR of [A^T | y] with the block of eight columns in registers in mma.m8n8k4 fragment
 // layout: lane (g8, t4) = (lane >> 2, lane & 3) owns column g8 of the block and the rows 8 mt + 4 u + t4
@@ -1013,9 +785,17 @@ __host__ __device__ constexpr int qrm_vp(int N) {            // reflector pitch:
     while (v % 16 != 4) ++v;
     return v;
 }
-__host__ __device__ inline size_t regress_qrm_ws_doubles(int N, int pmax) {
+// Reflector block i (reflectors 8 i .. 8 i + 7) is zero above row 8 i: only rows >= 8 i are stored, with a pitch of
+// its own (same bank rule).  Offset of block i's storage and its pitch, for rows padded to 8 nt:
+__host__ __device__ constexpr int qrm_block_vp(int nt, int i) { return qrm_vp(8 * (nt - i > 1 ? nt - i : 1)); }
+__host__ __device__ constexpr int qrm_block_off(int nt, int i) {
+    int off = 0;
+    for (int k = 0; k < i; ++k) off += 8 * qrm_block_vp(nt, k);
+    return off;
+}
+__host__ __device__ inline size_t regress_qrm_ws_doubles(int nt, int pmax) {
     const int nblk = pmax / 8 > 0 ? pmax / 8 : 1;         // reflector blocks that a later column block can need
-    return (size_t)nblk * 8 * qrm_vp(N) + (size_t)nblk * 8 * QRM_TP;
+    return (size_t)qrm_block_off(nt, nblk) + (size_t)nblk * 8 * QRM_TP;
 }
 
 template <int NT>
@@ -1023,10 +803,9 @@ __global__ void __launch_bounds__(256, 1) regress_qr_mma_kernel(const RegressPar
     extern __shared__ double smem[];
     const int lane = threadIdx.x & 31, g8 = lane >> 2, t4 = lane & 3;
     const int N = P.N, pmax = P.pmax;
-    constexpr int VP = qrm_vp(8 * NT);                     // rows are padded to 8 NT (zeros beyond N)
-    const int nblk_cap = pmax / 8 > 0 ? pmax / 8 : 1;
-    double *Vs = smem + (size_t)(threadIdx.x >> 5) * regress_qrm_ws_doubles(8 * NT, pmax);
-    double *Ts = Vs + (size_t)nblk_cap * 8 * VP;
+    const int nblk_cap = pmax / 8 > 0 ? pmax / 8 : 1;      // rows are padded to 8 NT (zeros beyond N)
+    double *Vs = smem + (size_t)(threadIdx.x >> 5) * regress_qrm_ws_doubles(NT, pmax);
+    double *Ts = Vs + qrm_block_off(NT, nblk_cap);
     const double denom = (double)(N - 1);
     const unsigned nf = (unsigned)(P.f1 - P.f0);
     const int pig = 4 * (g8 & 1) + (g8 >> 1);              // row (within an m-tile) of accumulator column n = g8
@@ -1081,7 +860,9 @@ __global__ void __launch_bounds__(256, 1) regress_qr_mma_kernel(const RegressPar
             // ---- earlier reflector blocks: C <- C - V T^T (V^T C) ----
             for (int ob = 0; ob < o && ob < K; ob += 8) {
                 const int mb = ob >> 3;
-                const double *Vb = Vs + (size_t)(ob + g8) * VP + t4;
+                const int VP = qrm_block_vp(NT, mb);
+                const double *Vblk = Vs + qrm_block_off(NT, mb) - 8 * mb;      // row r of reflector k: Vblk[k * VP + r]
+                const double *Vb = Vblk + (size_t)g8 * VP + t4;
                 double wa0 = 0.0, wa1 = 0.0, wb0 = 0.0, wb1 = 0.0, wc0 = 0.0, wc1 = 0.0, wd0 = 0.0, wd1 = 0.0;
 #pragma unroll
                 for (int mt = 0; mt < NT; ++mt) {
@@ -1095,7 +876,7 @@ __global__ void __launch_bounds__(256, 1) regress_qr_mma_kernel(const RegressPar
                 double z0 = 0.0, z1 = 0.0;                                                    // (C^T V T)[g8][2 t4 + {0, 1}]
                 mma_f64(z0, z1, w0, Tb[(2 * t4) * QRM_TP + g8]);
                 mma_f64(z0, z1, w1, Tb[(2 * t4 + 1) * QRM_TP + g8]);
-                const double *V3 = Vs + (size_t)(ob + 2 * t4) * VP + pig;
+                const double *V3 = Vblk + (size_t)(2 * t4) * VP + pig;
                 z0 = -z0; z1 = -z1;
 #pragma unroll
                 for (int mt = 0; mt < NT; ++mt) {
@@ -1121,6 +902,8 @@ __global__ void __launch_bounds__(256, 1) regress_qr_mma_kernel(const RegressPar
                 } else if (mt == m0) { dt[0] = c[mt][0]; dt[1] = c[mt][1]; c[mt][0] = 0.0; c[mt][1] = 0.0; }
             }
             // ---- factor the block in registers ----
+            const int VPown = qrm_block_vp(NT, m0);
+            double *Vown = Vs + qrm_block_off(NT, m0) - 8 * m0;               // this block's reflectors, if stored
             double Trow[8];                              // row g8 of the block's T
 #pragma unroll
             for (int k = 0; k < 8; ++k) Trow[k] = 0.0;
@@ -1175,16 +958,18 @@ __global__ void __launch_bounds__(256, 1) regress_qr_mma_kernel(const RegressPar
                         Trow[jj] = (g8 < jj) ? -tj * (sA + sB) : (g8 == jj ? tj : 0.0);
                     }
                     if (stored && g8 == jj) {
-                        double *vdst = Vs + (size_t)j * VP + t4;
+                        double *vdst = Vown + (size_t)jj * VPown + t4;
 #pragma unroll
-                        for (int mt = 0; mt < NT; ++mt) { vdst[8 * mt] = vv[mt][0]; vdst[8 * mt + 4] = vv[mt][1]; }
+                        for (int mt = 1; mt < NT; ++mt)
+                            if (mt > m0) { vdst[8 * mt] = vv[mt][0]; vdst[8 * mt + 4] = vv[mt][1]; }
                         vdst[8 * m0] = vd[0];
                         vdst[8 * m0 + 4] = vd[1];
                     }
                 } else if (stored && g8 == jj) {         // no reflector from this column (p > N): an identity factor
-                    double *vdst = Vs + (size_t)j * VP + t4;
+                    double *vdst = Vown + (size_t)jj * VPown + t4;
 #pragma unroll
-                    for (int mt = 0; mt < NT; ++mt) { vdst[8 * mt] = 0.0; vdst[8 * mt + 4] = 0.0; }
+                    for (int mt = 0; mt < NT; ++mt)
+                        if (mt >= m0) { vdst[8 * mt] = 0.0; vdst[8 * mt + 4] = 0.0; }
                 }
             }
             if (stored && t4 == 0) {
@@ -1583,14 +1368,6 @@ static cudaError_t launch_qr_t(const RegressParams &p, int grid, int warps, size
     return cudaGetLastError();
 }
 
-template <int S>
-static cudaError_t launch_qrp_t(const RegressParams &p, int grid, int warps, size_t smem, cudaStream_t s) {
-    cudaError_t e = cudaFuncSetAttribute(regress_qr_panel_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    regress_qr_panel_kernel<S><<<grid, warps * 32, smem, s>>>(p);
-    return cudaGetLastError();
-}
-
 template <int NT>
 static cudaError_t launch_qrm_t(const RegressParams &p, int grid, int warps, size_t smem, cudaStream_t s) {
     cudaError_t e = cudaFuncSetAttribute(regress_qr_mma_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1616,14 +1393,17 @@ cudaError_t launch_regress(const RegressParams &p_in, int sm_count, size_t smem_
     if (e != cudaSuccess) return e;
     // K2a
     const int S = (p.N + 31) / 32;
+    // ensembles of up to 128 members: tensor-core form; larger ones (or ENKFMC_QR=smem, for comparisons): the
+    // shared-memory SIMT form
     const char *qr_sel = getenv("ENKFMC_QR");
     if (p.N <= 128 && !qr_sel) {
         const int nt = (p.N + 7) / 8;
         const int NTc = nt <= 4 ? 4 : nt <= 6 ? 6 : nt <= 10 ? 10 : 16;      // the instantiation used below
-        const size_t ws = regress_qrm_ws_doubles(8 * NTc, p.pmax) * sizeof(double);
+        const size_t ws = regress_qrm_ws_doubles(NTc, p.pmax) * sizeof(double);
         int warps = (int)(smem_limit / ws);
         if (warps < 1) return cudaErrorInvalidConfiguration;
         if (warps > 8) warps = 8;
+        if (const char *wenv = getenv("ENKFMC_QR_WARPS")) { const int wv = atoi(wenv); if (wv >= 1 && wv < warps) warps = wv; }
         int64_t grid = sm_count;
         const int64_t need = (p.nwork + warps - 1) / warps;
         if (grid > need) grid = need;
@@ -1631,21 +1411,6 @@ cudaError_t launch_regress(const RegressParams &p_in, int sm_count, size_t smem_
         else if (nt <= 6) e = launch_qrm_t<6>(p, (int)grid, warps, ws * warps, s);
         else if (nt <= 10) e = launch_qrm_t<10>(p, (int)grid, warps, ws * warps, s);
         else e = launch_qrm_t<16>(p, (int)grid, warps, ws * warps, s);
-        if (e != cudaSuccess) return e;
-    } else if (S <= 4 && !(qr_sel && qr_sel[0] == 's')) {
-        const size_t ws = regress_qrp_ws_doubles(p.N, p.pmax) * sizeof(double);
-        int warps = (int)(smem_limit / ws);
-        if (warps < 1) return cudaErrorInvalidConfiguration;
-        if (warps > 10) warps = 10;                    // <= 320 threads: up to 204 registers per thread
-        int64_t grid = sm_count;
-        const int64_t need = (p.nwork + warps - 1) / warps;
-        if (grid > need) grid = need;
-        switch (S) {
-            case 1: e = launch_qrp_t<1>(p, (int)grid, warps, ws * warps, s); break;
-            case 2: e = launch_qrp_t<2>(p, (int)grid, warps, ws * warps, s); break;
-            case 3: e = launch_qrp_t<3>(p, (int)grid, warps, ws * warps, s); break;
-            default: e = launch_qrp_t<4>(p, (int)grid, warps, ws * warps, s); break;
-        }
         if (e != cudaSuccess) return e;
     } else {
         const size_t ws = regress_qr_ws_doubles(p.N, p.pmax) * sizeof(double);

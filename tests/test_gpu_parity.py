@@ -232,3 +232,25 @@ def test_nonfinite_and_shape_errors(mck):
         mck.fit_factors(X + 1.0, geo, 1)
     with pytest.raises(ValueError, match="rows"):
         mck.fit_factors(mck.center_rows(X)[:5], geo, 1)
+
+
+def test_regression_forms_agree(mck, monkeypatch):
+    """K2a has two forms (tensor-core fragments for ensembles of up to 128 members, shared-memory SIMT beyond):
+    on the same inputs they must give the same factors to rounding, for full and partial column blocks and
+    for more predecessors than members."""
+    from oracle import enkf_mc_oracle as orc
+    rng = np.random.default_rng(7)
+    for nx, ny, nens, zeta, nug in ((20, 14, 30, 3, 0.3), (16, 12, 9, 2, 0.5), (24, 10, 80, 4, 0.2), (12, 9, 100, 1, 0.4)):
+        geo = mck.GridGeometry("grid2d", nx, ny)
+        n = nx * ny
+        base = rng.standard_normal((n, nens)).cumsum(axis=0) * 0.1 + nug * rng.standard_normal((n, nens))
+        U = orc.center_rows(base)
+        monkeypatch.delenv("ENKFMC_QR", raising=False)
+        f1 = mck.fit_factors(U, geo, zeta)
+        monkeypatch.setenv("ENKFMC_QR", "smem")
+        f2 = mck.fit_factors(U, geo, zeta)
+        monkeypatch.delenv("ENKFMC_QR", raising=False)
+        assert relerr(f1.lower.data, f2.lower.data) < 1e-10, (nx, ny, nens, relerr(f1.lower.data, f2.lower.data))
+        assert np.max(np.abs(f1.variances - f2.variances) / f2.variances) < 1e-10
+        ref = orc.fit_factors(U, orc.Grid(nx, ny, True, False), zeta)
+        assert relerr(f1.lower.data, ref.data) < 1e-9 and np.max(np.abs(f1.variances - ref.d) / ref.d) < 1e-9
