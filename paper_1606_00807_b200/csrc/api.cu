@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -50,7 +51,8 @@ struct DeviceState {
     double *dX = nullptr, *dXa = nullptr, *dR = nullptr, *dYs = nullptr;
     int64_t stage_nens = 0, stage_nobs = -1;
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
-    cudaStream_t stream = nullptr;
+    cudaStream_t stream = nullptr, copy_stream = nullptr;
+    std::vector<cudaEvent_t> hev;    // events of the pipelined host path
 };
 
 namespace {
@@ -114,6 +116,7 @@ int ensure_device(enkfmc_plan *p) {
     CK(cudaMemset(d->counters, 0, 4 * sizeof(unsigned int)));
     for (auto &ev : d->ev) CK(cudaEventCreate(&ev));
     CK(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&d->copy_stream, cudaStreamNonBlocking));
     return ENKFMC_OK;
 }
 
@@ -200,8 +203,11 @@ int ensure_workspace(enkfmc_plan *p, int64_t nens) {
     return ENKFMC_OK;
 }
 
+// fields [fbeg, fend) (fend < 0: all)
 int do_regress(enkfmc_plan *p, const double *d_U, int64_t nens, double rank_tol, double floor_, double *d_T,
-               double *d_D, int32_t *d_flags, cudaStream_t s, cudaEvent_t mid = nullptr) {
+               double *d_D, int32_t *d_flags, cudaStream_t s, cudaEvent_t mid = nullptr, int64_t fbeg = 0,
+               int64_t fend = -1) {
+    if (fend < 0) fend = p->nfields;
     DeviceState *d = p->dev;
     int rc0 = ensure_orders(p);
     if (rc0) return rc0;
@@ -222,9 +228,9 @@ int do_regress(enkfmc_plan *p, const double *d_U, int64_t nens, double rank_tol,
         d->rq_alloc = chunk * d->rq_stride;
     }
     R.Rq = d->Rq;
-    for (int64_t f0 = 0; f0 < p->nfields; f0 += chunk) {
+    for (int64_t f0 = fbeg; f0 < fend; f0 += chunk) {
         R.f0 = (int)f0;
-        R.f1 = (int)std::min<int64_t>(p->nfields, f0 + chunk);
+        R.f1 = (int)std::min<int64_t>(fend, f0 + chunk);
         R.nwork = (int64_t)p->regress_order.size() * (R.f1 - R.f0);
         if (R.nwork > 0xfffffff0LL) { enkfmc_set_error("too many regressions for one launch"); return ENKFMC_E_CAPACITY; }
         cudaError_t e = launch_regress(R, d->sm_count, d->smem_limit, s, mid);
@@ -237,15 +243,18 @@ int do_regress(enkfmc_plan *p, const double *d_U, int64_t nens, double rank_tol,
         if (R.nwork > 0) p->counters[0] += 2;
     }
     if (!p->alias_row.empty()) {   // copy each distinct regression to the other tiles holding the same row
-        CK(launch_replicate_rows(d->alias_row, d->alias_rep, (int64_t)p->alias_row.size(), d->row_ptr, p->nfields,
-                                 p->nnz(), p->sum_nlocal(), d_T, d_D, d_flags, s));
+        CK(launch_replicate_rows(d->alias_row, d->alias_rep, (int64_t)p->alias_row.size(), d->row_ptr, fend - fbeg,
+                                 p->nnz(), p->sum_nlocal(), d_T + fbeg * p->nnz(), d_D + fbeg * p->sum_nlocal(),
+                                 d_flags ? d_flags + fbeg * p->sum_nlocal() : nullptr, s));
         p->counters[0] += 1;
     }
     return ENKFMC_OK;
 }
 
 int do_solve(enkfmc_plan *p, const double *d_X, const double *d_T, const double *d_D, const double *d_r,
-             const double *d_Ys, int64_t nens, double *d_Xa, int32_t *d_status, cudaStream_t s) {
+             const double *d_Ys, int64_t nens, double *d_Xa, int32_t *d_status, cudaStream_t s, int64_t fbeg = 0,
+             int64_t fend = -1) {
+    if (fend < 0) fend = p->nfields;
     DeviceState *d = p->dev;
     int rc = ensure_obs(p);
     if (rc) return rc;
@@ -268,10 +277,10 @@ int do_solve(enkfmc_plan *p, const double *d_X, const double *d_T, const double 
     int rc2 = ensure_band(p);
     if (rc2) return rc2;
     S.band = d->band;
-    CK(cudaMemsetAsync(d->counters + 3, 0, sizeof(unsigned int), s));   // clamped-pivot counter
-    for (int64_t f0 = 0; f0 < p->nfields; f0 += d->band_fields) {
+    if (fbeg == 0) CK(cudaMemsetAsync(d->counters + 3, 0, sizeof(unsigned int), s));   // clamped-pivot counter
+    for (int64_t f0 = fbeg; f0 < fend; f0 += d->band_fields) {
         S.f0 = (int)f0;
-        S.f1 = (int)std::min<int64_t>(p->nfields, f0 + d->band_fields);
+        S.f1 = (int)std::min<int64_t>(fend, f0 + d->band_fields);
         CK(launch_assemble_band(S, d->sm_count, d->smem_limit, s));
         cudaError_t e = launch_local_solve(S, d->solve_grid, d->smem_limit, s);
         if (e == cudaErrorInvalidConfiguration) {
@@ -299,6 +308,8 @@ void enkfmc_device_release(enkfmc_plan *p) {
     release(d->flags); release(d->status); release(d->counters); release(d->rq_ptr); release(d->Rq); release(d->band_ptr); release(d->band); release(d->row_tile); release(d->dX); release(d->dXa); release(d->dR);
     release(d->dYs);
     for (auto &ev : d->ev) if (ev) cudaEventDestroy(ev);
+    for (auto &ev : d->hev) cudaEventDestroy(ev);
+    if (d->copy_stream) cudaStreamDestroy(d->copy_stream);
     for (auto &ev : d->prof) cudaEventDestroy(ev);
     if (d->stream) cudaStreamDestroy(d->stream);
     delete d;
@@ -464,28 +475,64 @@ extern "C" int enkfmc_analysis_host(enkfmc_plan *p, const double *X, const doubl
         CK(cudaMalloc(&d->dYs, std::max<size_t>((size_t)p->nobs * nens, 1) * sizeof(double)));
         d->stage_nobs = p->nobs;
     }
-    cudaStream_t s = d->stream;
-    CK(cudaEventRecord(d->ev[0], s));
-    CK(cudaMemcpyAsync(d->dX, X, xbytes, cudaMemcpyHostToDevice, s));
-    if (p->nobs) {
-        CK(cudaMemcpyAsync(d->dR, r_diag, (size_t)p->nobs * sizeof(double), cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(d->dYs, Ys, (size_t)p->nobs * nens * sizeof(double), cudaMemcpyHostToDevice, s));
+    // Pipelined over groups of fields: the copy stream uploads group g + 1 and downloads the analysis of group
+    // g - 1 while the compute stream works on group g (fields are independent: PAPER.md:201).
+    cudaStream_t s = d->stream, cs = d->copy_stream;
+    int ngroups = (int)std::min<int64_t>(p->nfields, 4);
+    if (const char *genv = getenv("ENKFMC_HOST_GROUPS")) ngroups = (int)std::max<int64_t>(1, std::min<int64_t>(p->nfields, atoi(genv)));
+    const size_t need_ev = 2 + 7 * (size_t)ngroups;
+    while (d->hev.size() < need_ev) { cudaEvent_t e; CK(cudaEventCreate(&e)); d->hev.push_back(e); }
+    cudaEvent_t evY0 = d->hev[0], evY1 = d->hev[1];
+    auto EV = [&](int g, int k) { return d->hev[2 + 7 * (size_t)g + k]; };   // 0,1 H2D; 2,3,4 compute; 5,6 D2H
+    const size_t rowbytes = (size_t)nens * sizeof(double);
+    auto fcut = [&](int g) { return p->nfields * g / ngroups; };
+    for (int g = 0; g < ngroups; ++g) {
+        const size_t r0 = (size_t)fcut(g) * p->nstate2d, r1 = (size_t)fcut(g + 1) * p->nstate2d;
+        CK(cudaEventRecord(EV(g, 0), cs));
+        CK(cudaMemcpyAsync(d->dX + r0 * nens, X + r0 * nens, (r1 - r0) * rowbytes, cudaMemcpyHostToDevice, cs));
+        CK(cudaEventRecord(EV(g, 1), cs));
+        if (g == 0) {
+            CK(cudaEventRecord(evY0, cs));
+            if (p->nobs) {
+                CK(cudaMemcpyAsync(d->dR, r_diag, (size_t)p->nobs * sizeof(double), cudaMemcpyHostToDevice, cs));
+                CK(cudaMemcpyAsync(d->dYs, Ys, (size_t)p->nobs * nens * sizeof(double), cudaMemcpyHostToDevice, cs));
+            }
+            CK(cudaEventRecord(evY1, cs));
+        }
     }
-    CK(cudaEventRecord(d->ev[1], s));
-    CK(launch_center_rows(d->dX, d->U, nstate, (int)nens, s));
-    p->counters[0] += 1;
-    if ((rc = do_regress(p, d->U, nens, rank_tol, floor_, d->T, d->D, d->flags, s))) return rc;
-    CK(cudaEventRecord(d->ev[2], s));
-    if ((rc = do_solve(p, d->dX, d->T, d->D, d->dR, d->dYs, nens, d->dXa, d->status, s))) return rc;
-    CK(cudaEventRecord(d->ev[3], s));
-    CK(cudaMemcpyAsync(Xa, d->dXa, xbytes, cudaMemcpyDeviceToHost, s));
-    CK(cudaEventRecord(d->ev[4], s));
+    for (int g = 0; g < ngroups; ++g) {
+        const int64_t f0 = fcut(g), f1 = fcut(g + 1);
+        const size_t r0 = (size_t)f0 * p->nstate2d, r1 = (size_t)f1 * p->nstate2d;
+        CK(cudaStreamWaitEvent(s, EV(g, 1), 0));
+        CK(cudaEventRecord(EV(g, 2), s));
+        CK(launch_center_rows(d->dX + r0 * nens, d->U + r0 * nens, (int64_t)(r1 - r0), (int)nens, s));
+        p->counters[0] += 1;
+        if ((rc = do_regress(p, d->U, nens, rank_tol, floor_, d->T, d->D, d->flags, s, nullptr, f0, f1))) return rc;
+        CK(cudaEventRecord(EV(g, 3), s));
+        if (g == 0) CK(cudaStreamWaitEvent(s, evY1, 0));
+        if ((rc = do_solve(p, d->dX, d->T, d->D, d->dR, d->dYs, nens, d->dXa, d->status, s, f0, f1))) return rc;
+        CK(cudaEventRecord(EV(g, 4), s));
+        CK(cudaStreamWaitEvent(cs, EV(g, 4), 0));
+        CK(cudaEventRecord(EV(g, 5), cs));
+        CK(cudaMemcpyAsync(Xa + r0 * nens, d->dXa + r0 * nens, (r1 - r0) * rowbytes, cudaMemcpyDeviceToHost, cs));
+        CK(cudaEventRecord(EV(g, 6), cs));
+    }
+    CK(cudaStreamSynchronize(cs));
     CK(cudaStreamSynchronize(s));
-    if (timings_ms) {
-        for (int k = 0; k < 4; ++k) {
+    if (timings_ms) {   // busy time of each stage, summed over the groups (the stages overlap in wall-clock time)
+        auto span = [&](cudaEvent_t a, cudaEvent_t b, double &acc) {
             float ms = 0.f;
-            CK(cudaEventElapsedTime(&ms, d->ev[k], d->ev[k + 1]));
-            timings_ms[k] = ms;
+            cudaError_t e = cudaEventElapsedTime(&ms, a, b);
+            if (e == cudaSuccess) acc += ms;
+            return e;
+        };
+        timings_ms[0] = timings_ms[1] = timings_ms[2] = timings_ms[3] = 0.0;
+        CK(span(evY0, evY1, timings_ms[0]));
+        for (int g = 0; g < ngroups; ++g) {
+            CK(span(EV(g, 0), EV(g, 1), timings_ms[0]));
+            CK(span(EV(g, 2), EV(g, 3), timings_ms[1]));
+            CK(span(EV(g, 3), EV(g, 4), timings_ms[2]));
+            CK(span(EV(g, 5), EV(g, 6), timings_ms[3]));
         }
     }
     {
