@@ -418,39 +418,44 @@ __device__ __forceinline__ void vstore(double *dst, const Vec<PS> &a, int p, int
 // x = R^-1 b  (R upper triangular in W, diagonal reciprocals in rinv); b is overwritten.
 template <int PS>
 __device__ __forceinline__ void solve_upper(Vec<PS> &b, const double *W, const double *rinv, int ld, int p, int lane) {
+    // element k is final when column k is reached and never touched again: x = b * rinv once at the end
+    const Vec<PS> rv = vload<PS>(rinv, p, lane);
 #pragma unroll
     for (int sk = PS - 1; sk >= 0; --sk) {
         const int ktop = (p - 32 * sk < 32 ? p - 32 * sk : 32) - 1;
         const double *col = W + (size_t)(32 * sk + ktop) * ld + lane;
         for (int kk = ktop; kk >= 0; --kk, col -= ld) {
             const int k = 32 * sk + kk;
-            const double xk = __shfl_sync(FULL, b.v[sk], kk) * rinv[k];
+            const double xk = __shfl_sync(FULL, b.v[sk] * rv.v[sk], kk);
 #pragma unroll
             for (int t = 0; t <= sk; ++t)
                 if (lane + 32 * t < k) b.v[t] -= col[32 * t] * xk;
-            if (lane == kk) b.v[sk] = xk;
         }
     }
+#pragma unroll
+    for (int t = 0; t < PS; ++t) b.v[t] *= rv.v[t];
 }
 
 // u = R^-T z ; z is overwritten.
 template <int PS>
 __device__ __forceinline__ void solve_upper_t(Vec<PS> &z, const double *W, const double *rinv, int ld, int p, int lane) {
+    const Vec<PS> rv = vload<PS>(rinv, p, lane);
 #pragma unroll
     for (int sk = 0; sk < PS; ++sk) {
         const int kend = p - 32 * sk < 32 ? p - 32 * sk : 32;
         const double *row = W + 32 * sk + (size_t)lane * ld;   // R[k, lane + 32 t] = row[kk + 32 t ld]
         for (int kk = 0; kk < kend; ++kk) {
             const int k = 32 * sk + kk;
-            const double uk = __shfl_sync(FULL, z.v[sk], kk) * rinv[k];
+            const double uk = __shfl_sync(FULL, z.v[sk] * rv.v[sk], kk);
 #pragma unroll
             for (int t = sk; t < PS; ++t) {
                 const int j = lane + 32 * t;
                 if (j > k && j < p) z.v[t] -= row[kk + (size_t)32 * t * ld] * uk;
             }
-            if (lane == kk) z.v[sk] = uk;
         }
     }
+#pragma unroll
+    for (int t = 0; t < PS; ++t) z.v[t] *= rv.v[t];
 }
 
 // y = R v
@@ -520,33 +525,45 @@ __device__ void inverse_norms_mma(double *W, const double *rinv, int ld, int p, 
     const int t4 = lane & 3, m = lane >> 2;
     const int nbk = (p + 7) >> 3;
     double f2 = 0.0, g4 = 0.0;
-    for (int j = 0; j < nbk; ++j) {
-        {   // diagonal block: lane c' < 8 owns column c = 8 j + c'
-            const int c = 8 * j + lane;
-            const bool act = lane < 8 && c < p;
-            const double rc = act ? rinv[c] : 0.0;
-            f2 += rc * rc;
-            const int ktop = (8 * j + 7 < p - 1 ? 8 * j + 7 : p - 1) - 1;
-            for (int k = ktop; k >= 8 * j; --k) {
-                if (act && c > k) {
-                    double acc = W[(size_t)c * ld + k] * rc;                        // R[k,c] X[c,c]
-                    for (int i = k + 1; i < c; ++i) acc += W[(size_t)i * ld + k] * W[(size_t)i * ld + c];   // R[k,i] X[i,c]
-                    const double x = -rinv[k] * acc;
-                    W[(size_t)k * ld + c] = x;
-                    f2 += x * x;
-                }
+    // diagonal blocks, four at a time: lanes 8 g .. 8 g + 7 own the columns of block jb0 + g (back-substitution per column)
+    for (int jb0 = 0; jb0 < nbk; jb0 += 4) {
+        const int j = jb0 + (lane >> 3), l8 = lane & 7;
+        const int c = 8 * j + l8;
+        const bool act = c < p;
+        const double rc = act ? rinv[c] : 0.0;
+        f2 += rc * rc;
+        for (int kk = 6; kk >= 0; --kk) {
+            if (act && l8 > kk) {
+                const int k = 8 * j + kk;
+                double acc = W[(size_t)c * ld + k] * rc;                        // R[k,c] X[c,c]
+                for (int i = k + 1; i < c; ++i) acc += W[(size_t)i * ld + k] * W[(size_t)i * ld + c];   // R[k,i] X[i,c]
+                const double x = -rinv[k] * acc;
+                W[(size_t)k * ld + c] = x;
+                f2 += x * x;
             }
         }
-        __syncwarp();
+    }
+    __syncwarp();
+    // blocks above the diagonal, column block by column block: X_ij = -X_ii sum_{i<k<=j} R_ik X_kj.  Only X_jj, X_ii and the
+    // last (possibly partial) block column need the guarded element access.
+    for (int j = 1; j < nbk; ++j) {
+        const bool jfull = 8 * j + 8 <= p;
         for (int i = j - 1; i >= 0; --i) {
             double s0 = 0.0, s1 = 0.0;
-            for (int k = i + 1; k <= j; ++k) {
+            for (int k = i + 1; k < j; ++k) {                                   // dense R_ik (8 k + 7 < p) and dense X_kj
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
-                    const double a = r_elem(W, ld, p, 8 * i + m, 8 * k + 4 * h + t4);
-                    const double b = x_elem(W, rinv, ld, p, 8 * k + 4 * h + t4, 8 * j + m);
+                    const double a = W[(size_t)(8 * k + 4 * h + t4) * ld + 8 * i + m];
+                    const double b = jfull ? W[(size_t)(8 * k + 4 * h + t4) * ld + 8 * j + m]
+                                           : x_elem(W, rinv, ld, p, 8 * k + 4 * h + t4, 8 * j + m);
                     mma_f64(s0, s1, a, b);
                 }
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {                                       // k = j: R_ij may be partial, X_jj is triangular
+                const double a = r_elem(W, ld, p, 8 * i + m, 8 * j + 4 * h + t4);
+                const double b = x_elem(W, rinv, ld, p, 8 * j + 4 * h + t4, 8 * j + m);
+                mma_f64(s0, s1, a, b);
             }
             stage[m * 8 + 2 * t4] = s0;                     // S (8 x 8, row-major) -> B fragments of the next product
             stage[m * 8 + 2 * t4 + 1] = s1;
@@ -569,10 +586,17 @@ __device__ void inverse_norms_mma(double *W, const double *rinv, int ld, int p, 
         for (int b = a; b < nbk; ++b) {
             double h0 = 0.0, h1 = 0.0;
             for (int c = b; c < nbk; ++c) {
+                const bool plain = c > b && 8 * c + 8 <= p;                     // both blocks dense and inside the matrix
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
-                    const double av = x_elem(W, rinv, ld, p, 8 * a + m, 8 * c + 4 * h + t4);
-                    const double bv = x_elem(W, rinv, ld, p, 8 * b + m, 8 * c + 4 * h + t4);   // (X_bc^T)[k][n] = X_bc[n][k]
+                    double av, bv;
+                    if (plain) {
+                        av = W[(size_t)(8 * a + m) * ld + 8 * c + 4 * h + t4];
+                        bv = W[(size_t)(8 * b + m) * ld + 8 * c + 4 * h + t4];
+                    } else {
+                        av = x_elem(W, rinv, ld, p, 8 * a + m, 8 * c + 4 * h + t4);
+                        bv = x_elem(W, rinv, ld, p, 8 * b + m, 8 * c + 4 * h + t4);   // (X_bc^T)[k][n] = X_bc[n][k]
+                    }
                     mma_f64(h0, h1, av, bv);
                 }
             }
