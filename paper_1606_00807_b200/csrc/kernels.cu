@@ -834,6 +834,9 @@ __global__ void __launch_bounds__(256, 1) regress_qr_mma_kernel(const RegressPar
     const double denom = (double)(N - 1);
     const unsigned nf = (unsigned)(P.f1 - P.f0);
     const int pig = 4 * (g8 & 1) + (g8 >> 1);              // row (within an m-tile) of accumulator column n = g8
+    __shared__ int s_voff[16], s_vp[16];                   // offset and pitch of every reflector block (p <= 128)
+    if (threadIdx.x < 16) { s_voff[threadIdx.x] = qrm_block_off(NT, threadIdx.x); s_vp[threadIdx.x] = qrm_block_vp(NT, threadIdx.x); }
+    __syncthreads();
 
     for (;;) {
         unsigned int wk = 0;
@@ -885,8 +888,8 @@ __global__ void __launch_bounds__(256, 1) regress_qr_mma_kernel(const RegressPar
             // ---- earlier reflector blocks: C <- C - V T^T (V^T C) ----
             for (int ob = 0; ob < o && ob < K; ob += 8) {
                 const int mb = ob >> 3;
-                const int VP = qrm_block_vp(NT, mb);
-                const double *Vblk = Vs + qrm_block_off(NT, mb) - 8 * mb;      // row r of reflector k: Vblk[k * VP + r]
+                const int VP = s_vp[mb];
+                const double *Vblk = Vs + s_voff[mb] - 8 * mb;                 // row r of reflector k: Vblk[k * VP + r]
                 const double *Vb = Vblk + (size_t)g8 * VP + t4;
                 double wa0 = 0.0, wa1 = 0.0, wb0 = 0.0, wb1 = 0.0, wc0 = 0.0, wc1 = 0.0, wd0 = 0.0, wd1 = 0.0;
 #pragma unroll
@@ -927,8 +930,8 @@ __global__ void __launch_bounds__(256, 1) regress_qr_mma_kernel(const RegressPar
                 } else if (mt == m0) { dt[0] = c[mt][0]; dt[1] = c[mt][1]; c[mt][0] = 0.0; c[mt][1] = 0.0; }
             }
             // ---- factor the block in registers ----
-            const int VPown = qrm_block_vp(NT, m0);
-            double *Vown = Vs + qrm_block_off(NT, m0) - 8 * m0;               // this block's reflectors, if stored
+            const int VPown = s_vp[m0 & 15];
+            double *Vown = Vs + s_voff[m0 & 15] - 8 * m0;                     // this block's reflectors, if stored
             double Trow[8];                              // row g8 of the block's T
 #pragma unroll
             for (int k = 0; k < 8; ++k) Trow[k] = 0.0;

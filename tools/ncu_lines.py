@@ -37,9 +37,9 @@ for s in sections[1:]:
 assert sec is not None, kname
 addr2line, cur = {}, None
 for ln in sec.split("\n"):
-    m = re.search(r'//## File ".*?", line (\d+)', ln)
-    if m:
-        cur = int(m.group(1))
+    m = re.search(r'//## File "(.*?)", line (\d+)', ln)
+    if m:   # lines of inlined CUDA header code (shuffles, math) keep their header name
+        cur = int(m.group(2)) if m.group(1).endswith("kernels.cu") else os.path.basename(m.group(1)) + ":" + m.group(2)
         continue
     m = re.match(r"\s*/\*([0-9a-f]+)\*/\s+\S", ln)
     if m:
@@ -58,4 +58,5 @@ src = open(os.path.join(ROOT, "paper_1606_00807_b200", "csrc", "kernels.cu")).re
 tot, ts = sum(a[0] for a in agg.values()), sum(a[1] for a in agg.values())
 print(f"{kname}: {tot:.4g} warp instructions, {ts} samples")
 for l, a in sorted(agg.items(), key=lambda kv: -kv[1][0])[:top]:
-    print("%5.1f%% inst %5.1f%% samp  L%s: %s" % (100 * a[0] / tot, 100 * a[1] / max(ts, 1), l, src[l - 1].strip()[:105] if l else "?"))
+    text = src[l - 1].strip()[:105] if isinstance(l, int) else ("(CUDA header) " + l if l else "?")
+    print("%5.1f%% inst %5.1f%% samp  L%s: %s" % (100 * a[0] / tot, 100 * a[1] / max(ts, 1), l if isinstance(l, int) else 0, text))
