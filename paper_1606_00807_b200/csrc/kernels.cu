@@ -416,8 +416,10 @@ __device__ __forceinline__ void vstore(double *dst, const Vec<PS> &a, int p, int
 }
 
 // x = R^-1 b  (R upper triangular in W, diagonal reciprocals in rinv); b is overwritten.
+// (called, not inlined: regress_solve_kernel has a dozen call sites and was 21 k instructions long, far beyond the
+// instruction cache)
 template <int PS>
-__device__ __forceinline__ void solve_upper(Vec<PS> &b, const double *W, const double *rinv, int ld, int p, int lane) {
+__device__ __noinline__ Vec<PS> solve_upper(Vec<PS> b, const double *W, const double *rinv, int ld, int p, int lane) {
     // element k is final when column k is reached and never touched again: x = b * rinv once at the end
     const Vec<PS> rv = vload<PS>(rinv, p, lane);
 #pragma unroll
@@ -434,11 +436,12 @@ __device__ __forceinline__ void solve_upper(Vec<PS> &b, const double *W, const d
     }
 #pragma unroll
     for (int t = 0; t < PS; ++t) b.v[t] *= rv.v[t];
+    return b;
 }
 
 // u = R^-T z ; z is overwritten.
 template <int PS>
-__device__ __forceinline__ void solve_upper_t(Vec<PS> &z, const double *W, const double *rinv, int ld, int p, int lane) {
+__device__ __noinline__ Vec<PS> solve_upper_t(Vec<PS> z, const double *W, const double *rinv, int ld, int p, int lane) {
     const Vec<PS> rv = vload<PS>(rinv, p, lane);
 #pragma unroll
     for (int sk = 0; sk < PS; ++sk) {
@@ -456,11 +459,12 @@ __device__ __forceinline__ void solve_upper_t(Vec<PS> &z, const double *W, const
     }
 #pragma unroll
     for (int t = 0; t < PS; ++t) z.v[t] *= rv.v[t];
+    return z;
 }
 
 // y = R v
 template <int PS>
-__device__ __forceinline__ Vec<PS> mul_upper(const Vec<PS> &v, const double *W, int ld, int p, int lane) {
+__device__ __noinline__ Vec<PS> mul_upper(const Vec<PS> v, const double *W, int ld, int p, int lane) {
     Vec<PS> y;
 #pragma unroll
     for (int t = 0; t < PS; ++t) y.v[t] = 0.0;
@@ -481,7 +485,7 @@ __device__ __forceinline__ Vec<PS> mul_upper(const Vec<PS> &v, const double *W, 
 
 // w = R^T y
 template <int PS>
-__device__ __forceinline__ Vec<PS> mul_upper_t(const Vec<PS> &y, const double *W, int ld, int p, int lane) {
+__device__ __noinline__ Vec<PS> mul_upper_t(const Vec<PS> y, const double *W, int ld, int p, int lane) {
     Vec<PS> w;
 #pragma unroll
     for (int t = 0; t < PS; ++t) w.v[t] = 0.0;
@@ -520,7 +524,7 @@ __device__ __forceinline__ double x_elem(const double *W, const double *rinv, in
 // |X|_F^2 = sum 1/s_i^2 and |X X^T|_F^2 = sum 1/s_i^4 of X = R^-1, by 8 x 8 blocks on the FP64 tensor
 // cores (mma.sync m8n8k4): X_jj by back-substitution (one lane per column), X_ij = -X_ii sum_k R_ik X_kj.
 // X^T is left in the strict lower triangle of W; stage = 64 doubles of per-warp scratch.
-__device__ void inverse_norms_mma(double *W, const double *rinv, int ld, int p, double *stage, int lane, double *n2,
+__device__ __noinline__ void inverse_norms_mma(double *W, const double *rinv, int ld, int p, double *stage, int lane, double *n2,
                                   double *n4) {
     const int t4 = lane & 3, m = lane >> 2;
     const int nbk = (p + 7) >> 3;
@@ -610,7 +614,7 @@ __device__ void inverse_norms_mma(double *W, const double *rinv, int ld, int p, 
 // General fallback: one-sided Jacobi SVD on the rows of [R | c] (K x (p+1), explicit zeros below
 // the diagonal), truncation as estimator.py:55-57.  Writes beta to out[0..p); returns flag bits and
 // the squared norm of the truncated part of c in *dropped2.
-__device__ int jacobi_solve(double *W, int ld, int K, int p, double rank_tol, double *s2buf, double *coef,
+__device__ __noinline__ int jacobi_solve(double *W, int ld, int K, int p, double rank_tol, double *s2buf, double *coef,
                             double *out, double *dropped2, int lane) {
     int flag = 0;
     const int M = (K + 1) & ~1;
@@ -1141,8 +1145,8 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
                 double dz_old = 1.0;
                 for (int it = 0; it < INVIT_MAX; ++it) {
                     Vec<PS> zz = z;
-                    solve_upper_t<PS>(zz, W, rinv, ld, p, lane);
-                    solve_upper<PS>(zz, W, rinv, ld, p, lane);
+                    zz = solve_upper_t<PS>(zz, W, rinv, ld, p, lane);
+                    zz = solve_upper<PS>(zz, W, rinv, ld, p, lane);
                     for (int mm = 0; mm < m; ++mm) {
                         const Vec<PS> zm = vload<PS>(Zs + mm * pmax, p, lane);
                         const double pr = vdot<PS>(zz, zm);
@@ -1188,8 +1192,8 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
                     double w2 = 0.0, res2 = 0.0;
                     for (int k = 0; k < m; ++k) {
                         Vec<PS> w = vload<PS>(Zs + k * pmax, p, lane);
-                        solve_upper_t<PS>(w, W, rinv, ld, p, lane);
-                        solve_upper<PS>(w, W, rinv, ld, p, lane);
+                        w = solve_upper_t<PS>(w, W, rinv, ld, p, lane);
+                        w = solve_upper<PS>(w, W, rinv, ld, p, lane);
                         vstore<PS>(Ws + k * pmax, w, p, lane);
                         w2 += vdot<PS>(w, w);
                     }
@@ -1347,7 +1351,7 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
 #pragma unroll
                 for (int t = 0; t < PS; ++t) b.v[t] -= pr * xm.v[t];
             }
-            solve_upper<PS>(b, W, rinv, ld, p, lane);
+            b = solve_upper<PS>(b, W, rinv, ld, p, lane);
             for (int mm = 0; mm < m; ++mm) {
                 const Vec<PS> zm = vload<PS>(Zs + mm * pmax, p, lane);
                 const double pr = vdot<PS>(b, zm);
@@ -1474,8 +1478,10 @@ cudaError_t launch_regress(const RegressParams &p_in, int sm_count, size_t smem_
             if (wn < 1 || wn < std::min(warps1, 16) - 2) break;
             ++p.maxdefl;
         }
+        if (const char *denv = getenv("ENKFMC_K2B_MAXDEFL")) { const int dv = atoi(denv); if (dv >= 1 && dv <= REG_MAXDEFL_CAP) p.maxdefl = dv; }
         warps = (int)(smem_limit / (regress_solve_ws_doubles(p.pmax, p.maxdefl) * sizeof(double)));
         if (warps > 16) warps = 16;
+        if (const char *wenv = getenv("ENKFMC_K2B_WARPS")) { const int wv = atoi(wenv); if (wv >= 1 && wv < warps) warps = wv; }
         const size_t ws = regress_solve_ws_doubles(p.pmax, p.maxdefl) * sizeof(double);
         int64_t grid = sm_count;
         const int64_t need = (p.nwork + warps - 1) / warps;
