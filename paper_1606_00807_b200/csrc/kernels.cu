@@ -524,11 +524,10 @@ __device__ __forceinline__ double x_elem(const double *W, const double *rinv, in
 // |X|_F^2 = sum 1/s_i^2 and |X X^T|_F^2 = sum 1/s_i^4 of X = R^-1, by 8 x 8 blocks on the FP64 tensor
 // cores (mma.sync m8n8k4): X_jj by back-substitution (one lane per column), X_ij = -X_ii sum_k R_ik X_kj.
 // X^T is left in the strict lower triangle of W; stage = 64 doubles of per-warp scratch.
-__device__ __noinline__ void inverse_norms_mma(double *W, const double *rinv, int ld, int p, double *stage, int lane, double *n2,
-                                  double *n4) {
+__device__ __noinline__ double inverse_norm2_mma(double *W, const double *rinv, int ld, int p, double *stage, int lane) {
     const int t4 = lane & 3, m = lane >> 2;
     const int nbk = (p + 7) >> 3;
-    double f2 = 0.0, g4 = 0.0;
+    double f2 = 0.0;
     // diagonal blocks, four at a time: lanes 8 g .. 8 g + 7 own the columns of block jb0 + g (back-substitution per column)
     for (int jb0 = 0; jb0 < nbk; jb0 += 4) {
         const int j = jb0 + (lane >> 3), l8 = lane & 7;
@@ -585,7 +584,15 @@ __device__ __noinline__ void inverse_norms_mma(double *W, const double *rinv, in
             __syncwarp();
         }
     }
-    // H = X X^T by blocks a <= b: H_ab = sum_{c >= b} X_ac X_bc^T ; only its Frobenius norm is needed
+    return warp_sum(f2);
+}
+
+// |X X^T|_F^2 = sum 1/s_i^4 from the X left in W by inverse_norm2_mma (computed only when the second-power bound
+// alone does not settle a row).  H = X X^T by blocks a <= b: H_ab = sum_{c >= b} X_ac X_bc^T.
+__device__ __noinline__ double xxt_norm4_mma(const double *W, const double *rinv, int ld, int p, int lane) {
+    const int t4 = lane & 3, m = lane >> 2;
+    const int nbk = (p + 7) >> 3;
+    double g4 = 0.0;
     for (int a = 0; a < nbk; ++a) {
         for (int b = a; b < nbk; ++b) {
             double h0 = 0.0, h1 = 0.0;
@@ -607,8 +614,7 @@ __device__ __noinline__ void inverse_norms_mma(double *W, const double *rinv, in
             g4 += (a == b ? 1.0 : 2.0) * (h0 * h0 + h1 * h1);
         }
     }
-    *n2 = warp_sum(f2);
-    *n4 = warp_sum(g4);
+    return warp_sum(g4);
 }
 
 // General fallback: one-sided Jacobi SVD on the rows of [R | c] (K x (p+1), explicit zeros below
@@ -1106,8 +1112,7 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
                 }
                 power_done += iters;
             };
-            power(2);                        // two steps put the lower bound within a few per cent of s_max
-            bool refined = false;
+            bool refined = false;            // (the power iteration runs only for rows that need a probe)
             double smax_hi = fro;            // upper bound of s_max: |R|_F until the power iteration has converged
             // probes: smallest singular triplets by inverse iteration, deflating truncated ones
             // Rigorous certificate for "nothing (left) below the threshold": with X = R^-1,
@@ -1117,7 +1122,8 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
             // The fourth-power bound is within a few per cent of s_next even for clustered spectra.
             double tail2 = 0.0, tail4 = 0.0; // sum 1/s^2 and sum 1/s^4 over the singular values not yet deflated
             bool ok2 = true, ok4 = true;     // false once cancellation has eaten the respective certificate
-            inverse_norms_mma(W, rinv, ld, p, stage, lane, &tail2, &tail4);
+            tail2 = inverse_norm2_mma(W, rinv, ld, p, stage, lane);
+            bool have4 = false;              // the fourth-power sum is formed on demand
             // One inverse-iteration probe in the complement of the deflated vectors, from a pseudo-random
             // start.  The estimate bounds the smallest remaining singular value from above; once it is below
             // rank_tol * lower(s_max) the truncation is proven and the vector is iterated to convergence.
@@ -1254,7 +1260,8 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
 
             // depends on the regression only (not on the field, nor on which tile's copy of the row is computed)
             unsigned seed = (unsigned)P.state_row[q] * 7919u + (unsigned)p * 104729u;
-            const double T2 = tail2, T4 = tail4;   // totals over all singular values
+            const double T2 = tail2;               // totals over all singular values
+            double T4 = 0.0;
             double def2 = 0.0, def4 = 0.0;         // part carried by the deflated block
             double smin_defl = smax_lo;            // smallest deflated singular value (cancellation guard)
             bool polished = true;                  // the block spans an invariant subspace to rounding
@@ -1263,13 +1270,19 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
                 // X carries a relative error of at most about c eps cond(R); add it to what is left, so the bound
                 // stays a lower bound (it merely becomes useless once cancellation has eaten the sums)
                 tail2 = T2 - def2;
-                tail4 = T4 - def4;
                 const double noise = 2.2e-14 * (smax_hi / smin_defl);
-                const double up2 = fmax(tail2, 0.0) + noise * T2, up4 = fmax(tail4, 0.0) + 4.0 * noise * T4;
+                const double up2 = fmax(tail2, 0.0) + noise * T2;
                 ok2 = tail2 > -noise * T2;                                   // a clearly negative remainder: inconsistent sums
-                ok4 = tail4 > -4.0 * noise * T4;
-                const double lb = fmax(ok2 ? 1.0 / sqrt(up2) : 0.0, ok4 ? 1.0 / sqrt(sqrt(up4)) : 0.0);   // s_next >= lb
-                const bool done = lb >= P.rank_tol * smax_hi * (1.0 + 1e-3);
+                double lb = ok2 ? 1.0 / sqrt(up2) : 0.0;                     // s_next >= lb
+                bool done = lb >= P.rank_tol * smax_hi * (1.0 + 1e-3);
+                if (!done) {                                                 // sharpen with the fourth-power sum
+                    if (!have4) { T4 = xxt_norm4_mma(W, rinv, ld, p, lane); have4 = true; }
+                    tail4 = T4 - def4;
+                    const double up4 = fmax(tail4, 0.0) + 4.0 * noise * T4;
+                    ok4 = tail4 > -4.0 * noise * T4;
+                    lb = fmax(lb, ok4 ? 1.0 / sqrt(sqrt(up4)) : 0.0);
+                    done = lb >= P.rank_tol * smax_hi * (1.0 + 1e-3);
+                }
                 if (done && polished) break;                                 // nothing (left) to truncate
                 if (done || (!polished && m >= P.maxdefl)) {                 // verify / sharpen the block first
                     const int pr = polish(def2, def4);
@@ -1279,6 +1292,7 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
                     continue;
                 }
                 if (m >= P.maxdefl) { fallback = true; why = 3; break; }
+                if (power_done == 0) power(2);   // two steps put the lower bound of s_max within a few per cent
                 Vec<PS> z;
                 double zMz, Mz2;
                 const int found = probe(seed++, z, zMz, Mz2);
