@@ -704,33 +704,36 @@ __device__ __forceinline__ int64_t packed_col_offset(int j, int K) {
     return j <= K ? (int64_t)j * (j + 1) / 2 : (int64_t)K * (K + 1) / 2 + (int64_t)(j - K) * K;
 }
 
-// Packed block -> dense [R | c] with p rows (rows >= K and the strict lower part are zero).
+// Packed block -> dense [R | c] with p rows (rows >= K and the strict lower part are zero); p <= 32 PS.
+// *fro2 (if asked for) = |R|_F^2.
+template <int PS>
 __device__ __forceinline__ void unpack_rc(const double *in, double *W, int ld, int p, int K, int lane,
-                                          double *fro2 = nullptr, double *maxcol2 = nullptr) {
-    double f2 = 0.0, mc2 = 0.0;
+                                          double *fro2 = nullptr) {
+    double f2 = 0.0;
     for (int j0 = 0; j0 <= p; j0 += 4) {               // four columns in flight: the loads are latency-bound
-        double v[4][3];
+        double v[4][PS];
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
             const int j = j0 + b <= p ? j0 + b : p;
             const int h = j < p ? (j + 1 < K ? j + 1 : K) : K;
             const double *src = in + packed_col_offset(j, K);
 #pragma unroll
-            for (int t = 0; t < 3; ++t) { const int i = lane + 32 * t; v[b][t] = i < h ? src[i] : 0.0; }
+            for (int t = 0; t < PS; ++t) { const int i = lane + 32 * t; v[b][t] = i < h ? src[i] : 0.0; }
         }
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
             const int j = j0 + b;
             if (j > p) break;
             double *col = W + (size_t)j * ld;
-            double c2 = 0.0;
 #pragma unroll
-            for (int t = 0; t < 3; ++t) { const int i = lane + 32 * t; if (i < p) col[i] = v[b][t]; c2 += v[b][t] * v[b][t]; }
-            if (maxcol2 && j < p) { c2 = warp_sum(c2); f2 += c2; mc2 = fmax(mc2, c2); }
+            for (int t = 0; t < PS; ++t) {
+                const int i = lane + 32 * t;
+                if (i < p) col[i] = v[b][t];
+                if (j < p) f2 = fma(v[b][t], v[b][t], f2);
+            }
         }
     }
-    if (fro2) *fro2 = f2;
-    if (maxcol2) *maxcol2 = mc2;
+    if (fro2) *fro2 = warp_sum(f2);
 }
 
 }  // namespace
@@ -1071,12 +1074,12 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
         const int p = (int)(P.row_ptr[q + 1] - r0);
         if (p == 0) continue;                    // done in K2a
         const int K = p < N ? p : N;
-        int flag = 0;
+        int flag = 0, nsteps = 0;               // nsteps: inverse-iteration steps spent on this row (flag bits 8-15)
 
         // ---- unpack R | c into the dense workspace, zeros below the diagonal ---------------
         const double *in = P.Rq + (int64_t)fl * P.rq_stride + P.rq_ptr[q];
-        double dmin = DBL_MAX, dmax = 0.0, fro2 = 0.0, maxcol2 = 0.0;
-        unpack_rc(in, W, ld, p, K, lane, &fro2, &maxcol2);
+        double dmin = DBL_MAX, dmax = 0.0, fro2 = 0.0;
+        unpack_rc<PS>(in, W, ld, p, K, lane, &fro2);
         __syncwarp();
         for (int j = lane; j < K; j += 32) {
             const double v = W[(size_t)j * ld + j];
@@ -1098,7 +1101,7 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
             Vec<PS> v;
 #pragma unroll
             for (int t = 0; t < PS; ++t) v.v[t] = (lane + 32 * t < p) ? 1.0 : 0.0;
-            double smax_lo = fmax(dmax, sqrt(maxcol2));   // |R e_j| <= s_max
+            double smax_lo = dmax;                        // |r_jj| <= |R e_j| <= s_max
             int power_done = 0;
             auto power = [&](int iters) {
                 for (int it = 0; it < iters; ++it) {
@@ -1150,6 +1153,7 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
                 }
                 double dz_old = 1.0;
                 for (int it = 0; it < INVIT_MAX; ++it) {
+                    ++nsteps;
                     Vec<PS> zz = z;
                     zz = solve_upper_t<PS>(zz, W, rinv, ld, p, lane);
                     zz = solve_upper<PS>(zz, W, rinv, ld, p, lane);
@@ -1176,6 +1180,9 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
                     dz = sqrt(warp_sum(dz));
                     if (s_est < P.rank_tol * smax_lo) {          // s_next <= s_est < tol * s_max: truncated for sure
                         if ((dz < 1e-6 && dz > 0.9 * dz_old) || dz < 1e-12) return 2;      // at the rounding floor
+                        // linear convergence with ratio q = dz / dz_old: the iterate just computed is within
+                        // dz q / (1 - q) of the limit -- stop once that is at the 5e-14 level
+                        if (it >= 2 && dz < 0.25 * dz_old && dz * dz < 4e-14 * dz_old) return 2;
                         // slow phase: what still moves is a rotation among close sub-threshold directions --
                         // hand the vector to the block polish
                         if (it >= 6 && dz < 1e-2 && dz > 0.4 * dz_old && dz < 0.95 * dz_old) return 1;
@@ -1376,7 +1383,7 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
             __syncwarp();
         } else {
             flag |= 1 | 16 | (why << 5);
-            unpack_rc(in, W, ld, p, K, lane);      // the lower triangle may hold X^T
+            unpack_rc<PS>(in, W, ld, p, K, lane);  // the lower triangle may hold X^T
             __syncwarp();
             double dropped2;
             flag |= jacobi_solve(W, ld, K, p, P.rank_tol, rinv, tmp, aux, &dropped2, lane);
@@ -1388,7 +1395,7 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
         // singular values were truncated, and is then evaluated explicitly from R, c and beta.
         double rest2 = 0.0;
         if (fallback || m > 0) {
-            if (fallback) { unpack_rc(in, W, ld, p, K, lane); __syncwarp(); }
+            if (fallback) { unpack_rc<PS>(in, W, ld, p, K, lane); __syncwarp(); }
             const Vec<PS> b = vload<PS>(aux, p, lane);
             const Vec<PS> rb = mul_upper<PS>(b, W, ld, p, lane);
             const Vec<PS> c0 = vload<PS>(cvec, p, lane);
@@ -1400,7 +1407,7 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
             const double d = (e2 + rest2) / denom;
             if (d < P.variance_floor) flag |= 8;
             P.D[(int64_t)f * P.nloc + q] = fmax(d, P.variance_floor);
-            if (P.flags) P.flags[(int64_t)f * P.nloc + q] = flag;
+            if (P.flags) P.flags[(int64_t)f * P.nloc + q] = flag | ((nsteps < 255 ? nsteps : 255) << 8);
         }
         __syncwarp();
     }

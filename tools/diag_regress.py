@@ -42,5 +42,8 @@ for lo, hi in [(0, 1), (1, 16), (16, 32), (32, 41), (41, 61), (61, 200)]:
         print(f"  p in [{lo},{hi}): rows {int(sel.sum())}  truncated {int(((flags[sel] & 2) > 0).sum())}  "
               f"fallback {int(((flags[sel] & 16) > 0).sum())}")
 print("fallback reasons (1 zero pivot / p>N, 2 certificate inconclusive, 3 out of deflation slots, 4 refined s above threshold, 5 certificate lost to cancellation, 6 polish not converged, 7 kept direction in block):", np.bincount((flags[(flags & 16) > 0] >> 5) & 7, minlength=8))
+steps = (flags >> 8) & 255
+tr = (flags & 2) > 0
+print("inverse-iteration steps per truncated row: mean %.2f, histogram" % steps[tr].mean(), np.bincount(steps[tr], minlength=12)[:16])
 fl = plan.work(w.nens)
 print("algorithmic GF regress/solve:", fl[2] / 1e9, fl[1] / 1e9, " -> TF/s", fl[2] / ((ms[1] + ms[2]) / n) / 1e9, fl[1] / (ms[3] / n) / 1e9)
