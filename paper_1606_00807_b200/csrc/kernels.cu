@@ -617,6 +617,49 @@ __device__ __noinline__ double xxt_norm4_mma(const double *W, const double *rinv
     return warp_sum(g4);
 }
 
+// |X - (X U) U^T|_F^2 for m p-vectors U (rows of Us, pitch pmax), X = R^-1 as left in W by inverse_norm2_mma.
+// (X U) U^T has rank <= m, so by Eckart-Young sigma_{m+1}(X) <= |X - (X U) U^T|_2 <= the Frobenius norm returned,
+// whatever U is: 1 / sqrt(result) is a rigorous lower bound of the (m+1)-th smallest singular value of R.  Formed
+// element by element, it does not suffer the cancellation of |X|_F^2 - sum 1/s_k^2 when cond(R) is large.
+template <int PS, int M>
+__device__ __noinline__ double deflated_inverse_norm2(const double *W, const double *rinv, int ld, int p, const double *Us,
+                                                      int pmax, int m, int lane) {
+    double Y[PS][M];                                        // (X U)[lane + 32 t][k]
+#pragma unroll
+    for (int t = 0; t < PS; ++t)
+#pragma unroll
+        for (int k = 0; k < M; ++k) Y[t][k] = 0.0;
+    for (int c = 0; c < p; ++c) {
+        double uc[M];
+#pragma unroll
+        for (int k = 0; k < M; ++k) uc[k] = k < m ? Us[(size_t)k * pmax + c] : 0.0;
+        const double dg = rinv[c];
+#pragma unroll
+        for (int t = 0; t < PS; ++t) {
+            const int r = lane + 32 * t;
+            const double x = r < c ? W[(size_t)r * ld + c] : (r == c ? dg : 0.0);
+#pragma unroll
+            for (int k = 0; k < M; ++k) Y[t][k] = fma(x, uc[k], Y[t][k]);
+        }
+    }
+    double acc = 0.0;
+    for (int c = 0; c < p; ++c) {
+        double uc[M];
+#pragma unroll
+        for (int k = 0; k < M; ++k) uc[k] = k < m ? Us[(size_t)k * pmax + c] : 0.0;
+        const double dg = rinv[c];
+#pragma unroll
+        for (int t = 0; t < PS; ++t) {
+            const int r = lane + 32 * t;
+            double e = r < c ? W[(size_t)r * ld + c] : (r == c ? dg : 0.0);
+#pragma unroll
+            for (int k = 0; k < M; ++k) e = fma(-Y[t][k], uc[k], e);
+            if (r < p) acc = fma(e, e, acc);
+        }
+    }
+    return warp_sum(acc);
+}
+
 // General fallback: one-sided Jacobi SVD on the rows of [R | c] (K x (p+1), explicit zeros below
 // the diagonal), truncation as estimator.py:55-57.  Writes beta to out[0..p); returns flag bits and
 // the squared norm of the truncated part of c in *dropped2.
@@ -1096,6 +1139,25 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
         bool fallback = (K < p) || !(dmin > 1e-13 * dmax);
         int m = 0, why = fallback ? 1 : 0;   // fallback reason, reported in flag bits 5-7
 
+        // left singular subspace of the deflated values: orthonormal basis of R^-T Z in Ws (Z spans the right one;
+        // R^-T z is accurate to eps |R| / gap in direction, R z would only be to eps cond(R))
+        auto build_left_basis = [&]() {
+            for (int mm = 0; mm < m; ++mm) {
+                Vec<PS> xm = vload<PS>(Zs + mm * pmax, p, lane);
+                xm = solve_upper_t<PS>(xm, W, rinv, ld, p, lane);
+                for (int l = 0; l < mm; ++l) {
+                    const Vec<PS> xl = vload<PS>(Ws + l * pmax, p, lane);
+                    const double g = vdot<PS>(xl, xm);
+#pragma unroll
+                    for (int t = 0; t < PS; ++t) xm.v[t] -= g * xl.v[t];
+                }
+                const double inv = 1.0 / sqrt(vdot<PS>(xm, xm));
+#pragma unroll
+                for (int t = 0; t < PS; ++t) xm.v[t] *= inv;
+                vstore<PS>(Ws + mm * pmax, xm, p, lane);
+                __syncwarp();
+            }
+        };
         if (!fallback) {
             // s_max bracket: power iteration from below, Frobenius norm from above
             Vec<PS> v;
@@ -1269,6 +1331,7 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
             unsigned seed = (unsigned)P.state_row[q] * 7919u + (unsigned)p * 104729u;
             const double T2 = tail2;               // totals over all singular values
             double T4 = 0.0;
+            int ey_m = 0;                          // number of deflated vectors the Eckart-Young bound was last formed for
             double def2 = 0.0, def4 = 0.0;         // part carried by the deflated block
             double smin_defl = smax_lo;            // smallest deflated singular value (cancellation guard)
             bool polished = true;                  // the block spans an invariant subspace to rounding
@@ -1289,6 +1352,21 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
                     ok4 = tail4 > -4.0 * noise * T4;
                     lb = fmax(lb, ok4 ? 1.0 / sqrt(sqrt(up4)) : 0.0);
                     done = lb >= P.rank_tol * smax_hi * (1.0 + 1e-3);
+                }
+                if (!done && m > 0 && polished && ey_m != m) {               // scalar sums exhausted: explicit deflation of X
+                    ey_m = m;
+                    build_left_basis();
+                    double e2x;
+                    if (m <= 1) e2x = deflated_inverse_norm2<PS, 1>(W, rinv, ld, p, Ws, pmax, m, lane);
+                    else if (m <= 2) e2x = deflated_inverse_norm2<PS, 2>(W, rinv, ld, p, Ws, pmax, m, lane);
+                    else if (m <= 4) e2x = deflated_inverse_norm2<PS, 4>(W, rinv, ld, p, Ws, pmax, m, lane);
+                    else if (m <= 8) e2x = deflated_inverse_norm2<PS, 8>(W, rinv, ld, p, Ws, pmax, m, lane);
+                    else e2x = deflated_inverse_norm2<PS, REG_MAXDEFL_CAP>(W, rinv, ld, p, Ws, pmax, m, lane);
+                    // X carries a relative error of about noise: sigma(X_exact) <= sigma(X_computed) / (1 - noise)
+                    if (noise < 0.25 && e2x > 0.0) {
+                        lb = fmax(lb, (1.0 - noise) / sqrt(e2x));
+                        done = lb >= P.rank_tol * smax_hi * (1.0 + 1e-3);
+                    }
                 }
                 if (done && polished) break;                                 // nothing (left) to truncate
                 if (done || (!polished && m >= P.maxdefl)) {                 // verify / sharpen the block first
@@ -1349,22 +1427,7 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
 
         if (!fallback) {
             if (m > 0) flag |= 1 | 2;
-            // left singular subspace of the truncated values: orthonormal basis of R Z (Z spans the right one)
-            for (int mm = 0; mm < m; ++mm) {
-                const Vec<PS> zm = vload<PS>(Zs + mm * pmax, p, lane);
-                Vec<PS> xm = mul_upper<PS>(zm, W, ld, p, lane);
-                for (int l = 0; l < mm; ++l) {
-                    const Vec<PS> xl = vload<PS>(Ws + l * pmax, p, lane);
-                    const double g = vdot<PS>(xl, xm);
-#pragma unroll
-                    for (int t = 0; t < PS; ++t) xm.v[t] -= g * xl.v[t];
-                }
-                const double inv = 1.0 / sqrt(vdot<PS>(xm, xm));
-#pragma unroll
-                for (int t = 0; t < PS; ++t) xm.v[t] *= inv;
-                vstore<PS>(Ws + mm * pmax, xm, p, lane);
-                __syncwarp();
-            }
+            build_left_basis();
             Vec<PS> b = vload<PS>(cvec, p, lane);
             for (int mm = 0; mm < m; ++mm) {         // c -= X X^T c
                 const Vec<PS> xm = vload<PS>(Ws + mm * pmax, p, lane);
@@ -1869,15 +1932,18 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
                 double piv = __shfl_sync(FULL, a[c], c);
                 // A = T~^T D^-1 T~ + H^T R^-1 H is positive semi-definite by construction, so a pivot at
                 // or below the rounding level of the largest pivot seen is cancellation noise, not
-                // indefiniteness: clamp it (counted) instead of failing.  NaN / inf still fail.
+                // indefiniteness: pin that variable (counted) instead of failing.  NaN / inf still fail.
+                bool pin = false;
                 if (!(piv == piv) || !(fabs(piv) < DBL_MAX)) { if (lane == 0) s_fail = 2; }
                 else if (!(piv > 1e-13 * pivmax)) {
                     if (pivmax == 0.0) { if (lane == 0) s_fail = 1; }           // non-positive leading entry
-                    else { piv = 1e-13 * pivmax; if (lane == 0) atomicAdd(P.counter + 1, 1u); }
+                    else { pin = true; if (lane == 0) atomicAdd(P.counter + 1, 1u); }
                 }
                 pivmax = fmax(pivmax, piv);
-                const double inv = rsqrt(piv);
-                a[c] = (r == c) ? piv * inv : a[c] * inv;             // column c of L
+                // a pinned variable gets the pivot +infinity: column of L zero, unit diagonal, zero increment -- no
+                // element growth, unlike a tiny positive pivot
+                const double inv = pin ? 0.0 : rsqrt(piv);
+                a[c] = (r == c) ? (pin ? 1.0 : piv * inv) : a[c] * inv;   // column c of L
 #pragma unroll
                 for (int k = 0; k <= c; ++k) if (r == c) v[k] *= inv; // row c of L^-1 is final
 #pragma unroll

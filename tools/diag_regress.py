@@ -45,5 +45,6 @@ print("fallback reasons (1 zero pivot / p>N, 2 certificate inconclusive, 3 out o
 steps = (flags >> 8) & 255
 tr = (flags & 2) > 0
 print("inverse-iteration steps per truncated row: mean %.2f, histogram" % steps[tr].mean(), np.bincount(steps[tr], minlength=12)[:16])
+print("pinned Cholesky pivots in the last analysis:", plan.counter(5))
 fl = plan.work(w.nens)
 print("algorithmic GF regress/solve:", fl[2] / 1e9, fl[1] / 1e9, " -> TF/s", fl[2] / ((ms[1] + ms[2]) / n) / 1e9, fl[1] / (ms[3] / n) / 1e9)
