@@ -1138,6 +1138,7 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
         const double *cvec = W + (size_t)p * ld;   // Q^T y
         bool fallback = (K < p) || !(dmin > 1e-13 * dmax);
         int m = 0, why = fallback ? 1 : 0;   // fallback reason, reported in flag bits 5-7
+        bool left_fresh = false;             // Ws holds the orthonormal left basis of the m deflated vectors
 
         // left singular subspace of the deflated values: orthonormal basis of R^-T Z in Ws (Z spans the right one;
         // R^-T z is accurate to eps |R| / gap in direction, R z would only be to eps cond(R))
@@ -1194,7 +1195,7 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
             // rank_tol * lower(s_max) the truncation is proven and the vector is iterated to convergence.
             // Returns true with the converged pair, false if the estimate stays above the threshold (the
             // certificate was inconclusive) or the vector does not converge (no gap).
-            auto probe = [&](unsigned seed, Vec<PS> &z, double &zMz, double &Mz2) -> int {
+            auto probe = [&](unsigned seed, Vec<PS> &z, double &zMz, double &Mz2, Vec<PS> &yt) -> int {
 #pragma unroll
                 for (int t = 0; t < PS; ++t) {
                     const int e = lane + 32 * t;
@@ -1218,6 +1219,7 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
                     ++nsteps;
                     Vec<PS> zz = z;
                     zz = solve_upper_t<PS>(zz, W, rinv, ld, p, lane);
+                    yt = zz;                                       // R^-T z: the left singular direction, for free
                     zz = solve_upper<PS>(zz, W, rinv, ld, p, lane);
                     for (int mm = 0; mm < m; ++mm) {
                         const Vec<PS> zm = vload<PS>(Zs + mm * pmax, p, lane);
@@ -1332,6 +1334,7 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
             const double T2 = tail2;               // totals over all singular values
             double T4 = 0.0;
             int ey_m = 0;                          // number of deflated vectors the Eckart-Young bound was last formed for
+            left_fresh = false;
             double def2 = 0.0, def4 = 0.0;         // part carried by the deflated block
             double smin_defl = smax_lo;            // smallest deflated singular value (cancellation guard)
             bool polished = true;                  // the block spans an invariant subspace to rounding
@@ -1355,7 +1358,7 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
                 }
                 if (!done && m > 0 && polished && ey_m != m) {               // scalar sums exhausted: explicit deflation of X
                     ey_m = m;
-                    build_left_basis();
+                    if (!left_fresh) { build_left_basis(); left_fresh = true; }
                     double e2x;
                     if (m <= 1) e2x = deflated_inverse_norm2<PS, 1>(W, rinv, ld, p, Ws, pmax, m, lane);
                     else if (m <= 2) e2x = deflated_inverse_norm2<PS, 2>(W, rinv, ld, p, Ws, pmax, m, lane);
@@ -1370,6 +1373,7 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
                 }
                 if (done && polished) break;                                 // nothing (left) to truncate
                 if (done || (!polished && m >= P.maxdefl)) {                 // verify / sharpen the block first
+                    left_fresh = false;                                      // polish uses Ws as scratch
                     const int pr = polish(def2, def4);
                     if (pr) { fallback = true; why = 5 + pr; break; }
                     polished = true;
@@ -1378,14 +1382,22 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
                 }
                 if (m >= P.maxdefl) { fallback = true; why = 3; break; }
                 if (power_done == 0) power(2);   // two steps put the lower bound of s_max within a few per cent
-                Vec<PS> z;
+                Vec<PS> z, yt;
                 double zMz, Mz2;
-                const int found = probe(seed++, z, zMz, Mz2);
+                const int found = probe(seed++, z, zMz, Mz2, yt);
                 if (found) {
-                    const Vec<PS> rz = mul_upper<PS>(z, W, ld, p, lane);
-                    const double sv = sqrt(vdot<PS>(rz, rz));
+                    // s = 1 / |R^-T z| (an upper bound of the singular value, like |R z|, but tight to second order
+                    // in the error of z) and u = R^-T z / |R^-T z| from the last solve of the probe
+                    const double ny = sqrt(vdot<PS>(yt, yt));
+                    const double sv = 1.0 / ny;
                     if (!(sv < P.rank_tol * smax_lo)) { fallback = true; why = 4; break; }
                     vstore<PS>(Zs + m * pmax, z, p, lane);
+                    left_fresh = (m == 0 && found == 2);           // a single converged pair: Ws[0] = u is the left basis
+                    if (left_fresh) {
+#pragma unroll
+                        for (int t = 0; t < PS; ++t) yt.v[t] *= sv;
+                        vstore<PS>(Ws, yt, p, lane);
+                    }
                     __syncwarp();
                     ++m;
                     smin_defl = fmin(smin_defl, sv);
@@ -1397,6 +1409,7 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
                     continue;
                 }
                 if (!polished) {                                             // a loose block can hide what is left
+                    left_fresh = false;                                      // polish uses Ws as scratch
                     const int pr = polish(def2, def4);
                     if (pr) { fallback = true; why = 5 + pr; break; }
                     polished = true;
@@ -1427,7 +1440,7 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
 
         if (!fallback) {
             if (m > 0) flag |= 1 | 2;
-            build_left_basis();
+            if (!left_fresh) build_left_basis();
             Vec<PS> b = vload<PS>(cvec, p, lane);
             for (int mm = 0; mm < m; ++mm) {         // c -= X X^T c
                 const Vec<PS> xm = vload<PS>(Ws + mm * pmax, p, lane);
