@@ -33,7 +33,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-NCU_TRAFFIC_K2 = 15.13e9         # dram bytes read + written per bench launch: K2a 3.58 + 5.55 GB, K2b 5.66 + 0.35 GB (ncu --set full)
+NCU_TRAFFIC_K2 = 15.15e9         # dram bytes read + written per bench launch: K2a 3.59 + 5.55 GB, K2b 5.65 + 0.35 GB (ncu --set full)
 NCU_TRAFFIC_SOURCE = "profiles/r1_ncu_full_k2_bench_launch.csv"
 METRIC = "EnKF-MC analysis grid-points/sec (B^-1 est + local solve)"
 UNIT = "grid-points/s"

@@ -1403,7 +1403,7 @@ __global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressPara
                     smin_defl = fmin(smin_defl, sv);
                     // triangular solves lose eps * cond digits: beyond cond ~ 5e9 the deflated subspace would be less
                     // accurate than the reference's SVD -- let the Jacobi SVD handle those rows
-                    if (smax_hi > 5e9 * smin_defl) { fallback = true; why = 5; break; }
+                    if (smax_hi > P.cond_max * smin_defl) { fallback = true; why = 5; break; }
                     if (found == 2 && polished) { const double i2 = 1.0 / (sv * sv); def2 += i2; def4 += i2 * i2; }
                     else { def2 += zMz; def4 += Mz2; polished = false; }
                     continue;
@@ -1575,6 +1575,8 @@ cudaError_t launch_regress(const RegressParams &p_in, int sm_count, size_t smem_
             if (wn < 1 || wn < std::min(warps1, 16) - 2) break;
             ++p.maxdefl;
         }
+        p.cond_max = 5e9;
+        if (const char *cenv = getenv("ENKFMC_K2B_CONDMAX")) { const double cv = atof(cenv); if (cv >= 1.0) p.cond_max = cv; }
         if (const char *denv = getenv("ENKFMC_K2B_MAXDEFL")) { const int dv = atoi(denv); if (dv >= 1 && dv <= REG_MAXDEFL_CAP) p.maxdefl = dv; }
         warps = (int)(smem_limit / (regress_solve_ws_doubles(p.pmax, p.maxdefl) * sizeof(double)));
         if (warps > 16) warps = 16;

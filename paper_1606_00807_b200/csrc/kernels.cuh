@@ -21,6 +21,7 @@ struct RegressParams {
     int32_t *flags;            // [nfields][nloc] or null
     unsigned int *counter;     // two work-fetch counters (zeroed by the launcher)
     int maxdefl;               // deflation vectors the workspace holds (set by the launcher)
+    double cond_max;           // rows whose deflated values reach cond(R) beyond this go to the Jacobi SVD (launcher)
     int f0, f1;                // fields handled by this launch pair (scratch is sized for f1 - f0)
     double *Rq;                // packed QR output scratch [f1 - f0][rq_stride]
     int64_t rq_stride;

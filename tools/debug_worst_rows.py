@@ -51,4 +51,5 @@ for q in order:
     s = np.linalg.svd(U[ii[ip[j]:ip[j + 1]]], compute_uv=False)
     near = s[np.argmin(np.abs(np.log10(s / (1e-8 * s[0]))))]
     print(f"row {q} tile {t} p {ip[j+1]-ip[j]} flag {F[q]} abs err {rowerr[q]:.2e} rel {rowerr[q]/rownorm[q]:.2e} |T row| {rownorm[q]:.2e} "
-          f"D rel err {abs(D[q]-Dref[q])/Dref[q]:.2e} m_ref {(s < 1e-8*s[0]).sum()} nearest s/thr - 1 = {near/(1e-8*s[0]) - 1:.3e}")
+          f"D rel err {abs(D[q]-Dref[q])/Dref[q]:.2e} m_ref {(s < 1e-8*s[0]).sum()} nearest s/thr - 1 = {near/(1e-8*s[0]) - 1:.3e}"
+          f" steps {(F[q] >> 8) & 255} smallest s/s0: {np.array2string(s[-6:][::-1] / s[0], precision=2)}")
