@@ -313,7 +313,7 @@ def run_b200(args, rank, world, local_rank):
                     "breakdown_ms": {"h2d": rep.t_h2d * 1e3, "estimation": float(rep.t_estimation.sum()) * 1e3,
                                      "analysis": float(rep.t_analysis.sum()) * 1e3, "d2h": rep.t_d2h * 1e3,
                                      "call_wall": rep.t_total * 1e3},
-                    "pipelined": "4 groups of fields: H2D of group g+1 and D2H of group g-1 overlap the kernels of group g",
+                    "pipelined": "5 groups of fields: H2D of group g+1 and D2H of group g-1 overlap the kernels of group g",
                     "h2d_bytes_per_step": int(w.X.nbytes + w.Ys.nbytes + w.r_diag.nbytes),
                     "d2h_bytes_per_step": int(w.X.nbytes),
                     "api": "assimilate_parallel(EnsembleState, ObservationNetwork, AssimilationConfig, GridGeometry, Ys=)"},

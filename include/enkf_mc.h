@@ -117,7 +117,7 @@ int enkfmc_analysis_device(enkfmc_plan *plan, const double *d_X, const double *d
 /* ---- host-buffer entry point (what assimilate_parallel binds; driver.py:159-253) -- */
 
 /* Copies X, r_diag, Ys to the device, runs the analysis, copies Xa back.  The fields (independent
- * 2-D problems) are processed in up to four groups: a copy stream uploads group g+1 and downloads the
+ * 2-D problems) are processed in up to five groups: a copy stream uploads group g+1 and downloads the
  * analysis of group g-1 under the kernels of group g (pinned host buffers make the copies asynchronous;
  * ENKFMC_HOST_GROUPS overrides the group count).  timings_ms[4] (may be NULL) receives the busy time of
  * h2d, estimation (K0+K2), analysis (K3), d2h from CUDA events, summed over the groups.

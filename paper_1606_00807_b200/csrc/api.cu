@@ -478,27 +478,47 @@ extern "C" int enkfmc_analysis_host(enkfmc_plan *p, const double *X, const doubl
     // Pipelined over groups of fields: the copy stream uploads group g + 1 and downloads the analysis of group
     // g - 1 while the compute stream works on group g (fields are independent: PAPER.md:201).
     cudaStream_t s = d->stream, cs = d->copy_stream;
-    int ngroups = (int)std::min<int64_t>(p->nfields, 4);
-    if (const char *genv = getenv("ENKFMC_HOST_GROUPS")) ngroups = (int)std::max<int64_t>(1, std::min<int64_t>(p->nfields, atoi(genv)));
-    const size_t need_ev = 2 + 7 * (size_t)ngroups;
+    // Five groups for a dozen fields or more, the first and the last small (the kernels start after a short upload and
+    // only a short download is exposed; smaller groups than this cost more in kernel tails than they hide).
+    std::vector<int64_t> cuts;
+    {
+        const int64_t nf = p->nfields;
+        int64_t ng = nf >= 12 ? 5 : std::min<int64_t>(nf, 4);
+        if (const char *genv = getenv("ENKFMC_HOST_GROUPS")) ng = std::max<int64_t>(1, std::min<int64_t>(nf, atoi(genv)));
+        const int64_t edge = ng >= 3 ? std::max<int64_t>(1, nf / (4 * ng)) : 0;   // fields in the edge groups
+        for (int64_t g = 0; g <= ng; ++g) {
+            if (ng < 3) cuts.push_back(nf * g / ng);
+            else if (g == 0) cuts.push_back(0);
+            else if (g == ng) cuts.push_back(nf);
+            else cuts.push_back(edge + (nf - 2 * edge) * (g - 1) / (ng - 2));
+        }
+    }
+    const int ngroups = (int)cuts.size() - 1;
+    // observations are sorted by state index, hence by field: the rows of Ys / r_diag each group needs are contiguous
+    std::vector<int64_t> ocut((size_t)ngroups + 1, 0);
+    for (int g = 0; g <= ngroups; ++g)
+        ocut[(size_t)g] = std::lower_bound(p->obs_indices.begin(), p->obs_indices.end(), cuts[(size_t)g] * p->nstate2d) -
+                          p->obs_indices.begin();
+    const size_t need_ev = 2 + 8 * (size_t)ngroups;
     while (d->hev.size() < need_ev) { cudaEvent_t e; CK(cudaEventCreate(&e)); d->hev.push_back(e); }
     cudaEvent_t evY0 = d->hev[0], evY1 = d->hev[1];
-    auto EV = [&](int g, int k) { return d->hev[2 + 7 * (size_t)g + k]; };   // 0,1 H2D; 2,3,4 compute; 5,6 D2H
+    auto EV = [&](int g, int k) { return d->hev[2 + 8 * (size_t)g + k]; };   // 0,1 X up; 7 Ys up; 2,3,4 compute; 5,6 down
     const size_t rowbytes = (size_t)nens * sizeof(double);
-    auto fcut = [&](int g) { return p->nfields * g / ngroups; };
+    auto fcut = [&](int g) { return cuts[(size_t)g]; };
     for (int g = 0; g < ngroups; ++g) {
         const size_t r0 = (size_t)fcut(g) * p->nstate2d, r1 = (size_t)fcut(g + 1) * p->nstate2d;
         CK(cudaEventRecord(EV(g, 0), cs));
         CK(cudaMemcpyAsync(d->dX + r0 * nens, X + r0 * nens, (r1 - r0) * rowbytes, cudaMemcpyHostToDevice, cs));
         CK(cudaEventRecord(EV(g, 1), cs));
-        if (g == 0) {
+        if (g == 0) {   // r_diag is small and usually in pageable memory (a staged, host-blocking copy): once, up front
             CK(cudaEventRecord(evY0, cs));
-            if (p->nobs) {
-                CK(cudaMemcpyAsync(d->dR, r_diag, (size_t)p->nobs * sizeof(double), cudaMemcpyHostToDevice, cs));
-                CK(cudaMemcpyAsync(d->dYs, Ys, (size_t)p->nobs * nens * sizeof(double), cudaMemcpyHostToDevice, cs));
-            }
-            CK(cudaEventRecord(evY1, cs));
+            if (p->nobs) CK(cudaMemcpyAsync(d->dR, r_diag, (size_t)p->nobs * sizeof(double), cudaMemcpyHostToDevice, cs));
         }
+        const int64_t o0 = ocut[(size_t)g], o1 = ocut[(size_t)g + 1];
+        if (o1 > o0)
+            CK(cudaMemcpyAsync(d->dYs + o0 * nens, Ys + o0 * nens, (size_t)(o1 - o0) * rowbytes, cudaMemcpyHostToDevice, cs));
+        CK(cudaEventRecord(EV(g, 7), cs));
+        if (g == ngroups - 1) CK(cudaEventRecord(evY1, cs));
     }
     for (int g = 0; g < ngroups; ++g) {
         const int64_t f0 = fcut(g), f1 = fcut(g + 1);
@@ -509,7 +529,7 @@ extern "C" int enkfmc_analysis_host(enkfmc_plan *p, const double *X, const doubl
         p->counters[0] += 1;
         if ((rc = do_regress(p, d->U, nens, rank_tol, floor_, d->T, d->D, d->flags, s, nullptr, f0, f1))) return rc;
         CK(cudaEventRecord(EV(g, 3), s));
-        if (g == 0) CK(cudaStreamWaitEvent(s, evY1, 0));
+        CK(cudaStreamWaitEvent(s, EV(g, 7), 0));
         if ((rc = do_solve(p, d->dX, d->T, d->D, d->dR, d->dYs, nens, d->dXa, d->status, s, f0, f1))) return rc;
         CK(cudaEventRecord(EV(g, 4), s));
         CK(cudaStreamWaitEvent(cs, EV(g, 4), 0));
@@ -527,9 +547,9 @@ extern "C" int enkfmc_analysis_host(enkfmc_plan *p, const double *X, const doubl
             return e;
         };
         timings_ms[0] = timings_ms[1] = timings_ms[2] = timings_ms[3] = 0.0;
-        CK(span(evY0, evY1, timings_ms[0]));
+        (void)evY0; (void)evY1;
         for (int g = 0; g < ngroups; ++g) {
-            CK(span(EV(g, 0), EV(g, 1), timings_ms[0]));
+            CK(span(EV(g, 0), EV(g, 7), timings_ms[0]));
             CK(span(EV(g, 2), EV(g, 3), timings_ms[1]));
             CK(span(EV(g, 3), EV(g, 4), timings_ms[2]));
             CK(span(EV(g, 5), EV(g, 6), timings_ms[3]));
