@@ -147,10 +147,13 @@ def run_reference(args, rank, world):
 
 
 def workload_config(name, w, full_fields):
-    return {"workload": name, "grid": f"{w.ny}x{w.nx}", "fields": full_fields if full_fields else w.nfields,
-            "nstate": w.n2d * (full_fields if full_fields else w.nfields), "nens": w.nens, "zeta": w.zeta,
-            "delta": w.delta, "boundary": w.boundary, "nugget": w.nugget, "nobs": int(w.obs_indices.size),
-            "cache": "inputs larger than L2 (ensemble + T factors >> 126 MB)" if w.X.nbytes > 2.5e8 else
+    """Both arms report the full workload; the CPU arm builds one of its fields only (full_fields set)."""
+    nf = full_fields if full_fields else w.nfields
+    nbytes = w.X.nbytes * nf // w.nfields
+    return {"workload": name, "grid": f"{w.ny}x{w.nx}", "fields": nf, "nstate": w.n2d * nf, "nens": w.nens, "zeta": w.zeta,
+            "delta": w.delta, "boundary": w.boundary, "nugget": w.nugget,
+            "nobs": int(w.obs_indices.size) * nf // w.nfields,
+            "cache": "inputs larger than L2 (ensemble + T factors >> 126 MB)" if nbytes > 2.5e8 else
                      "L2 flushed between steps (256 MB write)"}
 
 
