@@ -922,6 +922,22 @@ __global__ void __launch_bounds__(256, 1) regress_qr_mma_kernel(const RegressPar
         double *out = P.Rq + (int64_t)fl * P.rq_stride + P.rq_ptr[q];
         double *yout = out + packed_col_offset(p, K);
 
+        // column block starting at column o0, in fragment layout (zeros beyond N rows / ncols columns)
+        auto load_block = [&](int o0, auto &dst) {
+            const int jc = o0 + g8;
+            const double *src = jc < p ? Uf + (int64_t)pred[jc < p ? jc : 0] * N : yrow;
+#pragma unroll
+            for (int mt = 0; mt < NT; ++mt) {
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int row = 8 * mt + 4 * u + t4;
+                    dst[mt][u] = (jc < ncols && row < N) ? src[row] : 0.0;
+                }
+            }
+        };
+        constexpr bool PREFETCH = NT <= 10;            // 16 m-tiles: the second block would spill
+        double cn[PREFETCH ? NT : 1][2];
+        if constexpr (PREFETCH) load_block(0, cn);
         for (int o = 0; o < ncols; o += 8) {
             const int m0 = o >> 3;                       // m-tile holding the diagonal rows of this block
             const bool stored = o + 8 < ncols;           // a later block will need these reflectors
@@ -930,16 +946,12 @@ __global__ void __launch_bounds__(256, 1) regress_qr_mma_kernel(const RegressPar
             double *dst = out + packed_col_offset(j_own < p ? j_own : p, K);
             const int h = j_own < p ? (j_own + 1 < K ? j_own + 1 : K) : 0;    // R entries of my column (0: y or padding)
             double c[NT][2];
-            {
-                const double *src = j_own < p ? Uf + (int64_t)pred[j_own < p ? j_own : 0] * N : yrow;
+            if constexpr (PREFETCH) {
 #pragma unroll
-                for (int mt = 0; mt < NT; ++mt) {
-#pragma unroll
-                    for (int u = 0; u < 2; ++u) {
-                        const int row = 8 * mt + 4 * u + t4;
-                        c[mt][u] = (j_own < ncols && row < N) ? src[row] : 0.0;
-                    }
-                }
+                for (int mt = 0; mt < NT; ++mt) { c[mt][0] = cn[mt][0]; c[mt][1] = cn[mt][1]; }
+                if (o + 8 < ncols) load_block(o + 8, cn);  // the next block's columns: in flight during this block's work
+            } else {
+                load_block(o, c);
             }
             // ---- earlier reflector blocks: C <- C - V T^T (V^T C) ----
             for (int ob = 0; ob < o && ob < K; ob += 8) {
