@@ -2247,7 +2247,9 @@ cudaError_t launch_assemble_band(const SolveParams &p, int sm_count, size_t smem
     const int64_t total = p.nrows_owned * (p.f1 - p.f0);
     if (total == 0) return cudaSuccess;
     const size_t tile_smem = asm_tile_smem_bytes(p.asm_nmax, p.asm_nnzmax, p.bmax);
-    if (p.asm_nmax > 0 && p.asm_nmax < 65536 && p.asm_nnzmax < 65536 && tile_smem <= smem_limit) {
+    // (ENKFMC_K3A=rows forces the warp-per-row form that large tiles fall back to: tests compare the two)
+    const char *k3a_sel = getenv("ENKFMC_K3A");
+    if (p.asm_nmax > 0 && p.asm_nmax < 65536 && p.asm_nnzmax < 65536 && tile_smem <= smem_limit && !(k3a_sel && k3a_sel[0] == 'r')) {
         cudaError_t e = cudaFuncSetAttribute(assemble_band_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)tile_smem);
         if (e != cudaSuccess) return e;

@@ -143,6 +143,30 @@ def test_dense_precision_and_apply(mck):
     assert np.allclose(f.precision_apply(v[:, 0]), dense @ v[:, 0], rtol=1e-12, atol=1e-12)
 
 
+def test_assembly_forms_agree(mck, monkeypatch):
+    """K3a has a tile-cooperative form (tile staged in shared memory) and a warp-per-row form for tiles that do
+    not fit: the same band to rounding, and the same analysis through either."""
+    import scipy.sparse as sp
+    from paper_1606_00807_b200 import synthetic
+    rng = np.random.default_rng(11)
+    n = 120
+    low = np.tril(rng.standard_normal((n, n)), -1) * (rng.random((n, n)) < 0.2)
+    f = mck.PrecisionFactors(sp.csr_matrix(low), rng.random(n) + 0.5)
+    monkeypatch.delenv("ENKFMC_K3A", raising=False)
+    a_tile = f.dense_precision()
+    monkeypatch.setenv("ENKFMC_K3A", "rows")
+    a_rows = f.dense_precision()
+    assert np.allclose(a_tile, a_rows, rtol=1e-14, atol=1e-14)
+    w = synthetic.config("cfg2", nugget=0.01)
+    geo = mck.GridGeometry("grid2d", w.nx, w.ny)
+    net = mck.ObservationNetwork(w.obs_indices, w.r_diag, w.y)
+    cfg = mck.AssimilationConfig(zeta=w.zeta, delta=w.delta)
+    x_rows, _ = mck.assimilate_parallel(mck.EnsembleState(w.X), net, cfg, geo, Ys=w.Ys)
+    monkeypatch.delenv("ENKFMC_K3A", raising=False)
+    x_tile, _ = mck.assimilate_parallel(mck.EnsembleState(w.X), net, cfg, geo, Ys=w.Ys)
+    assert relerr(x_rows.X, x_tile.X) < 1e-11
+
+
 def test_analysis_edge_cases(mck):
     import scipy.sparse as sp
     rng = np.random.default_rng(9)
