@@ -35,7 +35,7 @@ struct DeviceState {
     int64_t rq_stride = 0;
     double *Rq = nullptr;
     int64_t rq_alloc = 0;           // doubles the QR scratch holds
-    uint8_t *is_interior = nullptr;
+    uint8_t *is_interior = nullptr, *tile_mono = nullptr;
     int32_t *obs_slot = nullptr, *tile_nobs = nullptr;
     bool obs_current = false, orders_current = false;
     std::vector<cudaEvent_t> prof;   // 4 events per profiled analysis_device call
@@ -104,6 +104,7 @@ int ensure_device(enkfmc_plan *p) {
     if ((rc = upload(d->state_row, p->state_row))) return rc;
     if ((rc = upload(d->pred_state, p->pred_state))) return rc;
     if ((rc = upload(d->is_interior, p->is_interior))) return rc;
+    if ((rc = upload(d->tile_mono, p->tile_mono))) return rc;
     if ((rc = upload(d->row_tile, p->row_tile))) return rc;
     {   // row-form band of every tile: [8 ceil(n/8)][8 (Wb + 1)], Wb = floor((b + 7) / 8)
         std::vector<int64_t> bp(p->ntiles + 1, 0);
@@ -267,7 +268,7 @@ int do_solve(enkfmc_plan *p, const double *d_X, const double *d_T, const double 
     S.tile_ptr = d->tile_ptr; S.row_ptr = d->row_ptr; S.csc_ptr = d->csc_ptr; S.csc_src = d->csc_src;
     S.col_idx = d->col_idx; S.csc_row = d->csc_row; S.phys = d->phys; S.iphys = d->iphys; S.bw = d->bw;
     S.state_row = d->state_row; S.obs_slot = d->obs_slot; S.tile_nobs = d->tile_nobs; S.tile_order = d->tile_order;
-    S.is_interior = d->is_interior; S.scratch = d->scratch; S.status = d_status; S.counter = d->counters + 2;
+    S.is_interior = d->is_interior; S.tile_mono = d->tile_mono; S.scratch = d->scratch; S.status = d_status; S.counter = d->counters + 2;
     S.band_ptr = d->band_ptr; S.band_stride = d->band_stride; S.row_tile = d->row_tile; S.work_order = d->work_order;
     S.nrows_owned = (int64_t)p->work_order.size();
     S.asm_nmax = (int)p->max_nlocal;
@@ -303,7 +304,7 @@ void enkfmc_device_release(enkfmc_plan *p) {
     if (!d) return;
     release(d->tile_ptr); release(d->row_ptr); release(d->csc_ptr); release(d->csc_src); release(d->col_idx);
     release(d->csc_row); release(d->phys); release(d->iphys); release(d->bw); release(d->state_row);
-    release(d->pred_state); release(d->regress_order); release(d->alias_row); release(d->alias_rep); release(d->work_order); release(d->tile_order); release(d->is_interior);
+    release(d->pred_state); release(d->regress_order); release(d->alias_row); release(d->alias_rep); release(d->work_order); release(d->tile_order); release(d->is_interior); release(d->tile_mono);
     release(d->obs_slot); release(d->tile_nobs); release(d->U); release(d->T); release(d->D); release(d->scratch);
     release(d->flags); release(d->status); release(d->counters); release(d->rq_ptr); release(d->Rq); release(d->band_ptr); release(d->band); release(d->row_tile); release(d->dX); release(d->dXa); release(d->dR);
     release(d->dYs);
@@ -619,7 +620,7 @@ extern "C" int enkfmc_assemble_band(enkfmc_plan *p, const double *d_T, const dou
     S.band_ptr = d->band_ptr; S.band_stride = d->band_stride; S.row_tile = d->row_tile; S.work_order = d->work_order;
     S.nrows_owned = (int64_t)p->work_order.size();
     S.assemble_only = 1; S.f0 = 0; S.f1 = 1; S.band = d_band;
-    S.tile_order = d->tile_order; S.asm_nmax = (int)p->max_nlocal; S.asm_nnzmax = (int)std::min<int64_t>(p->nnz(), 1 << 30);
+    S.tile_order = d->tile_order; S.tile_mono = d->tile_mono; S.asm_nmax = (int)p->max_nlocal; S.asm_nnzmax = (int)std::min<int64_t>(p->nnz(), 1 << 30);
     CK(launch_assemble_band(S, d->sm_count, d->smem_limit, (cudaStream_t)stream));
     p->counters[0] += 1;
     return ENKFMC_OK;

@@ -1752,6 +1752,7 @@ __global__ void __launch_bounds__(ASMT_THREADS) assemble_band_tile_kernel(const 
     for (int e = tid; e < nz; e += ASMT_THREADS) { sT[e] = Tf[e]; sK[e] = (uint16_t)phys[P.col_idx[e0 + e]]; }
     __syncthreads();
 
+    const bool mono = P.tile_mono != nullptr && P.tile_mono[t] != 0;
     double *acc = accs + (size_t)warp * accw;
     for (int i = warp; i < n; i += ASMT_THREADS / 32) {
         const int I = sPhys[i];
@@ -1773,8 +1774,12 @@ __global__ void __launch_bounds__(ASMT_THREADS) assemble_band_tile_kernel(const 
                 else { j = __shfl_sync(FULL, jl, ee); tji = sT[__shfl_sync(FULL, sl, ee)]; }
                 const double sc = tji * sD[j];
                 const int q0 = sRow[j];
-                const int cnt = sRow[j + 1] - q0;
-                for (int m = lane - 1; m < cnt; m += 32) {
+                int cnt = sRow[j + 1] - q0, mfirst = lane - 1;
+                if (mono && eb >= 0) {              // sorted columns: nothing right of the pivot entry (column i) is wanted
+                    cnt = __shfl_sync(FULL, sl, ee) - q0 + 1;
+                    mfirst = lane;                  // nor is the diagonal of a later row
+                }
+                for (int m = mfirst; m < cnt; m += 32) {
                     int Kp; double tjk;
                     if (m < 0) { Kp = sPhys[j]; tjk = 1.0; } else { Kp = sK[q0 + m]; tjk = sT[q0 + m]; }
                     if (Kp <= I) acc[Kp - col0] += sc * tjk;

@@ -36,6 +36,7 @@ struct SolveParams {
     const int64_t *tile_ptr, *row_ptr, *csc_ptr, *csc_src;
     const int32_t *col_idx, *csc_row, *phys, *iphys, *bw, *state_row, *obs_slot, *tile_nobs, *tile_order;
     const uint8_t *is_interior;
+    const uint8_t *tile_mono;  // per tile: physical order == local order (may be null)
     double *scratch;           // per-CTA scratch
     int64_t scratch_stride;    // doubles per CTA
     int64_t off_z, off_win_a, off_win_r;  // offsets (doubles) inside a CTA's scratch

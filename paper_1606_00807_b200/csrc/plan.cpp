@@ -181,6 +181,13 @@ void finish_plan(enkfmc_plan &p) {
         const int64_t base = p.tile_ptr[t];
         for (int64_t j = 0; j < p.tile_ptr[t + 1] - base; ++j) p.iphys[base + p.phys[base + j]] = (int32_t)j;
     }
+    // tiles whose physical order is the local order (every clipped tile): K3a can stop a row's scan at the pivot entry
+    p.tile_mono.assign((size_t)p.ntiles, 1);
+    for (int64_t t = 0; t < p.ntiles; ++t) {
+        const int64_t base = p.tile_ptr[t];
+        for (int64_t j = 0; j < p.tile_ptr[t + 1] - base; ++j)
+            if (p.phys[base + j] != (int32_t)j) { p.tile_mono[(size_t)t] = 0; break; }
+    }
     // predecessor state rows, max predecessor count, half-bandwidth in physical order
     p.pred_state.resize(p.nnz());
     p.bw.assign(p.ntiles, 0);

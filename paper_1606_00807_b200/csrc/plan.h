@@ -27,6 +27,7 @@ struct enkfmc_plan {
     std::vector<int32_t> phys, iphys;   // physical (band) order inside the tile and its inverse
     std::vector<int32_t> bw;            // per tile: half-bandwidth of A in physical order
     std::vector<uint8_t> is_interior;   // per local row
+    std::vector<uint8_t> tile_mono;     // per tile: physical order == local order
     std::vector<int64_t> csc_ptr;       // per local row + 1: column lists of T (global offsets)
     std::vector<int32_t> csc_row;       // local row j holding the entry
     std::vector<int64_t> csc_src;       // offset of the entry in the CSR value array
