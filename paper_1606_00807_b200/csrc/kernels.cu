@@ -1801,7 +1801,23 @@ __global__ void __launch_bounds__(ASMT_THREADS) assemble_band_tile_kernel(const 
 __host__ __device__ inline size_t solve_strip_doubles(int Wb) { return (((4 * (size_t)Wb * (Wb + 1) * 2 + 7) / 8 + 1) & ~(size_t)1); }
 __host__ __device__ inline size_t solve_rowsrc_doubles(int rows) { return ((3 * (size_t)rows * 4 + 15) / 16) * 2; }
 
+#ifdef ENKFMC_K3B_TIMING
+__device__ unsigned long long g_k3b_t[16];
+#define K3T(i) do { if (blockIdx.x == 0 && threadIdx.x == 0) { const long long now_ = clock64(); atomicAdd(&g_k3b_t[i], (unsigned long long)(now_ - tmark_)); tmark_ = now_; } } while (0)
+extern "C" int enkfmc_debug_k3b_times(unsigned long long *out16) {
+    cudaMemcpyFromSymbol(out16, g_k3b_t, sizeof(g_k3b_t));
+    unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(g_k3b_t, z, sizeof(z));
+    return 0;
+}
+#else
+#define K3T(i) do { } while (0)
+#endif
+
 __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveParams P) {
+#ifdef ENKFMC_K3B_TIMING
+    long long tmark_ = clock64();
+#endif
     extern __shared__ double smem[];
     __shared__ unsigned int s_item;
     __shared__ int s_fail;
@@ -1836,6 +1852,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
         __syncthreads();
         const unsigned int item = s_item;
         if ((int)item >= total_items) break;
+        K3T(0);
         const int t = P.tile_order[item / nf];
         const int fl = (int)(item % nf), f = P.f0 + fl;
         const int64_t base = P.tile_ptr[t];
@@ -1941,8 +1958,10 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
                 Rw[(size_t)(rs + rr) * NR + m] = rhs_value(8 * R + rr, m);
             }
         };
+        K3T(1);
         for (int R = 0; R <= Wb && R < nb; ++R) load_block_row(R);
         __syncthreads();
+        K3T(2);
 
         // ---- forward: blocked Cholesky + forward substitution --------------------------------
         // Everything but the 8x8 diagonal factorisation runs as 8x8 tiles on the FP64 tensor cores (mma.m8n8k4, two
@@ -2004,6 +2023,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
         };
         if (warp == 0) factor_diag(0, 0);
         __syncthreads();
+        K3T(3);
         int sJ = 0;                                    // window slot of block row J
         for (int J = 0; J < nb; ++J) {
             if (s_fail) break;
@@ -2038,6 +2058,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
                 }
             }
             __syncthreads();
+            K3T(4);
             // (e) the next block row goes into the slot of block row J (retired by the barrier above): the
             // global loads are issued here and land behind the updates below
             const bool more = J + Wb + 1 < nb;
@@ -2065,18 +2086,26 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
                     mma_f64(c.x, c.y, -a1, b1);
                     *cp = c;
                 };
+                // The FP64 pipe of a sub-partition serves DFMA and DMMA alike: the serial factorisation of warp 0 would
+                // queue behind the tile products of the warps sharing its sub-partition (warps 4, 8, 12), so those sit
+                // this phase out when the next block has to be factored; the other twelve share the tiles.
+                const bool spare = (J + 1 < nb) && nwarps >= 8;
+                const int nwork = spare ? nwarps - (nwarps >> 2) : nwarps - 1;
+                const int widx = spare ? ((warp & 3) ? warp - 1 - (warp >> 2) : -1) : warp - 1;
                 if (warp == 0) {
+                    K3T(12);
                     if (nbl > 0) c_tile(0, 0);
+                    K3T(13);
                     if (J + 1 < nb) { __syncwarp(); factor_diag(s1, (J + 1) & 1); }
-                } else {
-                    for (int u = warp; u < nC; u += nwarps - 1) {
+                    K3T(14);
+                } else if (widx >= 0) {
+                    for (int u = 1 + widx; u < nC; u += nwork) {
                         const int rc = strips[u];
                         c_tile(rc >> 8, rc & 255);
                     }
                     // (d): units (rb, ct), rb-major, continuing the round-robin where (c) stopped
-                    int u = warp - 1 - (nC - 1) % (nwarps - 1);
-                    if (nC == 0) u = warp - 1;
-                    if (u < 0) u += nwarps - 1;
+                    int u = nC > 0 ? widx - (nC - 1) % nwork : widx;
+                    if (u < 0) u += nwork;
                     int rb = 0, ct = u;
                     while (ct >= nct) { ct -= nct; ++rb; }
                     while (rb < nbl) {
@@ -2088,13 +2117,16 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
                         mma_f64(c.x, c.y, -a0, Zb[(size_t)t4 * NR + 8 * ct + g8]);
                         mma_f64(c.x, c.y, -a1, Zb[(size_t)(4 + t4) * NR + 8 * ct + g8]);
                         *cp = c;
-                        ct += nwarps - 1;
+                        ct += nwork;
                         while (ct >= nct) { ct -= nct; ++rb; }
                     }
                 }
             }
+            K3T(5);
             if (more) { if (pf) commit_block_row(sJ, s1); else load_block_row(J + Wb + 1); }
+            K3T(6);
             __syncthreads();
+            K3T(7);
             sJ = s1;
         }
         if (s_fail) {
@@ -2138,6 +2170,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
         };
         load_panel(nb - 1, Lp0, rinv0);
         __syncthreads();
+        K3T(8);
         int sB = ((nb - 1) % nslot) * 8;                // window slot of block row J
         for (int J = nb - 1; J >= 0; --J) {
             const int cur = (nb - 1 - J) & 1;
@@ -2151,6 +2184,19 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
             if (warp < nct) {
                 const int col = 8 * warp + g8;
                 if (col < N) { zf0 = Z[(int64_t)(8 * J + t4) * N + col]; zf1 = Z[(int64_t)(8 * J + 4 + t4) * N + col]; }
+            }
+            // the background values of the interior rows this lane will write (first tile), likewise
+            int xi0 = -1;
+            double xb0 = 0.0, xb1 = 0.0;
+            if (warp < nct) {
+                const int i = 8 * J + g8;
+                if (rows_cached) xi0 = rxi[i];
+                else if (i < n) { const int il = iphys[i]; if (inter[il]) xi0 = srow[il]; }
+                const int col = 8 * warp + 2 * t4;
+                if (xi0 >= 0) {
+                    if (col < N) xb0 = Xf[(int64_t)xi0 * N + col];
+                    if (col + 1 < N) xb1 = Xf[(int64_t)xi0 * N + col + 1];
+                }
             }
             if (J > 0 && pfb) fetch_panel(J - 1);
             const double lt0 = linv(Lc, rinvc, t4, g8), lt1 = linv(Lc, rinvc, 4 + t4, g8);   // (L_JJ^-T)[g8][k]
@@ -2179,19 +2225,22 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
                 const int col = 8 * ct + 2 * t4;
                 if (col < N && (!(fabs(x0) < DBL_MAX) || (col + 1 < N && !(fabs(x1) < DBL_MAX)))) s_fail = 2;   // benign race
                 *reinterpret_cast<double2 *>(Rw + (size_t)(sB + g8) * NR + col) = make_double2(x0, x1);
-                const int i = 8 * J + g8;
-                int xi = -1;
-                if (rows_cached) xi = rxi[i];
-                else if (i < n) { const int il = iphys[i]; if (inter[il]) xi = srow[il]; }
-                if (xi >= 0) {
-                    const int64_t gidx = (int64_t)xi * N + col;
-                    if (col < N) Xaf[gidx] = Xf[gidx] + x0;
-                    if (col + 1 < N) Xaf[gidx + 1] = Xf[gidx + 1] + x1;
+                if (xi0 >= 0) {
+                    const int64_t gidx = (int64_t)xi0 * N + col;
+                    if (ct != warp) {
+                        if (col < N) xb0 = Xf[gidx];
+                        if (col + 1 < N) xb1 = Xf[gidx + 1];
+                    }
+                    if (col < N) Xaf[gidx] = xb0 + x0;
+                    if (col + 1 < N) Xaf[gidx + 1] = xb1 + x1;
                 }
                 __syncwarp();
             }
+            K3T(9);
             if (J > 0) { if (pfb) commit_panel(J - 1, Ln, rinv0 + 8 * (cur ^ 1)); else load_panel(J - 1, Ln, rinv0 + 8 * (cur ^ 1)); }
+            K3T(10);
             __syncthreads();
+            K3T(11);
             sB = sB == 0 ? Wr - 8 : sB - 8;
         }
         if (tid == 0) P.status[(int64_t)f * P.ntiles + t] = s_fail;
