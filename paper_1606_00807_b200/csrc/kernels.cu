@@ -1569,6 +1569,9 @@ cudaError_t launch_regress(const RegressParams &p_in, int sm_count, size_t smem_
             case 2: e = launch_qr_t<2>(p, (int)grid, warps, ws * warps, s); break;
             case 3: e = launch_qr_t<3>(p, (int)grid, warps, ws * warps, s); break;
             case 4: e = launch_qr_t<4>(p, (int)grid, warps, ws * warps, s); break;
+            case 5: e = launch_qr_t<5>(p, (int)grid, warps, ws * warps, s); break;   // the row guards assume S = ceil(N / 32) exactly
+            case 6: e = launch_qr_t<6>(p, (int)grid, warps, ws * warps, s); break;
+            case 7: e = launch_qr_t<7>(p, (int)grid, warps, ws * warps, s); break;
             default: e = launch_qr_t<8>(p, (int)grid, warps, ws * warps, s); break;
         }
         if (e != cudaSuccess) return e;

@@ -264,7 +264,8 @@ def test_regression_forms_agree(mck, monkeypatch):
     for more predecessors than members."""
     from oracle import enkf_mc_oracle as orc
     rng = np.random.default_rng(7)
-    for nx, ny, nens, zeta, nug in ((20, 14, 30, 3, 0.3), (16, 12, 9, 2, 0.5), (24, 10, 80, 4, 0.2), (12, 9, 100, 1, 0.4)):
+    for nx, ny, nens, zeta, nug in ((20, 14, 30, 3, 0.3), (16, 12, 9, 2, 0.5), (24, 10, 80, 4, 0.2), (12, 9, 100, 1, 0.4),
+                                   (14, 9, 128, 5, 0.3), (10, 8, 160, 2, 0.3), (9, 7, 250, 2, 0.3)):   # 128: largest tensor-core case; beyond: SIMT form only
         geo = mck.GridGeometry("grid2d", nx, ny)
         n = nx * ny
         base = rng.standard_normal((n, nens)).cumsum(axis=0) * 0.1 + nug * rng.standard_normal((n, nens))
@@ -278,3 +279,22 @@ def test_regression_forms_agree(mck, monkeypatch):
         assert np.max(np.abs(f1.variances - f2.variances) / f2.variances) < 1e-10
         ref = orc.fit_factors(U, orc.Grid(nx, ny, True, False), zeta)
         assert relerr(f1.lower.data, ref.data) < 1e-9 and np.max(np.abs(f1.variances - ref.d) / ref.d) < 1e-9
+
+
+@pytest.mark.parametrize("nens", [136, 200, 256])
+def test_large_ensembles_take_the_general_paths(mck, nens):
+    """More than 128 members: K2a in its SIMT form, K3b without register prefetch (and, for the largest, with its
+    right-hand-side window outside shared memory) -- same answers as the oracle."""
+    from oracle import enkf_mc_oracle as orc
+    rng = np.random.default_rng(nens)
+    nx, ny, zeta, delta = 24, 16, 2, 4
+    n = nx * ny
+    X = rng.standard_normal((n, nens)).cumsum(axis=0) * 0.05 + 0.5 * rng.standard_normal((n, nens)) + 3.0
+    obs = np.sort(rng.choice(n, n // 3, replace=False))
+    r = np.full(obs.size, 0.04)
+    Ys = X[obs].mean(axis=1, keepdims=True) + 0.3 * rng.standard_normal((obs.size, nens))
+    geo = mck.GridGeometry("grid2d", nx, ny)
+    xa, _ = mck.assimilate_parallel(mck.EnsembleState(X), mck.ObservationNetwork(obs, r, Ys.mean(axis=1)),
+                                    mck.AssimilationConfig(zeta=zeta, delta=delta), geo, Ys=Ys)
+    ref = orc.assimilate(X, obs, r, Ys, orc.Grid(nx, ny, True, False), delta, zeta)
+    assert relerr(xa.X, ref) < 1e-9
