@@ -2035,6 +2035,10 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
             int s1 = sJ + 8; if (s1 >= Wr) s1 = 0;     // window row of panel row r is wrap(s1 + r)
             const int below = (nb - 1 - J < Wb ? nb - 1 - J : Wb) * 8;     // panel rows under the diagonal block
             const int nbl = below >> 3;
+            // (e) the next block row will go into the slot of block row J: its global loads are issued first thing, into
+            // registers, and committed at the end of the step
+            const bool more = J + Wb + 1 < nb;
+            if (more && pf) fetch_block_row(J + Wb + 1);
             // (b) panel X = A_panel L_JJ^-T (one 8-row block per unit) and right-hand sides Z_J = L_JJ^-1 B_J (one
             // 8-member tile per unit)
             {
@@ -2062,10 +2066,6 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
             }
             __syncthreads();
             K3T(4);
-            // (e) the next block row goes into the slot of block row J (retired by the barrier above): the
-            // global loads are issued here and land behind the updates below
-            const bool more = J + Wb + 1 < nb;
-            if (more && pf) fetch_block_row(J + Wb + 1);
             // L block -> global (overwrites the A rows of block J, already consumed)
             for (int e = tid; e < (8 + below) * 8; e += nthreads)
                 band[(int64_t)8 * J * Wr + e] = Lp[(e >> 3) * LP_PITCH + (e & 7)];
