@@ -1,11 +1,13 @@
 // sm_100a kernels of the EnKF-MC analysis step.  FP64 throughout (the reference has no
-// reduced precision anywhere).  The work is FP64-DFMA / shared-memory bound,
-// not GEMM-shaped for tcgen05 (which has no FP64 kind), so these are SIMT kernels sized
-// for 148 SMs with persistent CTAs that fetch work items from an atomic counter.
+// reduced precision anywhere).  tcgen05 has no FP64 kind; wherever the work forms
+// 8 x 8 blocks it runs on the FP64 tensor cores through mma.sync.m8n8k4.f64 (DMMA), the rest is
+// SIMT.  Persistent CTAs (one per SM) fetch work items from an atomic counter.
 //
-//   K0 center_rows_kernel   validation.py:35-39
-//   K2 regress_kernel       estimator.py:46-61,133-150 + factors.py:60
-//   K3 local_solve_kernel   factors.py:136-145, kernels.py:178-218, driver.py:99-125
+//   K0  center_rows_kernel                       validation.py:35-39
+//   K2a regress_qr_mma_kernel / regress_qr_kernel  estimator.py:46-61,133-150 (the QR half)
+//   K2b regress_solve_kernel                     estimator.py:46-61 (truncated-SVD semantics) + factors.py:60
+//   K3a assemble_band_tile_kernel / assemble_band_kernel   factors.py:136-145, kernels.py:189-191
+//   K3b local_solve_kernel                       kernels.py:178-218, driver.py:99-125
 //
 // All results are deterministic run to run: no floating-point atomics, fixed reduction
 // trees, work items are independent.
@@ -101,26 +103,31 @@ cudaError_t launch_center_rows(const double *X, double *U, int64_t nrows, int N,
 // K2: per-component regression (estimator.py:46-61,133-150 + factors.py:60), one warp per
 // regression, in two kernels so that each phase runs at its own occupancy.
 //
-// K2a regress_qr_kernel.  Workspace W (shared, column-major, odd pitch ld >= N): column j < p is
-//   predecessor j's anomaly vector, column p the target y.  Householder QR of W[:, 0:p] without
-//   pivoting (reflectors also applied to y, never stored): lanes own rows (S register slots),
-//   eight columns share two transposing warp reductions.  Output per regression, packed in
-//   global scratch: R by columns (min(j+1, K) entries of column j), c = (Q^T y)[0:K] and
-//   e2 = |(Q^T y)[K:N]|^2 -- the squared residual of the full least-squares fit.
+// K2a: Householder QR of [A^T | y] (N x (p + 1); column j < p is predecessor j's anomaly vector, the
+//   last column the target y) without pivoting.  Output per regression, packed in global scratch:
+//   R by columns (min(j+1, K) entries of column j), c = (Q^T y)[0:K] and e2 = |(Q^T y)[K:N]|^2 --
+//   the squared residual of the full least-squares fit.  Two forms: regress_qr_mma_kernel (N <= 128:
+//   column blocks in tensor-core fragment layout in registers, described at its definition) and
+//   regress_qr_kernel (any N <= 256: W in shared memory, column-major, odd pitch; lanes own rows
+//   in S = ceil(N / 32) register slots, two reflectors per sweep, eight columns share two
+//   transposing warp reductions).
 //
 // K2b regress_solve_kernel.  R (p x p) in shared memory, p-vectors in registers.
-//   s_max(R) is bracketed by a 3-step power iteration (lower bound) and |R|_F (upper bound);
-//   s_min(R) by inverse iteration (two triangular solves per step).  The inverse-iteration
-//   estimate bounds s_min from above, so "estimate < rank_tol * lower(s_max)" proves that the
-//   reference's truncation (estimator.py:55-57) is active; the converged pair (z, x = R z / s) is
-//   deflated and the probe repeats in the orthogonal complement until the next singular value is
-//   kept.  beta = (I - Z Z^T) R^-1 (I - X X^T) c is then exactly U S^+ V^T y of the reference's
-//   truncated SVD.  Anything the probes cannot settle (zero pivots, p > N, no gap, a singular
-//   value within 5 % of the threshold, more truncated values than the workspace holds) goes to
-//   the general fallback: one-sided Jacobi SVD on the rows of [R | c] with the same rule.
-//   T = -beta;  D = max((e2 + sum over truncated k of (x_k^T c)^2) / (N-1), floor): this is
-//   |y - A^T beta|^2 of estimator.py:60,148 evaluated in the QR basis (orthogonal invariance),
-//   so the predecessor rows are not read a second time.
+//   X = R^-1 by 8 x 8 blocks on the tensor cores gives sum 1/s_i^2 = |X|_F^2 (and, on demand,
+//   sum 1/s_i^4 = |X X^T|_F^2): a rigorous lower bound of the smallest singular value not yet
+//   deflated; when cancellation eats those sums the same bound comes from |X - (X U) U^T|_F
+//   (Eckart-Young).  If the bound does not clear rank_tol * |R|_F, inverse iteration from a
+//   pseudo-random start (two triangular solves per step; its estimate is an upper bound) proves
+//   that the reference's truncation (estimator.py:55-57) is active, converges the pair
+//   (z, u = R^-T z / |R^-T z|), deflates it and the bounds are re-evaluated; close sub-threshold
+//   values are sharpened together by a block (subspace) iteration with a Ritz / Cholesky test.
+//   beta = (I - Z Z^T) R^-1 (I - U U^T) c is then exactly the reference's truncated-SVD answer.
+//   Anything that cannot be settled (zero pivots, p > N, cond(R) beyond cond_max, no gap, a
+//   singular value within 0.1 % of the threshold, more truncated values than the workspace
+//   holds) goes to the general fallback: one-sided Jacobi SVD on the rows of [R | c] with the
+//   same rule.  T = -beta;  D = max((e2 + |c - R beta|^2) / (N-1), floor): |y - A^T beta|^2 of
+//   estimator.py:60,148 evaluated in the QR basis (orthogonal invariance), the second term only
+//   when something was truncated -- the predecessor rows are not read a second time.
 // ------------------------------------------------------------------------------------------
 #define REG_MAXDEFL_CAP 12
 #define JACOBI_MAX_SWEEPS 30
@@ -1645,18 +1652,21 @@ cudaError_t launch_replicate_rows(const int32_t *alias_row, const int32_t *alias
 // kernels.py:189-191) is symmetric and banded (half-bandwidth b) in the tile's physical order.
 // Rows are grouped in blocks of 8; Wb = floor((b+7)/8) block sub-diagonals can be non-zero.
 //
-// K3a assemble_band_kernel: one warp per row I of A (high occupancy; the index chasing is
-//   latency-bound).  A[I, K] = sum_j T~[j,i] T~[j,k] / D_j over the rows j holding both i and k,
-//   accumulated in ascending j in a per-warp shared buffer (deterministic), stored in row form:
+// K3a: A[I, K] = sum_j T~[j,i] T~[j,k] / D_j over the rows j holding both i and k, accumulated in
+//   ascending j in a per-warp shared buffer (deterministic), stored in row form:
 //   band[tile][I][e] = A[I, 8 (I/8 - Wb) + e], e < Wr = 8 (Wb + 1), zeros elsewhere.
+//   assemble_band_tile_kernel (one CTA per (field, tile), the tile's T staged in shared memory)
+//   whenever the tile fits, else assemble_band_kernel (one warp per row, from global memory).
 // K3b local_solve_kernel: one CTA per (field, tile).  Right-looking blocked banded Cholesky
 //   through a sliding window of Wb+1 block rows in shared memory, carrying the N right-hand sides
 //   rhs[obs] = (Ys - Xb[obs]) / r (kernels.py:182-186) along (forward substitution fused).
-//   Per block column: 8x8 diagonal factor, panel solve, then register-tiled rank-8 updates of the
-//   trailing window (1x8 strips) and of the right-hand sides (one member per thread).  L
-//   overwrites the band block by block.  The backward substitution runs blockwise the same way
-//   and writes Xa = Xb + dx for the interior rows straight into the global analysis
-//   (kernels.py:218, driver.py:116).
+//   Per block column: warp 0 factors and inverts the next 8 x 8 diagonal block in registers while
+//   the other warps run the trailing update and the right-hand-side update as 8 x 8 tensor-core
+//   tiles; panel and right-hand-side solves are tensor-core products with the stored inverse.
+//   L (with the inverse of each diagonal block in that block's upper triangle) overwrites the
+//   band block by block.  The backward substitution runs blockwise the same way and writes
+//   Xa = Xb + dx for the interior rows straight into the global analysis (kernels.py:218,
+//   driver.py:116).
 // ------------------------------------------------------------------------------------------
 #define SOLVE_THREADS 512
 #define ASM_WARPS 8
@@ -1829,7 +1839,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
     const int N = P.N;
     double *scr = P.scratch + (int64_t)blockIdx.x * P.scratch_stride;
     double *Z = scr + P.off_z;                 // [nbp][N] forward-substituted right-hand sides
-    // shared layout: Lp[2][WrMax][LP_PITCH] | Zb[8][N] | invd[2][8] | rinv[2][8] | strips | row sources | window A | window RHS
+    // shared layout: Lp[2][WrMax][LP_PITCH] | Zb[8][NR] | invd[2][8] | rinv[2][8] | tile table | row sources | window A | window RHS
     const int WbMax = solve_wb(P.bmax), WrMax = 8 * (WbMax + 1);
     const int NR = P.nr_pitch;                 // member pitch of Zb / the RHS window / red: >= 8 ceil(N/8), = 8 mod 16
     double *Lp0 = smem;
