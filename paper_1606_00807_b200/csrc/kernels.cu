@@ -717,6 +717,7 @@ __device__ __noinline__ int jacobi_solve(double *W, int ld, int K, int p, double
         }
     }
     if (sweep >= JACOBI_MAX_SWEEPS && rotated) flag |= 4;
+    flag |= sweep << 16;                               // sweeps used (diagnostics, flag bits 16-21)
     double smax = 0.0;
     for (int k = lane; k < K; k += 32) {
         const double *row = W + k;

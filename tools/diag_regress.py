@@ -46,5 +46,8 @@ steps = (flags >> 8) & 255
 tr = (flags & 2) > 0
 print("inverse-iteration steps per truncated row: mean %.2f, histogram" % steps[tr].mean(), np.bincount(steps[tr], minlength=12)[:16])
 print("pinned Cholesky pivots in the last analysis:", plan.counter(5))
+fb = (flags & 16) > 0
+if fb.any():
+    print("Jacobi sweeps per fallback row: mean %.1f, histogram" % ((flags[fb] >> 16) & 63).mean(), np.bincount((flags[fb] >> 16) & 63, minlength=31)[:31])
 fl = plan.work(w.nens)
 print("algorithmic GF regress/solve:", fl[2] / 1e9, fl[1] / 1e9, " -> TF/s", fl[2] / ((ms[1] + ms[2]) / n) / 1e9, fl[1] / (ms[3] / n) / 1e9)
