@@ -94,8 +94,13 @@ int enkfmc_center_rows(const double *d_X, double *d_U, int64_t nrows, int64_t ne
 /* K2: T values (-beta, in the plan's CSR order, per field) and floored D for every local
  * row of every tile: estimator.py:46-61,133-159 + factors.py:60.
  * d_U [nstate][nens] centred; d_T [nfields][nnz]; d_D [nfields][sum n_local];
- * d_flags [nfields][sum n_local] (may be NULL): bit0 = SVD path taken, bit1 = truncation
- * active, bit2 = Jacobi sweep cap hit. */
+ * d_flags [nfields][sum n_local] (may be NULL): bit0 = singular values were examined beyond the
+ * certificate (deflation or fallback), bit1 = truncation active, bit2 = Jacobi sweep cap hit,
+ * bit3 = D on the variance floor, bit4 = Jacobi-SVD fallback taken, bits 5-7 = why (1 zero pivot or
+ * p > N, 2 certificate inconclusive, 3 out of deflation slots, 4 refined value above the threshold,
+ * 5 cond(R) beyond the fast path's limit or certificate lost to cancellation, 6 block iteration not
+ * converged, 7 kept direction inside the block); diagnostics: bits 8-15 inverse-iteration steps,
+ * bits 16-21 Jacobi sweeps. */
 int enkfmc_regress(enkfmc_plan *plan, const double *d_U, int64_t nens, double rank_tol,
                    double variance_floor, double *d_T, double *d_D, int32_t *d_flags, void *stream);
 
