@@ -158,3 +158,22 @@ def test_pivot_clamp_counter_and_flags(mck, cfg3):
     assert 0.3 < truncated < 0.6           # every interior row of the smooth cfg3 ensemble has one value below 1e-8 s_max
     assert fallback < 0.01                 # the Jacobi SVD is the exception on this workload
     assert plan.counter(5) >= 0
+
+
+def test_host_path_equals_device_path(mck):
+    """The pipelined host entry point (field groups on a copy stream and a compute stream) must give bitwise the
+    analysis of the single-launch device entry point: fields are independent units of work."""
+    import torch
+    from paper_1606_00807_b200 import device, synthetic
+    from paper_1606_00807_b200.plan import get_plan
+    w = synthetic.config("cfg3", fields=13)
+    geo = mck.GridGeometry("grid2d", w.nx, w.ny, nfields=w.nfields)
+    plan = get_plan(geo, w.delta, w.zeta)
+    plan.set_observations(w.obs_indices)
+    dX, dR, dYs = device.to_device(w.X), device.to_device(w.r_diag), device.to_device(w.Ys)
+    dXa = torch.empty_like(dX)
+    device.analysis_device(plan, dX, dR, dYs, dXa)
+    torch.cuda.synchronize()
+    xa, _ = mck.assimilate_parallel(mck.EnsembleState(w.X), mck.ObservationNetwork(w.obs_indices, w.r_diag, w.y),
+                                    mck.AssimilationConfig(zeta=w.zeta, delta=w.delta), geo, Ys=w.Ys)
+    assert np.array_equal(xa.X, dXa.cpu().numpy())
