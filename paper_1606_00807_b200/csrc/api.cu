@@ -282,8 +282,8 @@ int do_solve(enkfmc_plan *p, const double *d_X, const double *d_T, const double 
     for (int64_t f0 = fbeg; f0 < fend; f0 += d->band_fields) {
         S.f0 = (int)f0;
         S.f1 = (int)std::min<int64_t>(fend, f0 + d->band_fields);
-        CK(launch_assemble_band(S, d->sm_count, d->smem_limit, s));
-        cudaError_t e = launch_local_solve(S, d->solve_grid, d->smem_limit, s);
+        cudaError_t e = launch_assemble_band(S, d->sm_count, d->smem_limit, s);
+        if (e == cudaSuccess) e = launch_local_solve(S, d->solve_grid, d->smem_limit, s);
         if (e == cudaErrorInvalidConfiguration) {
             enkfmc_set_error("local-solve window (half-bandwidth " + std::to_string(p->max_bw) + ") exceeds shared memory");
             return ENKFMC_E_CAPACITY;
@@ -621,7 +621,14 @@ extern "C" int enkfmc_assemble_band(enkfmc_plan *p, const double *d_T, const dou
     S.nrows_owned = (int64_t)p->work_order.size();
     S.assemble_only = 1; S.f0 = 0; S.f1 = 1; S.band = d_band;
     S.tile_order = d->tile_order; S.tile_mono = d->tile_mono; S.asm_nmax = (int)p->max_nlocal; S.asm_nnzmax = (int)std::min<int64_t>(p->nnz(), 1 << 30);
-    CK(launch_assemble_band(S, d->sm_count, d->smem_limit, (cudaStream_t)stream));
+    {
+        cudaError_t e = launch_assemble_band(S, d->sm_count, d->smem_limit, (cudaStream_t)stream);
+        if (e == cudaErrorInvalidConfiguration) {
+            enkfmc_set_error("band of half-bandwidth " + std::to_string(p->max_bw) + " exceeds shared memory");
+            return ENKFMC_E_CAPACITY;
+        }
+        CK(e);
+    }
     p->counters[0] += 1;
     return ENKFMC_OK;
 }

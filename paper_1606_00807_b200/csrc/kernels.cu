@@ -2317,7 +2317,8 @@ cudaError_t launch_assemble_band(const SolveParams &p, int sm_count, size_t smem
     const size_t tile_smem = asm_tile_smem_bytes(p.asm_nmax, p.asm_nnzmax, p.bmax);
     // (ENKFMC_K3A=rows forces the warp-per-row form that large tiles fall back to: tests compare the two)
     const char *k3a_sel = getenv("ENKFMC_K3A");
-    if (p.asm_nmax > 0 && p.asm_nmax < 65536 && p.asm_nnzmax < 65536 && tile_smem <= smem_limit && !(k3a_sel && k3a_sel[0] == 'r')) {
+    if (p.asm_nmax > 0 && p.asm_nmax < 65536 && p.asm_nnzmax < 65536 && tile_smem + 2048 <= smem_limit &&   // 1 KB is reserved per CTA
+        !(k3a_sel && k3a_sel[0] == 'r')) {
         cudaError_t e = cudaFuncSetAttribute(assemble_band_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)tile_smem);
         if (e != cudaSuccess) return e;
@@ -2327,6 +2328,7 @@ cudaError_t launch_assemble_band(const SolveParams &p, int sm_count, size_t smem
     int64_t grid = (total + ASM_WARPS - 1) / ASM_WARPS;
     if (grid > (int64_t)sm_count * 8) grid = (int64_t)sm_count * 8;
     const size_t smem = (size_t)ASM_WARPS * 8 * (solve_wb(p.bmax) + 1) * sizeof(double);
+    if (smem + 2048 > smem_limit) return cudaErrorInvalidConfiguration;     // band too wide for a shared-memory row
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(assemble_band_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;

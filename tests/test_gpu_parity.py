@@ -298,3 +298,37 @@ def test_large_ensembles_take_the_general_paths(mck, nens):
                                     mck.AssimilationConfig(zeta=zeta, delta=delta), geo, Ys=Ys)
     ref = orc.assimilate(X, obs, r, Ys, orc.Grid(nx, ny, True, False), delta, zeta)
     assert relerr(xa.X, ref) < 1e-9
+
+
+def test_wide_regressions_and_long_local_domains(mck):
+    """Paths the BASELINE tests leave alone: 84 predecessors (three register slots per p-vector in K2b), a local
+    domain of 5000 rows (no shared-memory row tables in K3b, the warp-per-row assembly), and the 96-predecessor cap."""
+    from oracle import enkf_mc_oracle as orc
+    rng = np.random.default_rng(21)
+    # zeta = 6 on a clipped grid: up to 84 predecessors, N = 100
+    nx, ny, nens, zeta = 26, 16, 100, 6
+    n = nx * ny
+    U = orc.center_rows(rng.standard_normal((n, nens)).cumsum(axis=0) * 0.1 + 0.4 * rng.standard_normal((n, nens)))
+    geo = mck.GridGeometry("grid2d", nx, ny)
+    f = mck.fit_factors(U, geo, zeta)
+    ref = orc.fit_factors(U, orc.Grid(nx, ny, True, False), zeta)
+    assert np.diff(f.lower.indptr).max() == 84
+    assert relerr(f.lower.data, ref.data) < 1e-9 and np.max(np.abs(f.variances - ref.d) / ref.d) < 1e-9
+    # one long 1-D line as a single local domain (band of half-width 3, 5000 rows)
+    n, nens, zeta = 5000, 24, 3
+    X = rng.standard_normal((n, nens)).cumsum(axis=0) * 0.05 + 0.5 * rng.standard_normal((n, nens))
+    line = mck.GridGeometry("grid2d", n, 1)
+    fr = mck.fit_factors(orc.center_rows(X), line, zeta)
+    obs = np.arange(0, n, 3)
+    net = mck.ObservationNetwork(obs, np.full(obs.size, 0.1), np.zeros(obs.size))
+    Ys = X[obs] + 0.2 * rng.standard_normal((obs.size, nens))
+    xa = mck.analysis_primal(mck.EnsembleState(X), fr, net, Ys)
+    oref = orc.analysis_primal(X, orc.fit_factors(orc.center_rows(X), orc.Grid(n, 1, True, False), zeta), obs, net.r_diag, Ys)
+    assert relerr(xa.X, oref) < 1e-9
+    # the same length as a periodic ring in one piece: the wrap-around makes the band as wide as the domain -- refused
+    ring = mck.GridGeometry("ring1d", n)
+    with pytest.raises(mck.CapacityError):
+        mck.analysis_primal(mck.EnsembleState(X), mck.fit_factors(orc.center_rows(X), ring, zeta), net, Ys)
+    # zeta = 7 would need 112 predecessors: refused, not truncated
+    with pytest.raises(mck.CapacityError):
+        mck.fit_factors(orc.center_rows(rng.standard_normal((30 * 30, 130))), mck.GridGeometry("grid2d", 30, 30), 7)
