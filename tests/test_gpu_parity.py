@@ -332,3 +332,30 @@ def test_wide_regressions_and_long_local_domains(mck):
     # zeta = 7 would need 112 predecessors: refused, not truncated
     with pytest.raises(mck.CapacityError):
         mck.fit_factors(orc.center_rows(rng.standard_normal((30 * 30, 130))), mck.GridGeometry("grid2d", 30, 30), 7)
+
+
+def test_wide_band_and_tiny_problems(mck):
+    """A tile whose Cholesky window does not fit in shared memory (half-bandwidth 222: windows in global scratch),
+    and the smallest problems there are (one or two grid points, two members)."""
+    from oracle import enkf_mc_oracle as orc
+    rng = np.random.default_rng(33)
+    nx, ny, nens, zeta = 36, 20, 100, 6             # 84 predecessors < 100 members: well-conditioned regressions
+    n = nx * ny
+    X = rng.standard_normal((n, nens)).cumsum(axis=0) * 0.05 + 0.6 * rng.standard_normal((n, nens)) + 1.0
+    obs = np.sort(rng.choice(n, n // 4, replace=False))
+    r = np.full(obs.size, 0.09)
+    Ys = X[obs] + 0.3 * rng.standard_normal((obs.size, nens))
+    for delta in (1, 2):
+        xa, _ = mck.assimilate_parallel(mck.EnsembleState(X), mck.ObservationNetwork(obs, r, Ys.mean(axis=1)),
+                                        mck.AssimilationConfig(zeta=zeta, delta=delta), mck.GridGeometry("grid2d", nx, ny), Ys=Ys)
+        ref = orc.assimilate(X, obs, r, Ys, orc.Grid(nx, ny, True, False), delta, zeta)
+        assert relerr(xa.X, ref) < 1e-9, delta
+    for nx, ny, nens in ((1, 1, 2), (2, 1, 4), (3, 2, 6)):   # (two members on two points would be an exact fit: D on the floor)
+        n = nx * ny
+        X = rng.standard_normal((n, nens)) + 2.0
+        obs = np.array([0])
+        Ys = X[obs] + 0.1 * rng.standard_normal((1, nens))
+        xa, _ = mck.assimilate_parallel(mck.EnsembleState(X), mck.ObservationNetwork(obs, np.array([0.5]), np.zeros(1)),
+                                        mck.AssimilationConfig(zeta=1, delta=1), mck.GridGeometry("grid2d", nx, ny), Ys=Ys)
+        ref = orc.assimilate(X, obs, np.array([0.5]), Ys, orc.Grid(nx, ny, True, False), 1, 1)
+        assert relerr(xa.X, ref) < 1e-10, (nx, ny, nens)
