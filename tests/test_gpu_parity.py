@@ -359,3 +359,41 @@ def test_wide_band_and_tiny_problems(mck):
                                         mck.AssimilationConfig(zeta=1, delta=1), mck.GridGeometry("grid2d", nx, ny), Ys=Ys)
         ref = orc.assimilate(X, obs, np.array([0.5]), Ys, orc.Grid(nx, ny, True, False), 1, 1)
         assert relerr(xa.X, ref) < 1e-10, (nx, ny, nens)
+
+
+def test_changing_networks_orderings_and_empty_fields(mck):
+    """One cached plan serving different observation networks in turn (device-side tables must follow), a field
+    without any observation (copied through exactly), column-major ordering with a periodic boundary on stacked
+    fields, and a tile range together with the host entry point."""
+    from oracle import enkf_mc_oracle as orc
+    from paper_1606_00807_b200 import synthetic
+    from paper_1606_00807_b200.plan import get_plan
+    w = synthetic.make_workload("mf2", nx=20, ny=12, nens=40, corr_len=3.0, zeta=2, delta=6, obs="random", obs_arg=0.5,
+                                r_rel=0.1, r_abs=None, seed=5, nugget=0.02, boundary="periodic",
+                                variables=[("u", 5.0, 2), ("q", 1e-3, 1), ("p", 100.0, 1)])
+    nf = 4
+    cfg = mck.AssimilationConfig(zeta=2, delta=6)
+    for ordering in ("row_major", "column_major"):
+        geo = mck.GridGeometry("grid2d", w.nx, w.ny, ordering=ordering, boundary="periodic", nfields=nf)
+        grid = orc.Grid(w.nx, w.ny, ordering == "row_major", True, nf)
+        keep_sets = [np.ones(w.obs_indices.size, bool),
+                     (w.obs_indices // w.n2d) != 2,                      # field 2 loses all its observations
+                     np.arange(w.obs_indices.size) % 3 != 0]
+        for keep in keep_sets + keep_sets[:1]:                           # back to the first network at the end
+            net = mck.ObservationNetwork(w.obs_indices[keep], w.r_diag[keep], w.y[keep])
+            xa, _ = mck.assimilate_parallel(mck.EnsembleState(w.X), net, cfg, geo, Ys=w.Ys[keep])
+            ref = orc.assimilate(w.X, w.obs_indices[keep], w.r_diag[keep], w.Ys[keep], grid, 6, 2)
+            assert relerr(xa.X, ref) < XA_GATE
+            if keep is keep_sets[1]:
+                sl = slice(2 * w.n2d, 3 * w.n2d)
+                assert np.array_equal(xa.X[sl], w.X[sl])
+        # one rank's share through the host entry point: its interiors are exactly the full run's
+        plan = get_plan(geo, 6, 2)
+        full, _ = mck.assimilate_parallel(mck.EnsembleState(w.X), net, cfg, geo, Ys=w.Ys[keep])
+        plan.set_tile_range(2, 5)
+        part, _ = mck.assimilate_parallel(mck.EnsembleState(w.X), net, cfg, geo, Ys=w.Ys[keep])
+        plan.set_tile_range(0, plan.ntiles)
+        own = np.concatenate([sd.interior for sd in mck.decompose(mck.GridGeometry("grid2d", w.nx, w.ny, ordering=ordering,
+                                                                                    boundary="periodic"), 6, 2)[2:5]])
+        rows = (np.arange(nf)[:, None] * w.n2d + own[None, :]).ravel()
+        assert np.array_equal(part.X[rows], full.X[rows])
