@@ -45,6 +45,8 @@ struct DeviceState {
     double *U = nullptr, *T = nullptr, *D = nullptr, *scratch = nullptr;
     int32_t *flags = nullptr, *status = nullptr;
     unsigned int *counters = nullptr;
+    unsigned int *worklist = nullptr;
+    int64_t worklist_alloc = 0;
     SolveParams solve_layout{};
     int solve_grid = 0;
     // host-path staging
@@ -113,8 +115,8 @@ int ensure_device(enkfmc_plan *p) {
         d->band_stride = bp.back();
         if ((rc = upload(d->band_ptr, bp))) return rc;
     }
-    CK(cudaMalloc(&d->counters, 4 * sizeof(unsigned int)));
-    CK(cudaMemset(d->counters, 0, 4 * sizeof(unsigned int)));
+    CK(cudaMalloc(&d->counters, 8 * sizeof(unsigned int)));
+    CK(cudaMemset(d->counters, 0, 8 * sizeof(unsigned int)));
     for (auto &ev : d->ev) CK(cudaEventCreate(&ev));
     CK(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&d->copy_stream, cudaStreamNonBlocking));
@@ -218,7 +220,7 @@ int do_regress(enkfmc_plan *p, const double *d_U, int64_t nens, double rank_tol,
     R.nwork = (int64_t)p->regress_order.size() * p->nfields;
     R.row_ptr = d->row_ptr; R.pred_state = d->pred_state; R.state_row = d->state_row; R.work_order = d->regress_order;
     R.rank_tol = rank_tol; R.variance_floor = floor_; R.fast_ratio = 1e-6;
-    R.T = d_T; R.D = d_D; R.flags = d_flags; R.counter = d->counters;
+    R.T = d_T; R.D = d_D; R.flags = d_flags; R.counter = d->counters; R.lcounter = d->counters + 4;
     R.rq_ptr = d->rq_ptr; R.rq_stride = d->rq_stride;
     // QR scratch: as many fields per launch pair as fit in the budget (default 16 GiB)
     const int64_t budget = (int64_t)16 << 30;
@@ -229,6 +231,13 @@ int do_regress(enkfmc_plan *p, const double *d_U, int64_t nens, double rank_tol,
         d->rq_alloc = chunk * d->rq_stride;
     }
     R.Rq = d->Rq;
+    const int64_t list_need = (int64_t)p->regress_order.size() * chunk;
+    if (!d->worklist || d->worklist_alloc < list_need) {
+        release(d->worklist);
+        CK(cudaMalloc(&d->worklist, std::max<size_t>((size_t)list_need, 1) * sizeof(unsigned int)));
+        d->worklist_alloc = list_need;
+    }
+    R.worklist = d->worklist;
     for (int64_t f0 = fbeg; f0 < fend; f0 += chunk) {
         R.f0 = (int)f0;
         R.f1 = (int)std::min<int64_t>(fend, f0 + chunk);
@@ -237,11 +246,11 @@ int do_regress(enkfmc_plan *p, const double *d_U, int64_t nens, double rank_tol,
         cudaError_t e = launch_regress(R, d->sm_count, d->smem_limit, s, mid);
         if (e == cudaErrorInvalidConfiguration) {
             enkfmc_set_error("regression workspace (nens=" + std::to_string(nens) + ", predecessors=" +
-                             std::to_string(p->max_pred) + ") exceeds shared memory or the 96-predecessor cap");
+                             std::to_string(p->max_pred) + ") exceeds shared memory or the 128-predecessor cap");
             return ENKFMC_E_CAPACITY;
         }
         CK(e);
-        if (R.nwork > 0) p->counters[0] += 2;
+        if (R.nwork > 0) p->counters[0] += 3;
     }
     if (!p->alias_row.empty()) {   // copy each distinct regression to the other tiles holding the same row
         CK(launch_replicate_rows(d->alias_row, d->alias_rep, (int64_t)p->alias_row.size(), d->row_ptr, fend - fbeg,
@@ -306,7 +315,7 @@ void enkfmc_device_release(enkfmc_plan *p) {
     release(d->csc_row); release(d->phys); release(d->iphys); release(d->bw); release(d->state_row);
     release(d->pred_state); release(d->regress_order); release(d->alias_row); release(d->alias_rep); release(d->work_order); release(d->tile_order); release(d->is_interior); release(d->tile_mono);
     release(d->obs_slot); release(d->tile_nobs); release(d->U); release(d->T); release(d->D); release(d->scratch);
-    release(d->flags); release(d->status); release(d->counters); release(d->rq_ptr); release(d->Rq); release(d->band_ptr); release(d->band); release(d->row_tile); release(d->dX); release(d->dXa); release(d->dR);
+    release(d->flags); release(d->status); release(d->counters); release(d->rq_ptr); release(d->Rq); release(d->worklist); release(d->band_ptr); release(d->band); release(d->row_tile); release(d->dX); release(d->dXa); release(d->dR);
     release(d->dYs);
     for (auto &ev : d->ev) if (ev) cudaEventDestroy(ev);
     for (auto &ev : d->hev) cudaEventDestroy(ev);

@@ -5,7 +5,7 @@
 //
 //   K0  center_rows_kernel                       validation.py:35-39
 //   K2a regress_qr_mma_kernel / regress_qr_kernel  estimator.py:46-61,133-150 (the QR half)
-//   K2b regress_solve_kernel                     estimator.py:46-61 (truncated-SVD semantics) + factors.py:60
+//   K2b regress_clean_kernel / regress_trunc_kernel (regress_solve.cuh)   estimator.py:46-61 (truncated-SVD semantics) + factors.py:60
 //   K3a assemble_band_tile_kernel / assemble_band_kernel   factors.py:136-145, kernels.py:189-191
 //   K3b local_solve_kernel                       kernels.py:178-218, driver.py:99-125
 //
@@ -112,34 +112,12 @@ cudaError_t launch_center_rows(const double *X, double *U, int64_t nrows, int N,
 //   in S = ceil(N / 32) register slots, two reflectors per sweep, eight columns share two
 //   transposing warp reductions).
 //
-// K2b regress_solve_kernel.  R (p x p) in shared memory, p-vectors in registers.
-//   X = R^-1 by 8 x 8 blocks on the tensor cores gives sum 1/s_i^2 = |X|_F^2 (and, on demand,
-//   sum 1/s_i^4 = |X X^T|_F^2): a rigorous lower bound of the smallest singular value not yet
-//   deflated; when cancellation eats those sums the same bound comes from |X - (X U) U^T|_F
-//   (Eckart-Young).  If the bound does not clear rank_tol * |R|_F, inverse iteration from a
-//   pseudo-random start (two triangular solves per step; its estimate is an upper bound) proves
-//   that the reference's truncation (estimator.py:55-57) is active, converges the pair
-//   (z, u = R^-T z / |R^-T z|), deflates it and the bounds are re-evaluated; close sub-threshold
-//   values are sharpened together by a block (subspace) iteration with a Ritz / Cholesky test.
-//   beta = (I - Z Z^T) R^-1 (I - U U^T) c is then exactly the reference's truncated-SVD answer.
-//   Anything that cannot be settled (zero pivots, p > N, cond(R) beyond cond_max, no gap, a
-//   singular value within 0.1 % of the threshold, more truncated values than the workspace
-//   holds) goes to the general fallback: one-sided Jacobi SVD on the rows of [R | c] with the
-//   same rule.  T = -beta;  D = max((e2 + |c - R beta|^2) / (N-1), floor): |y - A^T beta|^2 of
-//   estimator.py:60,148 evaluated in the QR basis (orthogonal invariance), the second term only
-//   when something was truncated -- the predecessor rows are not read a second time.
+// K2b regress_clean_kernel + regress_trunc_kernel: regress_solve.cuh (certificate and plain solve; block inverse
+//   iteration + Rayleigh-Ritz for the rows that truncate; one-sided Jacobi SVD as the general fallback).
 // ------------------------------------------------------------------------------------------
-#define REG_MAXDEFL_CAP 12
-#define JACOBI_MAX_SWEEPS 30
-#define INVIT_MAX 40
 
 __host__ __device__ inline size_t regress_qr_ws_doubles(int N, int pmax) {
     const size_t d = (size_t)(N | 1) * (pmax + 1) + (size_t)pmax + 2;   // W | rdiag
-    return (d + 1) & ~(size_t)1;
-}
-__host__ __device__ inline size_t regress_solve_ws_doubles(int pmax, int maxdefl) {
-    // R (pitch pmax|1, pmax+1 columns: the last is c) | rinv | aux | tmp | mma staging | Z[maxdefl] | W[maxdefl] | G
-    const size_t d = (size_t)(pmax | 1) * (pmax + 1) + (size_t)(3 + 2 * maxdefl) * pmax + (size_t)maxdefl * maxdefl + 2 + 64;
     return (d + 1) & ~(size_t)1;
 }
 size_t regress_warp_workspace_doubles(int N, int pmax) { return regress_qr_ws_doubles(N, pmax); }
@@ -423,8 +401,7 @@ __device__ __forceinline__ void vstore(double *dst, const Vec<PS> &a, int p, int
 }
 
 // x = R^-1 b  (R upper triangular in W, diagonal reciprocals in rinv); b is overwritten.
-// (called, not inlined: regress_solve_kernel has a dozen call sites and was 21 k instructions long, far beyond the
-// instruction cache)
+// (called, not inlined: several call sites)
 template <int PS>
 __device__ __noinline__ Vec<PS> solve_upper(Vec<PS> b, const double *W, const double *rinv, int ld, int p, int lane) {
     // element k is final when column k is reached and never touched again: x = b * rinv once at the end
@@ -513,281 +490,25 @@ __device__ __noinline__ Vec<PS> mul_upper_t(const Vec<PS> y, const double *W, in
     return w;
 }
 
-// ---- tensor-core helpers for the truncation certificate ---------------------------------------
-__device__ __forceinline__ void mma_f64(double &d0, double &d1, double a, double b) {
-    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-        : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
-}
-// R[r, c] (upper triangular incl. diagonal, column-major in W) with zero padding beyond p
-__device__ __forceinline__ double r_elem(const double *W, int ld, int p, int r, int c) {
-    return (r <= c && c < p) ? W[(size_t)c * ld + r] : 0.0;
-}
-// X = R^-1: strictly upper part stored transposed in the strict lower triangle of W, diagonal = rinv
-__device__ __forceinline__ double x_elem(const double *W, const double *rinv, int ld, int p, int r, int c) {
-    if (r > c || c >= p) return 0.0;
-    return r == c ? rinv[r] : W[(size_t)r * ld + c];
-}
-
-// |X|_F^2 = sum 1/s_i^2 and |X X^T|_F^2 = sum 1/s_i^4 of X = R^-1, by 8 x 8 blocks on the FP64 tensor
-// cores (mma.sync m8n8k4): X_jj by back-substitution (one lane per column), X_ij = -X_ii sum_k R_ik X_kj.
-// X^T is left in the strict lower triangle of W; stage = 64 doubles of per-warp scratch.
-__device__ __noinline__ double inverse_norm2_mma(double *W, const double *rinv, int ld, int p, double *stage, int lane) {
-    const int t4 = lane & 3, m = lane >> 2;
-    const int nbk = (p + 7) >> 3;
-    double f2 = 0.0;
-    // diagonal blocks, four at a time: lanes 8 g .. 8 g + 7 own the columns of block jb0 + g (back-substitution per column)
-    for (int jb0 = 0; jb0 < nbk; jb0 += 4) {
-        const int j = jb0 + (lane >> 3), l8 = lane & 7;
-        const int c = 8 * j + l8;
-        const bool act = c < p;
-        const double rc = act ? rinv[c] : 0.0;
-        f2 += rc * rc;
-        for (int kk = 6; kk >= 0; --kk) {
-            if (act && l8 > kk) {
-                const int k = 8 * j + kk;
-                double acc = W[(size_t)c * ld + k] * rc;                        // R[k,c] X[c,c]
-                for (int i = k + 1; i < c; ++i) acc += W[(size_t)i * ld + k] * W[(size_t)i * ld + c];   // R[k,i] X[i,c]
-                const double x = -rinv[k] * acc;
-                W[(size_t)k * ld + c] = x;
-                f2 += x * x;
-            }
+// Single reflector per call (column k keeps its tail below the diagonal: the reflector can be rebuilt later).
+template <int S>
+__device__ __forceinline__ void qr_step1_dispatch(double *W, int ld, int N, int k, int plast, double *rdiag, int lane) {
+    if constexpr (S <= 4) {
+        switch (k >> 5) {
+            case 0: qr_step<S, 0>(W, ld, N, k, plast, rdiag, lane); break;
+            case 1: if constexpr (S > 1) qr_step<S, 1>(W, ld, N, k, plast, rdiag, lane); break;
+            case 2: if constexpr (S > 2) qr_step<S, 2>(W, ld, N, k, plast, rdiag, lane); break;
+            default: if constexpr (S > 3) qr_step<S, 3>(W, ld, N, k, plast, rdiag, lane); break;
         }
+    } else {
+        qr_step<S, 0>(W, ld, N, k, plast, rdiag, lane);
     }
-    __syncwarp();
-    // blocks above the diagonal, column block by column block: X_ij = -X_ii sum_{i<k<=j} R_ik X_kj.  Only X_jj, X_ii and the
-    // last (possibly partial) block column need the guarded element access.
-    for (int j = 1; j < nbk; ++j) {
-        const bool jfull = 8 * j + 8 <= p;
-        for (int i = j - 1; i >= 0; --i) {
-            double s0 = 0.0, s1 = 0.0;
-            for (int k = i + 1; k < j; ++k) {                                   // dense R_ik (8 k + 7 < p) and dense X_kj
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const double a = W[(size_t)(8 * k + 4 * h + t4) * ld + 8 * i + m];
-                    const double b = jfull ? W[(size_t)(8 * k + 4 * h + t4) * ld + 8 * j + m]
-                                           : x_elem(W, rinv, ld, p, 8 * k + 4 * h + t4, 8 * j + m);
-                    mma_f64(s0, s1, a, b);
-                }
-            }
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {                                       // k = j: R_ij may be partial, X_jj is triangular
-                const double a = r_elem(W, ld, p, 8 * i + m, 8 * j + 4 * h + t4);
-                const double b = x_elem(W, rinv, ld, p, 8 * j + 4 * h + t4, 8 * j + m);
-                mma_f64(s0, s1, a, b);
-            }
-            stage[m * 8 + 2 * t4] = s0;                     // S (8 x 8, row-major) -> B fragments of the next product
-            stage[m * 8 + 2 * t4 + 1] = s1;
-            __syncwarp();
-            double x0 = 0.0, x1 = 0.0;
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const double a = x_elem(W, rinv, ld, p, 8 * i + m, 8 * i + 4 * h + t4);
-                mma_f64(x0, x1, a, stage[(4 * h + t4) * 8 + m]);
-            }
-            const int row = 8 * i + m, c0 = 8 * j + 2 * t4;
-            if (c0 < p) W[(size_t)row * ld + c0] = -x0;     // X[row, c0] at (row c0, column row); row < 8 j <= c0
-            if (c0 + 1 < p) W[(size_t)row * ld + c0 + 1] = -x1;
-            f2 += x0 * x0 + x1 * x1;                        // padded entries are exactly zero
-            __syncwarp();
-        }
-    }
-    return warp_sum(f2);
-}
-
-// |X X^T|_F^2 = sum 1/s_i^4 from the X left in W by inverse_norm2_mma (computed only when the second-power bound
-// alone does not settle a row).  H = X X^T by blocks a <= b: H_ab = sum_{c >= b} X_ac X_bc^T.
-__device__ __noinline__ double xxt_norm4_mma(const double *W, const double *rinv, int ld, int p, int lane) {
-    const int t4 = lane & 3, m = lane >> 2;
-    const int nbk = (p + 7) >> 3;
-    double g4 = 0.0;
-    for (int a = 0; a < nbk; ++a) {
-        for (int b = a; b < nbk; ++b) {
-            double h0 = 0.0, h1 = 0.0;
-            for (int c = b; c < nbk; ++c) {
-                const bool plain = c > b && 8 * c + 8 <= p;                     // both blocks dense and inside the matrix
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    double av, bv;
-                    if (plain) {
-                        av = W[(size_t)(8 * a + m) * ld + 8 * c + 4 * h + t4];
-                        bv = W[(size_t)(8 * b + m) * ld + 8 * c + 4 * h + t4];
-                    } else {
-                        av = x_elem(W, rinv, ld, p, 8 * a + m, 8 * c + 4 * h + t4);
-                        bv = x_elem(W, rinv, ld, p, 8 * b + m, 8 * c + 4 * h + t4);   // (X_bc^T)[k][n] = X_bc[n][k]
-                    }
-                    mma_f64(h0, h1, av, bv);
-                }
-            }
-            g4 += (a == b ? 1.0 : 2.0) * (h0 * h0 + h1 * h1);
-        }
-    }
-    return warp_sum(g4);
-}
-
-// |X - (X U) U^T|_F^2 for m p-vectors U (rows of Us, pitch pmax), X = R^-1 as left in W by inverse_norm2_mma.
-// (X U) U^T has rank <= m, so by Eckart-Young sigma_{m+1}(X) <= |X - (X U) U^T|_2 <= the Frobenius norm returned,
-// whatever U is: 1 / sqrt(result) is a rigorous lower bound of the (m+1)-th smallest singular value of R.  Formed
-// element by element, it does not suffer the cancellation of |X|_F^2 - sum 1/s_k^2 when cond(R) is large.
-template <int PS, int M>
-__device__ __noinline__ double deflated_inverse_norm2(const double *W, const double *rinv, int ld, int p, const double *Us,
-                                                      int pmax, int m, int lane) {
-    double Y[PS][M];                                        // (X U)[lane + 32 t][k]
-#pragma unroll
-    for (int t = 0; t < PS; ++t)
-#pragma unroll
-        for (int k = 0; k < M; ++k) Y[t][k] = 0.0;
-    for (int c = 0; c < p; ++c) {
-        double uc[M];
-#pragma unroll
-        for (int k = 0; k < M; ++k) uc[k] = k < m ? Us[(size_t)k * pmax + c] : 0.0;
-        const double dg = rinv[c];
-#pragma unroll
-        for (int t = 0; t < PS; ++t) {
-            const int r = lane + 32 * t;
-            const double x = r < c ? W[(size_t)r * ld + c] : (r == c ? dg : 0.0);
-#pragma unroll
-            for (int k = 0; k < M; ++k) Y[t][k] = fma(x, uc[k], Y[t][k]);
-        }
-    }
-    double acc = 0.0;
-    for (int c = 0; c < p; ++c) {
-        double uc[M];
-#pragma unroll
-        for (int k = 0; k < M; ++k) uc[k] = k < m ? Us[(size_t)k * pmax + c] : 0.0;
-        const double dg = rinv[c];
-#pragma unroll
-        for (int t = 0; t < PS; ++t) {
-            const int r = lane + 32 * t;
-            double e = r < c ? W[(size_t)r * ld + c] : (r == c ? dg : 0.0);
-#pragma unroll
-            for (int k = 0; k < M; ++k) e = fma(-Y[t][k], uc[k], e);
-            if (r < p) acc = fma(e, e, acc);
-        }
-    }
-    return warp_sum(acc);
-}
-
-// General fallback: one-sided Jacobi SVD on the rows of [R | c] (K x (p+1), explicit zeros below
-// the diagonal), truncation as estimator.py:55-57.  Writes beta to out[0..p); returns flag bits and
-// the squared norm of the truncated part of c in *dropped2.
-__device__ __noinline__ int jacobi_solve(double *W, int ld, int K, int p, double rank_tol, double *s2buf, double *coef,
-                            double *out, double *dropped2, int lane) {
-    int flag = 0;
-    const int M = (K + 1) & ~1;
-    const int npairs = M >> 1;
-    const int T = lanes_per_item(npairs);
-    const int per = 32 / T, sub = lane % T;
-    const double tolj = DBL_EPSILON * sqrt((double)p);
-    double *cvec = W + (size_t)p * ld;
-    int sweep = 0;
-    bool rotated = (K > 1);
-    while (rotated && sweep < JACOBI_MAX_SWEEPS) {
-        rotated = false;
-        ++sweep;
-        for (int r = 0; r < M - 1; ++r) {
-            for (int q0 = 0; q0 < npairs; q0 += per) {
-                const int qi = q0 + lane / T;
-                int a, b;
-                if (qi == 0) { a = M - 1; b = r; }
-                else { a = (r + qi) % (M - 1); b = (r - qi + (M - 1)) % (M - 1); }
-                const bool on = (qi < npairs) && (a < K) && (b < K);
-                if (!on) { a = 0; b = 0; }
-                const double *ra = W + a, *rb = W + b;
-                double g = 0.0, da = 0.0, db = 0.0;
-                if (on) for (int c = sub; c < p; c += T) {
-                    const double x = ra[(size_t)c * ld], y = rb[(size_t)c * ld];
-                    g += x * y; da += x * x; db += y * y;
-                }
-                g = group_sum(g, T); da = group_sum(da, T); db = group_sum(db, T);
-                const bool rot = on && (fabs(g) > tolj * sqrt(da * db)) && (g != 0.0);
-                if (rot) {
-                    const double zeta = (db - da) / (2.0 * g);
-                    const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-                    const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
-                    double *wa = W + a, *wb = W + b;
-                    for (int c = sub; c <= p; c += T) {
-                        const double x = wa[(size_t)c * ld], y = wb[(size_t)c * ld];
-                        wa[(size_t)c * ld] = cs * x - sn * y;
-                        wb[(size_t)c * ld] = sn * x + cs * y;
-                    }
-                }
-                if (__any_sync(FULL, rot)) rotated = true;
-            }
-            __syncwarp();
-        }
-    }
-    if (sweep >= JACOBI_MAX_SWEEPS && rotated) flag |= 4;
-    flag |= sweep << 16;                               // sweeps used (diagnostics, flag bits 16-21)
-    double smax = 0.0;
-    for (int k = lane; k < K; k += 32) {
-        const double *row = W + k;
-        double s2 = 0.0;
-        for (int c = 0; c < p; ++c) { const double v = row[(size_t)c * ld]; s2 += v * v; }
-        s2buf[k] = s2;
-        smax = fmax(smax, s2);
-    }
-    smax = sqrt(warp_max(smax));
-    __syncwarp();
-    bool dropped = false;
-    double d2 = 0.0;
-    for (int k = lane; k < K; k += 32) {
-        const double s = sqrt(s2buf[k]);
-        const bool keep = (s >= rank_tol * smax) && (s > 0.0);
-        coef[k] = keep ? cvec[k] / s2buf[k] : 0.0;
-        if (!keep) d2 += cvec[k] * cvec[k];
-        dropped |= !keep;
-    }
-    *dropped2 = warp_sum(d2);
-    if (__any_sync(FULL, dropped)) flag |= 2;
-    __syncwarp();
-    for (int j = lane; j < p; j += 32) {
-        const double *col = W + (size_t)j * ld;
-        double b = 0.0;
-        for (int k = 0; k < K; ++k) b += col[k] * coef[k];
-        out[j] = b;
-    }
-    __syncwarp();
-    return flag;
-}
-
-// offset of column j inside a packed R with K rows: sum_{i<j} min(i+1, K)
-__device__ __forceinline__ int64_t packed_col_offset(int j, int K) {
-    return j <= K ? (int64_t)j * (j + 1) / 2 : (int64_t)K * (K + 1) / 2 + (int64_t)(j - K) * K;
-}
-
-// Packed block -> dense [R | c] with p rows (rows >= K and the strict lower part are zero); p <= 32 PS.
-// *fro2 (if asked for) = |R|_F^2.
-template <int PS>
-__device__ __forceinline__ void unpack_rc(const double *in, double *W, int ld, int p, int K, int lane,
-                                          double *fro2 = nullptr) {
-    double f2 = 0.0;
-    for (int j0 = 0; j0 <= p; j0 += 4) {               // four columns in flight: the loads are latency-bound
-        double v[4][PS];
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-            const int j = j0 + b <= p ? j0 + b : p;
-            const int h = j < p ? (j + 1 < K ? j + 1 : K) : K;
-            const double *src = in + packed_col_offset(j, K);
-#pragma unroll
-            for (int t = 0; t < PS; ++t) { const int i = lane + 32 * t; v[b][t] = i < h ? src[i] : 0.0; }
-        }
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-            const int j = j0 + b;
-            if (j > p) break;
-            double *col = W + (size_t)j * ld;
-#pragma unroll
-            for (int t = 0; t < PS; ++t) {
-                const int i = lane + 32 * t;
-                if (i < p) col[i] = v[b][t];
-                if (j < p) f2 = fma(v[b][t], v[b][t], f2);
-            }
-        }
-    }
-    if (fro2) *fro2 = warp_sum(f2);
 }
 
 }  // namespace
+
+#include "regress_solve.cuh"
+
 
 // ---- K2a: load + Householder QR ------------------------------------------------------------
 template <int S>
@@ -1109,406 +830,6 @@ __global__ void __launch_bounds__(256, 1) regress_qr_mma_kernel(const RegressPar
     }
 }
 
-// ---- K2b: truncation probes + solve --------------------------------------------------------
-template <int PS>
-__global__ void __launch_bounds__(512, 1) regress_solve_kernel(const RegressParams P) {
-    extern __shared__ double smem[];
-    const int lane = threadIdx.x & 31;
-    const int N = P.N, pmax = P.pmax, ld = pmax | 1;
-    double *W = smem + (size_t)(threadIdx.x >> 5) * regress_solve_ws_doubles(pmax, P.maxdefl);
-    double *rinv = W + (size_t)ld * (pmax + 1);
-    double *aux = rinv + pmax;
-    double *tmp = aux + pmax;
-    double *stage = tmp + pmax;                 // 64 doubles of scratch for the tensor-core block products
-    double *Zs = stage + 64;                    // deflated right singular vectors (x = R z / s is rebuilt on use)
-    double *Ws = Zs + P.maxdefl * pmax;         // M Z during the block polish
-    double *Gs = Ws + P.maxdefl * pmax;         // Z^T M Z
-    const double denom = (double)(N - 1);
-    const unsigned nf = (unsigned)(P.f1 - P.f0);
-
-    for (;;) {
-        unsigned int wk = 0;
-        if (lane == 0) wk = atomicAdd(P.counter + 1, 1u);
-        wk = __shfl_sync(FULL, wk, 0);
-        if ((int64_t)wk >= P.nwork) break;
-        const int q = P.work_order[wk / nf];
-        const int fl = (int)(wk % nf), f = P.f0 + fl;
-        const int64_t r0 = P.row_ptr[q];
-        const int p = (int)(P.row_ptr[q + 1] - r0);
-        if (p == 0) continue;                    // done in K2a
-        const int K = p < N ? p : N;
-        int flag = 0, nsteps = 0;               // nsteps: inverse-iteration steps spent on this row (flag bits 8-15)
-
-        // ---- unpack R | c into the dense workspace, zeros below the diagonal ---------------
-        const double *in = P.Rq + (int64_t)fl * P.rq_stride + P.rq_ptr[q];
-        double dmin = DBL_MAX, dmax = 0.0, fro2 = 0.0;
-        unpack_rc<PS>(in, W, ld, p, K, lane, &fro2);
-        __syncwarp();
-        for (int j = lane; j < K; j += 32) {
-            const double v = W[(size_t)j * ld + j];
-            rinv[j] = 1.0 / v;
-            dmin = fmin(dmin, fabs(v));
-            dmax = fmax(dmax, fabs(v));
-        }
-        const double e2 = in[packed_col_offset(p, K) + K];
-        dmin = warp_min(dmin);
-        dmax = warp_max(dmax);
-        const double fro = sqrt(fro2);
-        __syncwarp();
-        const double *cvec = W + (size_t)p * ld;   // Q^T y
-        bool fallback = (K < p) || !(dmin > 1e-13 * dmax);
-        int m = 0, why = fallback ? 1 : 0;   // fallback reason, reported in flag bits 5-7
-        bool left_fresh = false;             // Ws holds the orthonormal left basis of the m deflated vectors
-
-        // left singular subspace of the deflated values: orthonormal basis of R^-T Z in Ws (Z spans the right one;
-        // R^-T z is accurate to eps |R| / gap in direction, R z would only be to eps cond(R))
-        auto build_left_basis = [&]() {
-            for (int mm = 0; mm < m; ++mm) {
-                Vec<PS> xm = vload<PS>(Zs + mm * pmax, p, lane);
-                xm = solve_upper_t<PS>(xm, W, rinv, ld, p, lane);
-                for (int l = 0; l < mm; ++l) {
-                    const Vec<PS> xl = vload<PS>(Ws + l * pmax, p, lane);
-                    const double g = vdot<PS>(xl, xm);
-#pragma unroll
-                    for (int t = 0; t < PS; ++t) xm.v[t] -= g * xl.v[t];
-                }
-                const double inv = 1.0 / sqrt(vdot<PS>(xm, xm));
-#pragma unroll
-                for (int t = 0; t < PS; ++t) xm.v[t] *= inv;
-                vstore<PS>(Ws + mm * pmax, xm, p, lane);
-                __syncwarp();
-            }
-        };
-        if (!fallback) {
-            // s_max bracket: power iteration from below, Frobenius norm from above
-            Vec<PS> v;
-#pragma unroll
-            for (int t = 0; t < PS; ++t) v.v[t] = (lane + 32 * t < p) ? 1.0 : 0.0;
-            double smax_lo = dmax;                        // |r_jj| <= |R e_j| <= s_max
-            int power_done = 0;
-            auto power = [&](int iters) {
-                for (int it = 0; it < iters; ++it) {
-                    Vec<PS> y = mul_upper<PS>(v, W, ld, p, lane);
-                    v = mul_upper_t<PS>(y, W, ld, p, lane);
-                    const double nv = sqrt(vdot<PS>(v, v));
-                    if (power_done + it > 0) smax_lo = fmax(smax_lo, sqrt(nv));   // first pass starts unnormalised
-                    const double inv = 1.0 / nv;
-#pragma unroll
-                    for (int t = 0; t < PS; ++t) v.v[t] *= inv;
-                }
-                power_done += iters;
-            };
-            bool refined = false;            // (the power iteration runs only for rows that need a probe)
-            double smax_hi = fro;            // upper bound of s_max: |R|_F until the power iteration has converged
-            // probes: smallest singular triplets by inverse iteration, deflating truncated ones
-            // Rigorous certificate for "nothing (left) below the threshold": with X = R^-1,
-            // |X|_F^2 = sum_i 1/s_i^2 and |X X^T|_F^2 = sum_i 1/s_i^4, so after deflating converged triplets
-            // s_1..s_m the next singular value obeys
-            //     s_next >= max( (sum_2 - sum_k 1/s_k^2)^(-1/2), (sum_4 - sum_k 1/s_k^4)^(-1/4) ).
-            // The fourth-power bound is within a few per cent of s_next even for clustered spectra.
-            double tail2 = 0.0, tail4 = 0.0; // sum 1/s^2 and sum 1/s^4 over the singular values not yet deflated
-            bool ok2 = true, ok4 = true;     // false once cancellation has eaten the respective certificate
-            tail2 = inverse_norm2_mma(W, rinv, ld, p, stage, lane);
-            bool have4 = false;              // the fourth-power sum is formed on demand
-            // One inverse-iteration probe in the complement of the deflated vectors, from a pseudo-random
-            // start.  The estimate bounds the smallest remaining singular value from above; once it is below
-            // rank_tol * lower(s_max) the truncation is proven and the vector is iterated to convergence.
-            // Returns true with the converged pair, false if the estimate stays above the threshold (the
-            // certificate was inconclusive) or the vector does not converge (no gap).
-            auto probe = [&](unsigned seed, Vec<PS> &z, double &zMz, double &Mz2, Vec<PS> &yt) -> int {
-#pragma unroll
-                for (int t = 0; t < PS; ++t) {
-                    const int e = lane + 32 * t;
-                    unsigned h = (unsigned)(e + 1) * 2654435761u ^ (seed * 40503u + 0x9e3779b9u);
-                    h ^= h >> 15; h *= 2246822519u; h ^= h >> 13; h *= 3266489917u; h ^= h >> 16;
-                    z.v[t] = e < p ? (double)(h >> 8) * (1.0 / 8388608.0) - 1.0 : 0.0;
-                }
-                for (int mm = 0; mm < m; ++mm) {
-                    const Vec<PS> zm = vload<PS>(Zs + mm * pmax, p, lane);
-                    const double pr = vdot<PS>(z, zm);
-#pragma unroll
-                    for (int t = 0; t < PS; ++t) z.v[t] -= pr * zm.v[t];
-                }
-                {
-                    const double inv = 1.0 / sqrt(vdot<PS>(z, z));
-#pragma unroll
-                    for (int t = 0; t < PS; ++t) z.v[t] *= inv;
-                }
-                double dz_old = 1.0;
-                for (int it = 0; it < INVIT_MAX; ++it) {
-                    ++nsteps;
-                    Vec<PS> zz = z;
-                    zz = solve_upper_t<PS>(zz, W, rinv, ld, p, lane);
-                    yt = zz;                                       // R^-T z: the left singular direction, for free
-                    zz = solve_upper<PS>(zz, W, rinv, ld, p, lane);
-                    for (int mm = 0; mm < m; ++mm) {
-                        const Vec<PS> zm = vload<PS>(Zs + mm * pmax, p, lane);
-                        const double pr = vdot<PS>(zz, zm);
-#pragma unroll
-                        for (int t = 0; t < PS; ++t) zz.v[t] -= pr * zm.v[t];
-                    }
-                    const double nz = sqrt(vdot<PS>(zz, zz));
-                    zMz = vdot<PS>(zz, z);                         // z^T M z and |M z|^2 of the previous iterate
-                    Mz2 = nz * nz;
-                    const double inv = 1.0 / nz;
-                    const double s_est = 1.0 / sqrt(nz);
-                    const double sg = zMz >= 0.0 ? 1.0 : -1.0;
-                    double dz = 0.0;
-#pragma unroll
-                    for (int t = 0; t < PS; ++t) {
-                        const double zn = zz.v[t] * inv;
-                        const double df = zn - sg * z.v[t];
-                        dz += df * df;
-                        z.v[t] = zn;
-                    }
-                    dz = sqrt(warp_sum(dz));
-                    if (s_est < P.rank_tol * smax_lo) {          // s_next <= s_est < tol * s_max: truncated for sure
-                        if ((dz < 1e-6 && dz > 0.9 * dz_old) || dz < 1e-12) return 2;      // at the rounding floor
-                        // linear convergence with ratio q = dz / dz_old: the iterate just computed is within
-                        // dz q / (1 - q) of the limit -- stop once that is at the 5e-14 level
-                        if (it >= 2 && dz < 0.25 * dz_old && dz * dz < 4e-14 * dz_old) return 2;
-                        // slow phase: what still moves is a rotation among close sub-threshold directions --
-                        // hand the vector to the block polish
-                        if (it >= 6 && dz < 1e-2 && dz > 0.4 * dz_old && dz < 0.95 * dz_old) return 1;
-                    } else if (it >= 12) {
-                        return 0;                                // stays above the threshold: cannot certify here
-                    }
-                    dz_old = dz;
-                }
-                return 0;
-            };
-            // Block polish of the deflated vectors Z (m columns): subspace iteration Z <- orth(M Z), M = (R^T R)^-1,
-            // until the invariance residual |M Z - Z (Z^T M Z)|_F / |M Z|_F is at the rounding floor.  Returns the
-            // exact deflated sums tr(Z^T M Z), |M Z|_F^2 and checks that every singular value inside span(Z) is
-            // below the threshold (Cholesky test of Z^T M Z - mu I).  0 ok, 1 not converged, 2 a kept direction
-            // (or a near-threshold value) sits in the block.
-            auto polish = [&](double &sum2, double &sum4) -> int {
-                double res_old = 1e300;
-                bool conv = false;
-                for (int round = 0; round < 8 && !conv; ++round) {
-                    double w2 = 0.0, res2 = 0.0;
-                    for (int k = 0; k < m; ++k) {
-                        Vec<PS> w = vload<PS>(Zs + k * pmax, p, lane);
-                        w = solve_upper_t<PS>(w, W, rinv, ld, p, lane);
-                        w = solve_upper<PS>(w, W, rinv, ld, p, lane);
-                        vstore<PS>(Ws + k * pmax, w, p, lane);
-                        w2 += vdot<PS>(w, w);
-                    }
-                    __syncwarp();
-                    for (int k = 0; k < m; ++k) {
-                        Vec<PS> r = vload<PS>(Ws + k * pmax, p, lane);
-                        const Vec<PS> w = r;
-                        for (int l = 0; l < m; ++l) {
-                            const Vec<PS> zl = vload<PS>(Zs + l * pmax, p, lane);
-                            const double g = vdot<PS>(zl, w);
-                            if (lane == 0) Gs[l * m + k] = g;
-#pragma unroll
-                            for (int t = 0; t < PS; ++t) r.v[t] -= g * zl.v[t];
-                        }
-                        res2 += vdot<PS>(r, r);
-                    }
-                    __syncwarp();
-                    const double res = sqrt(res2 / w2);
-                    sum4 = w2;
-                    conv = (res < 1e-7 && res > 0.9 * res_old) || res < 1e-11;   // at the rounding floor, not merely slow
-                    res_old = res;
-                    if (conv) break;
-                    for (int k = 0; k < m; ++k) {              // Z <- orth(W), modified Gram-Schmidt
-                        Vec<PS> w = vload<PS>(Ws + k * pmax, p, lane);
-                        for (int l = 0; l < k; ++l) {
-                            const Vec<PS> zl = vload<PS>(Zs + l * pmax, p, lane);
-                            const double g = vdot<PS>(zl, w);
-#pragma unroll
-                            for (int t = 0; t < PS; ++t) w.v[t] -= g * zl.v[t];
-                        }
-                        const double inv = 1.0 / sqrt(vdot<PS>(w, w));
-#pragma unroll
-                        for (int t = 0; t < PS; ++t) w.v[t] *= inv;
-                        vstore<PS>(Zs + k * pmax, w, p, lane);
-                        __syncwarp();
-                    }
-                }
-                if (!conv) return 1;
-                sum2 = 0.0;
-                for (int k = 0; k < m; ++k) sum2 += Gs[k * m + k];
-                // all singular values inside span(Z) below the threshold  <=>  G - mu I positive definite
-                int bad = 0;
-                if (lane == 0) {
-                    const double thr = P.rank_tol * smax_lo * (1.0 - 1e-3);
-                    const double mu = 1.0 / (thr * thr);
-                    for (int a = 0; a < m && !bad; ++a) {
-                        for (int b = 0; b <= a; ++b) {
-                            double v = 0.5 * (Gs[a * m + b] + Gs[b * m + a]) - (a == b ? mu : 0.0);
-                            for (int c = 0; c < b; ++c) v -= Gs[a * m + c] * Gs[b * m + c];   // lower factor overwrites G
-                            if (a == b) { if (!(v > 0.0)) { bad = 1; break; } Gs[a * m + a] = sqrt(v); }
-                            else Gs[a * m + b] = v / Gs[b * m + b];
-                        }
-                    }
-                }
-                bad = __shfl_sync(FULL, bad, 0);
-                return bad ? 2 : 0;
-            };
-
-            // depends on the regression only (not on the field, nor on which tile's copy of the row is computed)
-            unsigned seed = (unsigned)P.state_row[q] * 7919u + (unsigned)p * 104729u;
-            const double T2 = tail2;               // totals over all singular values
-            double T4 = 0.0;
-            int ey_m = 0;                          // number of deflated vectors the Eckart-Young bound was last formed for
-            left_fresh = false;
-            double def2 = 0.0, def4 = 0.0;         // part carried by the deflated block
-            double smin_defl = smax_lo;            // smallest deflated singular value (cancellation guard)
-            bool polished = true;                  // the block spans an invariant subspace to rounding
-            for (;;) {
-                // X carries a relative error of about eps * cond(R); what is left must stay well above it
-                // X carries a relative error of at most about c eps cond(R); add it to what is left, so the bound
-                // stays a lower bound (it merely becomes useless once cancellation has eaten the sums)
-                tail2 = T2 - def2;
-                const double noise = 2.2e-14 * (smax_hi / smin_defl);
-                const double up2 = fmax(tail2, 0.0) + noise * T2;
-                ok2 = tail2 > -noise * T2;                                   // a clearly negative remainder: inconsistent sums
-                double lb = ok2 ? 1.0 / sqrt(up2) : 0.0;                     // s_next >= lb
-                bool done = lb >= P.rank_tol * smax_hi * (1.0 + 1e-3);
-                if (!done) {                                                 // sharpen with the fourth-power sum
-                    if (!have4) { T4 = xxt_norm4_mma(W, rinv, ld, p, lane); have4 = true; }
-                    tail4 = T4 - def4;
-                    const double up4 = fmax(tail4, 0.0) + 4.0 * noise * T4;
-                    ok4 = tail4 > -4.0 * noise * T4;
-                    lb = fmax(lb, ok4 ? 1.0 / sqrt(sqrt(up4)) : 0.0);
-                    done = lb >= P.rank_tol * smax_hi * (1.0 + 1e-3);
-                }
-                if (!done && m > 0 && polished && ey_m != m) {               // scalar sums exhausted: explicit deflation of X
-                    ey_m = m;
-                    if (!left_fresh) { build_left_basis(); left_fresh = true; }
-                    double e2x;
-                    if (m <= 1) e2x = deflated_inverse_norm2<PS, 1>(W, rinv, ld, p, Ws, pmax, m, lane);
-                    else if (m <= 2) e2x = deflated_inverse_norm2<PS, 2>(W, rinv, ld, p, Ws, pmax, m, lane);
-                    else if (m <= 4) e2x = deflated_inverse_norm2<PS, 4>(W, rinv, ld, p, Ws, pmax, m, lane);
-                    else if (m <= 8) e2x = deflated_inverse_norm2<PS, 8>(W, rinv, ld, p, Ws, pmax, m, lane);
-                    else e2x = deflated_inverse_norm2<PS, REG_MAXDEFL_CAP>(W, rinv, ld, p, Ws, pmax, m, lane);
-                    // X carries a relative error of about noise: sigma(X_exact) <= sigma(X_computed) / (1 - noise)
-                    if (noise < 0.25 && e2x > 0.0) {
-                        lb = fmax(lb, (1.0 - noise) / sqrt(e2x));
-                        done = lb >= P.rank_tol * smax_hi * (1.0 + 1e-3);
-                    }
-                }
-                if (done && polished) break;                                 // nothing (left) to truncate
-                if (done || (!polished && m >= P.maxdefl)) {                 // verify / sharpen the block first
-                    left_fresh = false;                                      // polish uses Ws as scratch
-                    const int pr = polish(def2, def4);
-                    if (pr) { fallback = true; why = 5 + pr; break; }
-                    polished = true;
-                    if (!done && m >= P.maxdefl) { fallback = true; why = 3; break; }
-                    continue;
-                }
-                if (m >= P.maxdefl) { fallback = true; why = 3; break; }
-                if (power_done == 0) power(2);   // two steps put the lower bound of s_max within a few per cent
-                Vec<PS> z, yt;
-                double zMz, Mz2;
-                const int found = probe(seed++, z, zMz, Mz2, yt);
-                if (found) {
-                    // s = 1 / |R^-T z| (an upper bound of the singular value, like |R z|, but tight to second order
-                    // in the error of z) and u = R^-T z / |R^-T z| from the last solve of the probe
-                    const double ny = sqrt(vdot<PS>(yt, yt));
-                    const double sv = 1.0 / ny;
-                    if (!(sv < P.rank_tol * smax_lo)) { fallback = true; why = 4; break; }
-                    vstore<PS>(Zs + m * pmax, z, p, lane);
-                    left_fresh = (m == 0 && found == 2);           // a single converged pair: Ws[0] = u is the left basis
-                    if (left_fresh) {
-#pragma unroll
-                        for (int t = 0; t < PS; ++t) yt.v[t] *= sv;
-                        vstore<PS>(Ws, yt, p, lane);
-                    }
-                    __syncwarp();
-                    ++m;
-                    smin_defl = fmin(smin_defl, sv);
-                    // triangular solves lose eps * cond digits: beyond cond ~ 5e9 the deflated subspace would be less
-                    // accurate than the reference's SVD -- let the Jacobi SVD handle those rows
-                    if (smax_hi > P.cond_max * smin_defl) { fallback = true; why = 5; break; }
-                    if (found == 2 && polished) { const double i2 = 1.0 / (sv * sv); def2 += i2; def4 += i2 * i2; }
-                    else { def2 += zMz; def4 += Mz2; polished = false; }
-                    continue;
-                }
-                if (!polished) {                                             // a loose block can hide what is left
-                    left_fresh = false;                                      // polish uses Ws as scratch
-                    const int pr = polish(def2, def4);
-                    if (pr) { fallback = true; why = 5 + pr; break; }
-                    polished = true;
-                    continue;
-                }
-                // inconclusive: maybe only because the bracket [lower bound, |R|_F] of s_max is wide --
-                // run the power iteration to convergence once and look again
-                if (!refined) {
-                    double prev = smax_lo, inc_old = 0.0;
-                    bool conv = false;
-                    for (int round = 0; round < 40 && !conv; ++round) {
-                        power(4);
-                        const double inc = smax_lo - prev;
-                        prev = smax_lo;
-                        // the Rayleigh estimate rises monotonically; with ratio qq per round the tail is inc qq/(1-qq)
-                        const double qq = inc_old > 0.0 ? inc / inc_old : 1.0;
-                        if (inc <= 3e-5 * smax_lo && qq < 0.9) { conv = true; smax_hi = smax_lo * (1.0 + 1e-6) + 10.0 * inc; }
-                        inc_old = inc;
-                    }
-                    refined = true;
-                    if (conv) continue;
-                }
-                fallback = true;                                             // the Jacobi SVD decides
-                why = (ok2 || ok4) ? 2 : 5;                                  // 2: certificate alive but inconclusive, 5: lost to cancellation
-                break;
-            }
-        }
-
-        if (!fallback) {
-            if (m > 0) flag |= 1 | 2;
-            if (!left_fresh) build_left_basis();
-            Vec<PS> b = vload<PS>(cvec, p, lane);
-            for (int mm = 0; mm < m; ++mm) {         // c -= X X^T c
-                const Vec<PS> xm = vload<PS>(Ws + mm * pmax, p, lane);
-                const double pr = vdot<PS>(b, xm);
-#pragma unroll
-                for (int t = 0; t < PS; ++t) b.v[t] -= pr * xm.v[t];
-            }
-            b = solve_upper<PS>(b, W, rinv, ld, p, lane);
-            for (int mm = 0; mm < m; ++mm) {
-                const Vec<PS> zm = vload<PS>(Zs + mm * pmax, p, lane);
-                const double pr = vdot<PS>(b, zm);
-#pragma unroll
-                for (int t = 0; t < PS; ++t) b.v[t] -= pr * zm.v[t];
-            }
-            vstore<PS>(aux, b, p, lane);
-            __syncwarp();
-        } else {
-            flag |= 1 | 16 | (why << 5);
-            unpack_rc<PS>(in, W, ld, p, K, lane);  // the lower triangle may hold X^T
-            __syncwarp();
-            double dropped2;
-            flag |= jacobi_solve(W, ld, K, p, P.rank_tol, rinv, tmp, aux, &dropped2, lane);
-        }
-
-        double *Tout = P.T + (int64_t)f * P.nnz + r0;
-        for (int j = lane; j < p; j += 32) Tout[j] = -aux[j];
-        // |y - A^T beta|^2 = e2 + |c - R beta|^2 ; the second term vanishes (to rounding) unless
-        // singular values were truncated, and is then evaluated explicitly from R, c and beta.
-        double rest2 = 0.0;
-        if (fallback || m > 0) {
-            if (fallback) { unpack_rc<PS>(in, W, ld, p, K, lane); __syncwarp(); }
-            const Vec<PS> b = vload<PS>(aux, p, lane);
-            const Vec<PS> rb = mul_upper<PS>(b, W, ld, p, lane);
-            const Vec<PS> c0 = vload<PS>(cvec, p, lane);
-#pragma unroll
-            for (int t = 0; t < PS; ++t) { const double df = c0.v[t] - rb.v[t]; rest2 += df * df; }
-            rest2 = warp_sum(rest2);
-        }
-        if (lane == 0) {
-            const double d = (e2 + rest2) / denom;
-            if (d < P.variance_floor) flag |= 8;
-            P.D[(int64_t)f * P.nloc + q] = fmax(d, P.variance_floor);
-            if (P.flags) P.flags[(int64_t)f * P.nloc + q] = flag | ((nsteps < 255 ? nsteps : 255) << 8);
-        }
-        __syncwarp();
-    }
-}
-
 template <int S>
 static cudaError_t launch_qr_t(const RegressParams &p, int grid, int warps, size_t smem, cudaStream_t s) {
     cudaError_t e = cudaFuncSetAttribute(regress_qr_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1526,19 +847,29 @@ static cudaError_t launch_qrm_t(const RegressParams &p, int grid, int warps, siz
 }
 
 template <int PS>
-static cudaError_t launch_solve_t(const RegressParams &p, int grid, int warps, size_t smem, cudaStream_t s) {
-    cudaError_t e = cudaFuncSetAttribute(regress_solve_kernel<PS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+static cudaError_t launch_clean_t(const RegressParams &p, int grid, int warps, size_t smem, cudaStream_t s) {
+    cudaError_t e = cudaFuncSetAttribute(regress_clean_kernel<PS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    regress_solve_kernel<PS><<<grid, warps * 32, smem, s>>>(p);
+    regress_clean_kernel<PS><<<grid, warps * 32, smem, s>>>(p);
     return cudaGetLastError();
 }
 
-// Launches K2a + K2b for fields [p.f0, p.f1).  p.counter points at two zero-initialised words.
+template <int PS>
+static cudaError_t launch_trunc_t(const RegressParams &p, int grid, int warps, size_t smem, cudaStream_t s) {
+    cudaError_t e = cudaFuncSetAttribute(regress_trunc_kernel<PS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    regress_trunc_kernel<PS><<<grid, warps * 32, smem, s>>>(p);
+    return cudaGetLastError();
+}
+
+// Launches K2a + K2b-1 + K2b-2 for fields [p.f0, p.f1).  p.counter: two words, p.lcounter: three words (zeroed here).
 cudaError_t launch_regress(const RegressParams &p_in, int sm_count, size_t smem_limit, cudaStream_t s, cudaEvent_t mid) {
     if (p_in.nwork == 0) return cudaSuccess;
-    if (p_in.pmax > 96) return cudaErrorInvalidConfiguration;
+    if (p_in.pmax > 128) return cudaErrorInvalidConfiguration;
     RegressParams p = p_in;
     cudaError_t e = cudaMemsetAsync(p.counter, 0, 2 * sizeof(unsigned int), s);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(p.lcounter, 0, 3 * sizeof(unsigned int), s);
     if (e != cudaSuccess) return e;
     // K2a
     const int S = (p.N + 31) / 32;
@@ -1585,32 +916,37 @@ cudaError_t launch_regress(const RegressParams &p_in, int sm_count, size_t smem_
         if (e != cudaSuccess) return e;
     }
     if (mid) { e = cudaEventRecord(mid, s); if (e != cudaSuccess) return e; }
-    // K2b
+    // K2b-1: certificate + plain solve; rows that (may) truncate are listed for K2b-2
     {
-        int warps = (int)(smem_limit / (regress_solve_ws_doubles(p.pmax, 1) * sizeof(double)));
+        const size_t ws = regress_clean_ws_doubles(p.pmax) * sizeof(double);
+        int warps = (int)(smem_limit / ws);
         if (warps < 1) return cudaErrorInvalidConfiguration;
         if (warps > 16) warps = 16;
-        // deflation vectors: as many (<= 12) as fit while giving up at most two resident warps
-        const int warps1 = warps;
-        p.maxdefl = 1;
-        while (p.maxdefl < REG_MAXDEFL_CAP) {
-            const int wn = (int)(smem_limit / (regress_solve_ws_doubles(p.pmax, p.maxdefl + 1) * sizeof(double)));
-            if (wn < 1 || wn < std::min(warps1, 16) - 2) break;
-            ++p.maxdefl;
-        }
-        p.cond_max = 5e9;
-        if (const char *cenv = getenv("ENKFMC_K2B_CONDMAX")) { const double cv = atof(cenv); if (cv >= 1.0) p.cond_max = cv; }
-        if (const char *denv = getenv("ENKFMC_K2B_MAXDEFL")) { const int dv = atoi(denv); if (dv >= 1 && dv <= REG_MAXDEFL_CAP) p.maxdefl = dv; }
-        warps = (int)(smem_limit / (regress_solve_ws_doubles(p.pmax, p.maxdefl) * sizeof(double)));
-        if (warps > 16) warps = 16;
-        if (const char *wenv = getenv("ENKFMC_K2B_WARPS")) { const int wv = atoi(wenv); if (wv >= 1 && wv < warps) warps = wv; }
-        const size_t ws = regress_solve_ws_doubles(p.pmax, p.maxdefl) * sizeof(double);
         int64_t grid = sm_count;
         const int64_t need = (p.nwork + warps - 1) / warps;
         if (grid > need) grid = need;
-        if (p.pmax <= 32) e = launch_solve_t<1>(p, (int)grid, warps, ws * warps, s);
-        else if (p.pmax <= 64) e = launch_solve_t<2>(p, (int)grid, warps, ws * warps, s);
-        else e = launch_solve_t<3>(p, (int)grid, warps, ws * warps, s);
+        if (p.pmax <= 32) e = launch_clean_t<1>(p, (int)grid, warps, ws * warps, s);
+        else if (p.pmax <= 64) e = launch_clean_t<2>(p, (int)grid, warps, ws * warps, s);
+        else if (p.pmax <= 96) e = launch_clean_t<3>(p, (int)grid, warps, ws * warps, s);
+        else e = launch_clean_t<4>(p, (int)grid, warps, ws * warps, s);
+        if (e != cudaSuccess) return e;
+    }
+    // K2b-2: block size by the predecessor count (the number of sub-threshold singular values grows with it), reduced
+    // until at least one warp fits
+    {
+        p.bmax = p.pmax < 8 ? 0 : p.pmax <= 16 ? 8 : p.pmax <= 48 ? 16 : p.pmax <= 64 ? 24 : 32;
+        if (const char *benv = getenv("ENKFMC_K2B_BMAX")) { const int bv = atoi(benv); if (bv >= 8 && bv <= 32) p.bmax = bv & ~7; }
+        while (p.bmax > 8 && regress_trunc_ws_doubles(p.pmax, p.bmax) * sizeof(double) > smem_limit) p.bmax -= 8;
+        const size_t ws = regress_trunc_ws_doubles(p.pmax, p.bmax) * sizeof(double);
+        int warps = (int)(smem_limit / ws);
+        if (warps < 1) return cudaErrorInvalidConfiguration;
+        if (warps > 8) warps = 8;
+        if (const char *wenv = getenv("ENKFMC_K2B_WARPS")) { const int wv = atoi(wenv); if (wv >= 1 && wv < warps) warps = wv; }
+        const int64_t grid = sm_count;                       // the list length is known on the device only
+        if (p.pmax <= 32) e = launch_trunc_t<1>(p, (int)grid, warps, ws * warps, s);
+        else if (p.pmax <= 64) e = launch_trunc_t<2>(p, (int)grid, warps, ws * warps, s);
+        else if (p.pmax <= 96) e = launch_trunc_t<3>(p, (int)grid, warps, ws * warps, s);
+        else e = launch_trunc_t<4>(p, (int)grid, warps, ws * warps, s);
     }
     return e;
 }
