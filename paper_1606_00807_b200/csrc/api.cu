@@ -115,8 +115,8 @@ int ensure_device(enkfmc_plan *p) {
         d->band_stride = bp.back();
         if ((rc = upload(d->band_ptr, bp))) return rc;
     }
-    CK(cudaMalloc(&d->counters, 8 * sizeof(unsigned int)));
-    CK(cudaMemset(d->counters, 0, 8 * sizeof(unsigned int)));
+    CK(cudaMalloc(&d->counters, 16 * sizeof(unsigned int)));
+    CK(cudaMemset(d->counters, 0, 16 * sizeof(unsigned int)));
     for (auto &ev : d->ev) CK(cudaEventCreate(&ev));
     CK(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&d->copy_stream, cudaStreamNonBlocking));
@@ -220,7 +220,7 @@ int do_regress(enkfmc_plan *p, const double *d_U, int64_t nens, double rank_tol,
     R.nwork = (int64_t)p->regress_order.size() * p->nfields;
     R.row_ptr = d->row_ptr; R.pred_state = d->pred_state; R.state_row = d->state_row; R.work_order = d->regress_order;
     R.rank_tol = rank_tol; R.variance_floor = floor_; R.fast_ratio = 1e-6;
-    R.T = d_T; R.D = d_D; R.flags = d_flags; R.counter = d->counters; R.lcounter = d->counters + 4;
+    R.T = d_T; R.D = d_D; R.flags = d_flags; R.counter = d->counters; R.lcounter = d->counters + 8;
     R.rq_ptr = d->rq_ptr; R.rq_stride = d->rq_stride;
     // QR scratch: as many fields per launch pair as fit in the budget (default 16 GiB)
     const int64_t budget = (int64_t)16 << 30;
@@ -234,10 +234,11 @@ int do_regress(enkfmc_plan *p, const double *d_U, int64_t nens, double rank_tol,
     const int64_t list_need = (int64_t)p->regress_order.size() * chunk;
     if (!d->worklist || d->worklist_alloc < list_need) {
         release(d->worklist);
-        CK(cudaMalloc(&d->worklist, std::max<size_t>((size_t)list_need, 1) * sizeof(unsigned int)));
+        CK(cudaMalloc(&d->worklist, std::max<size_t>((size_t)list_need, 1) * 2 * sizeof(unsigned int)));
         d->worklist_alloc = list_need;
     }
     R.worklist = d->worklist;
+    R.worklist2 = d->worklist + std::max<int64_t>(list_need, 1);
     for (int64_t f0 = fbeg; f0 < fend; f0 += chunk) {
         R.f0 = (int)f0;
         R.f1 = (int)std::min<int64_t>(fend, f0 + chunk);
@@ -250,7 +251,7 @@ int do_regress(enkfmc_plan *p, const double *d_U, int64_t nens, double rank_tol,
             return ENKFMC_E_CAPACITY;
         }
         CK(e);
-        if (R.nwork > 0) p->counters[0] += 3;
+        if (R.nwork > 0) p->counters[0] += 4;
     }
     if (!p->alias_row.empty()) {   // copy each distinct regression to the other tiles holding the same row
         CK(launch_replicate_rows(d->alias_row, d->alias_rep, (int64_t)p->alias_row.size(), d->row_ptr, fend - fbeg,

@@ -862,14 +862,14 @@ static cudaError_t launch_trunc_t(const RegressParams &p, int grid, int warps, s
     return cudaGetLastError();
 }
 
-// Launches K2a + K2b-1 + K2b-2 for fields [p.f0, p.f1).  p.counter: two words, p.lcounter: three words (zeroed here).
+// Launches K2a + K2b-1 + K2b-2 for fields [p.f0, p.f1).  p.counter: two words, p.lcounter: five words (zeroed here).
 cudaError_t launch_regress(const RegressParams &p_in, int sm_count, size_t smem_limit, cudaStream_t s, cudaEvent_t mid) {
     if (p_in.nwork == 0) return cudaSuccess;
     if (p_in.pmax > 128) return cudaErrorInvalidConfiguration;
     RegressParams p = p_in;
     cudaError_t e = cudaMemsetAsync(p.counter, 0, 2 * sizeof(unsigned int), s);
     if (e != cudaSuccess) return e;
-    e = cudaMemsetAsync(p.lcounter, 0, 3 * sizeof(unsigned int), s);
+    e = cudaMemsetAsync(p.lcounter, 0, 5 * sizeof(unsigned int), s);
     if (e != cudaSuccess) return e;
     // K2a
     const int S = (p.N + 31) / 32;
@@ -931,22 +931,31 @@ cudaError_t launch_regress(const RegressParams &p_in, int sm_count, size_t smem_
         else e = launch_clean_t<4>(p, (int)grid, warps, ws * warps, s);
         if (e != cudaSuccess) return e;
     }
-    // K2b-2: block size by the predecessor count (the number of sub-threshold singular values grows with it), reduced
-    // until at least one warp fits
+    // K2b-2, two passes: small blocks at high occupancy first; rows whose block has to grow beyond that are handed to a
+    // second pass with room for up to 32 vectors (the number of sub-threshold singular values grows with the predecessor
+    // count).  The list lengths are known on the device only: both passes are always launched.
     {
-        p.bmax = p.pmax < 8 ? 0 : p.pmax <= 16 ? 8 : p.pmax <= 48 ? 16 : p.pmax <= 64 ? 24 : 32;
-        if (const char *benv = getenv("ENKFMC_K2B_BMAX")) { const int bv = atoi(benv); if (bv >= 8 && bv <= 32) p.bmax = bv & ~7; }
-        while (p.bmax > 8 && regress_trunc_ws_doubles(p.pmax, p.bmax) * sizeof(double) > smem_limit) p.bmax -= 8;
-        const size_t ws = regress_trunc_ws_doubles(p.pmax, p.bmax) * sizeof(double);
-        int warps = (int)(smem_limit / ws);
-        if (warps < 1) return cudaErrorInvalidConfiguration;
-        if (warps > 8) warps = 8;
-        if (const char *wenv = getenv("ENKFMC_K2B_WARPS")) { const int wv = atoi(wenv); if (wv >= 1 && wv < warps) warps = wv; }
-        const int64_t grid = sm_count;                       // the list length is known on the device only
-        if (p.pmax <= 32) e = launch_trunc_t<1>(p, (int)grid, warps, ws * warps, s);
-        else if (p.pmax <= 64) e = launch_trunc_t<2>(p, (int)grid, warps, ws * warps, s);
-        else if (p.pmax <= 96) e = launch_trunc_t<3>(p, (int)grid, warps, ws * warps, s);
-        else e = launch_trunc_t<4>(p, (int)grid, warps, ws * warps, s);
+        const int b1 = p.pmax < 8 ? 0 : p.pmax <= 48 ? 8 : 16;
+        int b2 = p.pmax < 8 ? 0 : p.pmax <= 16 ? 8 : p.pmax <= 64 ? 24 : 32;
+        if (const char *benv = getenv("ENKFMC_K2B_BMAX")) { const int bv = atoi(benv); if (bv >= 8 && bv <= 32) b2 = bv & ~7; }
+        while (b2 > 8 && regress_trunc_ws_doubles(p.pmax, b2) * sizeof(double) > smem_limit) b2 -= 8;
+        for (int level = 0; level < 2; ++level) {
+            p.level = level;
+            p.bmax = level == 0 ? std::min(b1, b2) : b2;
+            p.bmax2 = b2;
+            if (level == 1 && b2 <= std::min(b1, b2)) break;     // nothing is ever escalated
+            const size_t ws = regress_trunc_ws_doubles(p.pmax, p.bmax) * sizeof(double);
+            int warps = (int)(smem_limit / ws);
+            if (warps < 1) return cudaErrorInvalidConfiguration;
+            if (warps > 8) warps = 8;
+            if (const char *wenv = getenv("ENKFMC_K2B_WARPS")) { const int wv = atoi(wenv); if (wv >= 1 && wv < warps) warps = wv; }
+            const int64_t grid = sm_count;
+            if (p.pmax <= 32) e = launch_trunc_t<1>(p, (int)grid, warps, ws * warps, s);
+            else if (p.pmax <= 64) e = launch_trunc_t<2>(p, (int)grid, warps, ws * warps, s);
+            else if (p.pmax <= 96) e = launch_trunc_t<3>(p, (int)grid, warps, ws * warps, s);
+            else e = launch_trunc_t<4>(p, (int)grid, warps, ws * warps, s);
+            if (e != cudaSuccess) return e;
+        }
     }
     return e;
 }

@@ -269,11 +269,11 @@ __device__ __forceinline__ void blk_solve(bool transposed, double *B, int ZP, in
 // triangular, element (l, k) at G[k * GP + l], with B_in[:, k] = sum_l G[l, k] B_out[:, l].  Returns false on
 // breakdown (a column vanished or is not finite).
 template <int PS>
-__device__ __noinline__ bool orth_block(double *B, int ZP, int c0, int b, int p, double *G, int GP, int lane) {
+__device__ __noinline__ bool orth_block(double *B, int ZP, int c0, int b, int p, double *G, int GP, int lane, int passes = 2) {
     for (int k = c0; k < b; ++k) {
         Vec<PS> v = vload<PS>(B + (size_t)k * ZP, p, lane);
 #pragma unroll 1
-        for (int pass = 0; pass < 2; ++pass) {
+        for (int pass = 0; pass < passes; ++pass) {
             for (int l0 = 0; l0 < k; l0 += 4) {
                 Vec<PS> q[4];
                 double d[4];
@@ -314,6 +314,67 @@ __device__ __noinline__ bool orth_block(double *B, int ZP, int c0, int b, int p,
     return true;
 }
 
+// Rotation (cs, sn) that orthogonalises the row pair x, y with x.y = g, |x|^2 = da, |y|^2 = db:
+// x' = cs x - sn y, y' = sn x + cs y.  tan = sgn(tau) g / (|tau| + sqrt(tau^2 + g^2)), tau = (db - da) / 2, evaluated with
+// reciprocal square roots and one reciprocal (no division / square-root sequences).
+__device__ __forceinline__ void jacobi_rotation(double g, double da, double db, double &cs, double &sn) {
+    const double tau = 0.5 * (db - da);
+    const double h2 = fma(tau, tau, g * g);
+    const double r = h2 * rsqrt(h2);
+    const double t = (tau >= 0.0 ? g : -g) * __drcp_rn(fabs(tau) + r);
+    cs = rsqrt(fma(t, t, 1.0));
+    sn = cs * t;
+}
+
+// The same on an 8 x 16 matrix held in registers: lane (r, t4) = (lane >> 2, lane & 3) owns M[r][t4 + 4 j], j < 4;
+// the first eight columns enter the inner products.  Four disjoint row pairs rotate at a time (round robin).
+__device__ __noinline__ int jacobi8_regs(double *W, int ld, int lane) {
+    const int r = lane >> 2, t4 = lane & 3;
+    double m[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) m[j] = W[(size_t)(t4 + 4 * j) * ld + r];
+    const double tol2 = 8.0 * DBL_EPSILON * DBL_EPSILON;
+    int sweep = 0;
+    bool rotated = true;
+    while (rotated && sweep < JACOBI_MAX_SWEEPS) {
+        rotated = false;
+        ++sweep;
+#pragma unroll 1
+        for (int rr = 0; rr < 7; ++rr) {
+            int partner;
+            if (r == 7) partner = rr;
+            else if (r == rr) partner = 7;
+            else {
+                const int d = (r - rr + 7) % 7;
+                partner = d <= 3 ? (rr - d + 7) % 7 : (rr + 7 - d) % 7;
+            }
+            const bool isx = r < partner;                   // the pair's lower row plays x
+            double pm[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) pm[j] = __shfl_sync(FULL, m[j], 4 * partner + t4);
+            double g = fma(m[1], pm[1], m[0] * pm[0]);
+            double dm = fma(m[1], m[1], m[0] * m[0]);
+            double dp = fma(pm[1], pm[1], pm[0] * pm[0]);
+            g += __shfl_xor_sync(FULL, g, 1); dm += __shfl_xor_sync(FULL, dm, 1); dp += __shfl_xor_sync(FULL, dp, 1);
+            g += __shfl_xor_sync(FULL, g, 2); dm += __shfl_xor_sync(FULL, dm, 2); dp += __shfl_xor_sync(FULL, dp, 2);
+            const double da = isx ? dm : dp, db = isx ? dp : dm;
+            const bool rot = (g * g > tol2 * da * db) && (g != 0.0);
+            if (rot) {
+                double cs, sn;
+                jacobi_rotation(g, da, db, cs, sn);
+                const double sg = isx ? -sn : sn;          // x' = cs x - sn y ; y' = cs y + sn x
+#pragma unroll
+                for (int j = 0; j < 4; ++j) m[j] = fma(sg, pm[j], cs * m[j]);
+            }
+            if (__any_sync(FULL, rot)) rotated = true;
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) W[(size_t)(t4 + 4 * j) * ld + r] = m[j];
+    __syncwarp();
+    return (sweep >= JACOBI_MAX_SWEEPS && rotated) ? JACOBI_MAX_SWEEPS + 1 : sweep;
+}
+
 // One-sided Jacobi on the rows of a K x na matrix (column-major, pitch ld): plane rotations of row pairs until the
 // first nd columns of all rows are mutually orthogonal; the rotations act on all na columns.  Returns the sweeps
 // used (JACOBI_MAX_SWEEPS + 1 if not converged).
@@ -343,11 +404,10 @@ __device__ __noinline__ int jacobi_rows(double *W, int ld, int K, int nd, int na
                     g += x * y; da += x * x; db += y * y;
                 }
                 g = group_sum(g, T); da = group_sum(da, T); db = group_sum(db, T);
-                const bool rot = on && (fabs(g) > tolj * sqrt(da * db)) && (g != 0.0);
+                const bool rot = on && (g * g > tolj * tolj * da * db) && (g != 0.0);
                 if (rot) {
-                    const double zeta = (db - da) / (2.0 * g);
-                    const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-                    const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+                    double cs, sn;
+                    jacobi_rotation(g, da, db, cs, sn);
                     double *wa = W + a, *wb = W + b;
                     for (int c = sub; c < na; c += T) {
                         const double x = wa[(size_t)c * ld], y = wb[(size_t)c * ld];
@@ -581,14 +641,15 @@ __global__ void __launch_bounds__(256, 1) regress_trunc_kernel(const RegressPara
     double *Gs = Ys + (size_t)bmax * ZP;        // [G | P]: bmax x 2 bmax, pitch GP
     const double denom = (double)(N - 1);
     const unsigned nf = (unsigned)(P.f1 - P.f0);
-    const unsigned nlist = P.lcounter[0];
+    const unsigned nlist = P.lcounter[P.level ? 3 : 0];
+    const unsigned int *list = P.level ? P.worklist2 : P.worklist;
 
     for (;;) {
         unsigned int it = 0;
-        if (lane == 0) it = atomicAdd(P.lcounter + 1, 1u);
+        if (lane == 0) it = atomicAdd(P.lcounter + (P.level ? 4 : 1), 1u);
         it = __shfl_sync(FULL, it, 0);
         if (it >= nlist) break;
-        const unsigned wk = P.worklist[it];
+        const unsigned wk = list[it];
         const int q = P.work_order[wk / nf];
         const int fl = (int)(wk % nf), f = P.f0 + fl;
         const int64_t r0 = P.row_ptr[q];
@@ -599,6 +660,7 @@ __global__ void __launch_bounds__(256, 1) regress_trunc_kernel(const RegressPara
         const double *in = P.Rq + (int64_t)fl * P.rq_stride + P.rq_ptr[q];
         const double e2 = in[packed_col_offset(p, K) + K];
         int flag = 1, why = 0, sweeps = 0, b = 8;
+        bool escalate = false;
         unsigned tmask = 0;                      // Ritz values below the threshold
         double fro2 = 0.0, smax_lo = 0.0;
 
@@ -673,26 +735,39 @@ __global__ void __launch_bounds__(256, 1) regress_trunc_kernel(const RegressPara
             fill_random(0, b);
             const int bcap = bmax < (pe & ~7) ? bmax : (pe & ~7);
             int need = 2;
+            bool final_done = false, wide_span = true;
             for (;;) {
                 ++sweeps;
+                // one Gram-Schmidt pass keeps the block well conditioned as long as its Ritz values span less than ~1e6 (what a
+                // single pass leaves of the dominant direction is amplified by that ratio in the next solve); the first sweep
+                // (span unknown) and the predicted last one (the accurate one) take two
+                const int passes = (sweeps >= need || sweeps == 1 || wide_span) ? 2 : 1;
                 blk_copy(Ys, Zs, ZP, b, lane);
                 blk_solve(true, Ys, ZP, b, W, rinv, ld, pe, lane);                    // Y = R^-T Z
-                if (!orth_block<PS>(Ys, ZP, 0, b, pe, nullptr, GP, lane)) { fallback = true; why = 1; break; }
+                if (!orth_block<PS>(Ys, ZP, 0, b, pe, nullptr, GP, lane, passes)) { fallback = true; why = 1; break; }
                 blk_copy(Zs, Ys, ZP, b, lane);
                 blk_solve(false, Zs, ZP, b, W, rinv, ld, pe, lane);                   // Z G = R^-1 Y
-                if (!orth_block<PS>(Zs, ZP, 0, b, pe, Gs, GP, lane)) { fallback = true; why = 1; break; }
+                if (!orth_block<PS>(Zs, ZP, 0, b, pe, Gs, GP, lane, passes)) { fallback = true; why = 1; break; }
+                final_done = passes == 2;
                 // 1 / |G_kk| estimate the Ritz values of the block; the largest is at least 1 / min |G_kk|
                 double gk = lane < b ? fabs(Gs[(size_t)lane * GP + lane]) : DBL_MAX;
                 const double top = 1.0 / warp_min(gk);
+                wide_span = warp_max(lane < b ? gk : 0.0) * top > 1e6;
                 if (top < 8.0 * thr_hi) {                                            // the block does not reach far enough
                     if (b + 8 > bcap) {
                         if (b == pe) break;                                           // the block is the whole space
+                        if (P.level == 0 && b + 8 <= (pe & ~7) && P.bmax2 > bmax) {    // the second pass has room for it
+                            if (lane == 0) P.worklist2[atomicAdd(P.lcounter + 3, 1u)] = wk;
+                            escalate = true;
+                            break;
+                        }
                         fallback = true; why = 2; break;
                     }
                     fill_random(b, b + 8);
                     if (!orth_block<PS>(Zs, ZP, b, b + 8, pe, nullptr, GP, lane)) { fallback = true; why = 1; break; }
                     b += 8;
                     need = sweeps + 2;
+                    final_done = false;
                     continue;
                 }
                 const double est = lane < b ? 1.0 / gk : 0.0;
@@ -703,10 +778,11 @@ __global__ void __launch_bounds__(256, 1) regress_trunc_kernel(const RegressPara
                     if (n > TRUNC_MAX_SWEEPS) n = TRUNC_MAX_SWEEPS;
                     if (n > need) need = n;
                 }
-                if (sweeps >= need) break;
+                if (sweeps >= need && final_done) break;
                 if (sweeps >= TRUNC_MAX_SWEEPS + 4) { fallback = true; why = 4; break; }
             }
         }
+        if (escalate) continue;
         double sig = 0.0;                            // lane k: Ritz value k
         if (!fallback) {
             // ---- Rayleigh-Ritz: G = P S Q^T by one-sided Jacobi on the rows of [G | I] ----
@@ -716,7 +792,7 @@ __global__ void __launch_bounds__(256, 1) regress_trunc_kernel(const RegressPara
                 else Gs[e] = (r == c - b) ? 1.0 : 0.0;
             }
             __syncwarp();
-            const int js = jacobi_rows(Gs, GP, b, b, 2 * b, lane);
+            const int js = b == 8 ? jacobi8_regs(Gs, GP, lane) : jacobi_rows(Gs, GP, b, b, 2 * b, lane);
             flag |= (js > 63 ? 63 : js) << 16;
             if (js > JACOBI_MAX_SWEEPS) { fallback = true; why = 1; }
             double s2 = 0.0;
@@ -735,10 +811,12 @@ __global__ void __launch_bounds__(256, 1) regress_trunc_kernel(const RegressPara
                 return __any_sync(FULL, amb);
             };
             if (ambiguous()) {
-                // power iteration on R^T R (p_e-vector), from the all-ones vector; the estimate rises monotonically
+                // power iteration on R^T R (p_e-vector) from the normalised all-ones vector: every Rayleigh estimate is a
+                // lower bound of s_max and they rise monotonically
                 Vec<PS> v;
+                const double v0 = rsqrt((double)pe);
 #pragma unroll
-                for (int t = 0; t < PS; ++t) v.v[t] = (lane + 32 * t < pe) ? 1.0 : 0.0;
+                for (int t = 0; t < PS; ++t) v.v[t] = (lane + 32 * t < pe) ? v0 : 0.0;
                 double prev = 0.0, inc_old = 0.0;
                 for (int round = 0; round < 60; ++round) {
                     Vec<PS> y = wide ? mul_upper_t<PS>(v, W, ld, pe, lane) : mul_upper<PS>(v, W, ld, pe, lane);
@@ -748,17 +826,14 @@ __global__ void __launch_bounds__(256, 1) regress_trunc_kernel(const RegressPara
                     const double inv = 1.0 / nv;
 #pragma unroll
                     for (int t = 0; t < PS; ++t) v.v[t] *= inv;
-                    if (round == 0) { prev = cur; continue; }                         // first pass starts unnormalised
                     smax_lo = fmax(smax_lo, cur);
                     const double inc = cur - prev;
                     prev = cur;
-                    // the Rayleigh estimate rises monotonically; with ratio qq per step the tail is inc qq / (1 - qq)
+                    // with ratio qq per step the tail of the increments is inc qq / (1 - qq)
                     const double qq = inc_old > 0.0 ? inc / inc_old : 1.0;
-                    if (round >= 2 && qq < 0.9) {
-                        smax_hi = fmin(fro, smax_lo * (1.0 + 1e-7) + 10.0 * inc * qq / (1.0 - qq));
-                        if (!ambiguous()) break;
-                        if (inc <= 1e-10 * cur) break;                                // converged: what is still inside is at the threshold
-                    }
+                    if (round >= 2 && qq < 0.9) smax_hi = fmin(fro, smax_lo * (1.0 + 1e-7) + 10.0 * inc * qq / (1.0 - qq));
+                    if (!ambiguous()) break;
+                    if (round >= 2 && qq < 0.9 && inc <= 1e-10 * cur) break;          // converged: what is still inside is at the threshold
                     inc_old = inc;
                 }
                 if (ambiguous()) { fallback = true; why = 3; }

@@ -329,9 +329,16 @@ def test_wide_regressions_and_long_local_domains(mck):
     ring = mck.GridGeometry("ring1d", n)
     with pytest.raises(mck.CapacityError):
         mck.analysis_primal(mck.EnsembleState(X), mck.fit_factors(orc.center_rows(X), ring, zeta), net, Ys)
-    # zeta = 7 would need 112 predecessors: refused, not truncated
+    # zeta = 7: 112 predecessors (up to 128 are supported), against the oracle
+    geo7 = mck.GridGeometry("grid2d", 18, 16)
+    U7 = orc.center_rows(rng.standard_normal((18 * 16, 130)))
+    f7 = mck.fit_factors(U7, geo7, 7)
+    o7 = orc.fit_factors(U7, orc.Grid(18, 16), 7)
+    assert np.array_equal(f7.lower.indices, o7.indices)
+    assert relerr(f7.lower.data, o7.data) < 1e-9 and np.max(np.abs(f7.variances - o7.d) / o7.d) < 1e-9
+    # zeta = 8 would need 144 predecessors: refused, not truncated
     with pytest.raises(mck.CapacityError):
-        mck.fit_factors(orc.center_rows(rng.standard_normal((30 * 30, 130))), mck.GridGeometry("grid2d", 30, 30), 7)
+        mck.fit_factors(orc.center_rows(rng.standard_normal((30 * 30, 150))), mck.GridGeometry("grid2d", 30, 30), 8)
 
 
 def test_wide_band_and_tiny_problems(mck):

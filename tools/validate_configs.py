@@ -35,6 +35,17 @@ def run(name, w, oracle_fields):
     T = device.workspace_tensor(plan, 1, (plan.nfields, plan.nnz))
     D = device.workspace_tensor(plan, 2, (plan.nfields, plan.sum_nlocal))
     flags = device.workspace_tensor(plan, 3, (plan.nfields, plan.sum_nlocal), "i32")
+    fl = plan.work(w.nens)
+    nrow = flags.size
+    if not oracle_fields:
+        sw = (flags >> 8) & 255
+        tr = (flags & 1) > 0
+        print(f"| {name} | {w.nstate} | {w.nens} | {w.zeta} | - | - | - | - | "
+              f"{100 * ((flags & 2) > 0).sum() / nrow:.1f} | {100 * ((flags & 16) > 0).sum() / nrow:.2f} | {100 * ((flags & 8) > 0).sum() / nrow:.1f} | "
+              f"{ms[1] + ms[2]:.2f} | {ms[3]:.2f} | {w.nstate / (ms.sum() * 1e-3) / 1e6:.2f} | {fl[2] / (ms[1] + ms[2]) / 1e9:.2f} | {fl[1] / ms[3] / 1e9:.2f} | "
+              f"no oracle; K2a {ms[1]:.2f} K2b {ms[2]:.2f} ms; listed {100 * tr.mean():.1f} %, sweeps mean {sw[tr].mean() if tr.any() else 0:.2f} max {sw.max()}, "
+              f"block/8 hist {np.bincount(((flags >> 22) & 7)[tr]).tolist() if tr.any() else []}, why hist {np.bincount(((flags >> 5) & 7)[(flags & 16) > 0]).tolist()} |", flush=True)
+        return
     grid = orc.Grid(w.nx, w.ny, True, w.boundary == "periodic", w.nfields)
     t0 = time.perf_counter()
     ref, kept = orc.assimilate(w.X, w.obs_indices, w.r_diag, w.Ys, grid, w.delta, w.zeta, keep_tiles=True,
@@ -50,8 +61,6 @@ def run(name, w, oracle_fields):
         derr = max(derr, np.max(np.abs(D[f] - dref) / dref))
         sl = slice(f * w.n2d, (f + 1) * w.n2d)
         xerr = max(xerr, np.linalg.norm(Xa[sl] - ref[sl]) / np.linalg.norm(ref[sl]))
-    fl = plan.work(w.nens)
-    nrow = flags.size
     print(f"| {name} | {w.nstate} | {w.nens} | {w.zeta} | {'yes' if maps_ok else 'NO'} | {terr:.1e} | {derr:.1e} | {xerr:.1e} | "
           f"{100 * ((flags & 2) > 0).sum() / nrow:.1f} | {100 * ((flags & 16) > 0).sum() / nrow:.2f} | {100 * ((flags & 8) > 0).sum() / nrow:.1f} | "
           f"{ms[1] + ms[2]:.2f} | {ms[3]:.2f} | {w.nstate / (ms.sum() * 1e-3) / 1e6:.2f} | {fl[2] / (ms[1] + ms[2]) / 1e9:.2f} | {fl[1] / ms[3] / 1e9:.2f} | "
@@ -60,10 +69,15 @@ def run(name, w, oracle_fields):
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--which", default="cfg1,cfg1p,cfg2,cfg2n,cfg4,cfg3,cfg3n,cfg5")
+ap.add_argument("--no-oracle", action="store_true")
+ap.add_argument("--fields", type=int, default=None)
 a = ap.parse_args()
 print("| config | n_state | N | zeta | maps bit-exact | T err (norm-wise) | D err (max rel) | Xa err (norm-wise) | rows truncated % | "
       "Jacobi fallback % | D at floor % | K2 ms | K3 ms | Mpts/s | K2 TF/s | K3 TF/s | oracle sample |")
 print("|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|")
+_run = run
+def run(name, w, fields):
+    return _run(name, w, [] if a.no_oracle else fields)
 for which in a.which.split(","):
     if which == "cfg1":
         run("cfg1 clipped", synthetic.config("cfg1"), [0])
@@ -78,8 +92,8 @@ for which in a.which.split(","):
             run(f"cfg4 r={z}", synthetic.config("cfg4", zeta=z), [0])
         run("cfg4 r=5 + 1% nugget", synthetic.config("cfg4", zeta=5, nugget=0.01), [0])
     elif which == "cfg3":
-        run("cfg3 (29 fields)", synthetic.config("cfg3"), [0, 14, 28])
+        run("cfg3 (29 fields)", synthetic.config("cfg3", fields=a.fields), [0, 14, 28] if a.fields is None else [0])
     elif which == "cfg3n":
         run("cfg3 + 1% nugget", synthetic.config("cfg3", nugget=0.01), [0, 28])
     elif which == "cfg5":
-        run("cfg5 (8 of 40 fields)", synthetic.config("cfg5", fields=8), [0])
+        run(f"cfg5 ({a.fields or 8} of 40 fields)", synthetic.config("cfg5", fields=a.fields or 8), [0])
