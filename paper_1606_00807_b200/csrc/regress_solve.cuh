@@ -5,9 +5,11 @@
 //
 //  regress_clean_kernel (K2b-1, small workspace, high occupancy).  R | c unpacked to shared memory.  X = R^-1 by 8 x 8
 //    blocks on the FP64 tensor cores gives sum 1/s_i^2 = |X|_F^2, a rigorous lower bound of the smallest singular
-//    value: if it clears rank_tol * |R|_F nothing is truncated and beta = R^-1 c by back-substitution.  Everything
-//    else (bound inconclusive, a pivot below rank_tol * the largest, more predecessors than members) is appended to a
-//    work list.
+//    value: if it clears rank_tol * |R|_F nothing is truncated and beta = R^-1 c by back-substitution.  Otherwise one
+//    inverse-iteration probe looks for a single, well separated sub-threshold value (the common case on smooth
+//    ensembles with p < N / 2): if it converges and |X|_F^2 - 1/s_1^2 proves every other value above the threshold, the
+//    pair is deflated here.  Everything else (several small values, slow convergence, a pivot far below the threshold,
+//    more predecessors than members) is appended to a work list.
 //
 //  regress_trunc_kernel (K2b-2).  For the listed rows the singular values below the threshold are found together by
 //    block inverse iteration: an orthonormal block Z (p x b, b = 8, 16, ...; pseudo-random start) is iterated as
@@ -30,9 +32,9 @@
 //  T = -beta;  D = max((e2 + |c - R beta|^2) / (N - 1), floor): |y - A^T beta|^2 of estimator.py:60,148 in the QR
 //  basis (orthogonal invariance), the second term only when something was truncated.
 //
-// flag bits: 1 row went to K2b-2, 2 truncated, 8 D floored, 16 Jacobi fallback, 5-7 fallback reason (1 non-finite /
-// breakdown, 2 block too small, 3 Ritz value at the threshold, 4 sweep cap), 8-15 block sweeps, 16-21 Jacobi sweeps,
-// 22-24 block size / 8.
+// flag bits: 1 row went to K2b-2, 2 truncated, 8 D floored, 16 Jacobi fallback, 5-7 with bit 16: fallback reason (1
+// non-finite / breakdown, 2 block too small, 3 Ritz value at the threshold, 4 sweep cap), bit 5 without bit 16: single pair
+// deflated in K2b-1, 8-15 block sweeps / probe steps, 16-21 Jacobi sweeps, 22-24 block size / 8.
 #pragma once
 
 #define JACOBI_MAX_SWEEPS 30
@@ -585,7 +587,9 @@ __global__ void __launch_bounds__(512, 1) regress_clean_kernel(const RegressPara
         if (p == 0) continue;                    // done in K2a
         const int K = p < N ? p : N;
         const double *in = P.Rq + (int64_t)fl * P.rq_stride + P.rq_ptr[q];
-        bool clean = false;
+        bool clean = false, single = false;          // single: exactly one singular value below the threshold, deflated here
+        double e2 = 0.0, sv = 0.0;
+        int nsteps = 0;
         if (K == p) {
             double dmin = DBL_MAX, dmax = 0.0, fro2 = 0.0;
             unpack_rc<PS>(in, W, ld, p, K, lane, &fro2);
@@ -598,11 +602,118 @@ __global__ void __launch_bounds__(512, 1) regress_clean_kernel(const RegressPara
             }
             dmin = warp_min(dmin);
             dmax = warp_max(dmax);
+            e2 = in[packed_col_offset(p, K) + K];
             __syncwarp();
-            // s_min <= min |r_jj| and s_max >= max |r_jj|: a small pivot ratio proves the truncation outright
-            if (dmin > P.rank_tol * dmax && fro2 < 1e300) {
+            // a pivot ratio far below the threshold (s_min <= min |r_jj|, s_max >= max |r_jj|) means several small values in
+            // practice: straight to the block kernel
+            if (dmin > 1e-3 * P.rank_tol * dmax && fro2 < 1e300) {
+                const double fro = sqrt(fro2);
                 const double tail2 = inverse_norm2_mma(W, rinv, ld, p, stage, lane);   // sum 1 / s_i^2 >= 1 / s_min^2
-                clean = tail2 > 0.0 && 1.0 / sqrt(tail2) >= P.rank_tol * sqrt(fro2) * (1.0 + 1e-3);
+                clean = tail2 > 0.0 && 1.0 / sqrt(tail2) >= P.rank_tol * fro * (1.0 + 1e-3);
+                if (!clean && tail2 > 0.0 && p >= 2) {
+                    // One inverse-iteration probe (two scalar triangular solves per step) from a pseudo-random start.  If it
+                    // converges to a value s_1 that is provably below the threshold and the rest of the spectrum is provably
+                    // above it -- sum_{i>=2} 1/s_i^2 = |X|_F^2 - 1/s_1^2 bounds s_2 from below -- the row is finished here
+                    // with the single pair deflated; anything else goes to the block kernel.
+                    Vec<PS> z, yt;
+                    const unsigned seed = (unsigned)P.state_row[q] * 7919u + (unsigned)p * 104729u;
+#pragma unroll
+                    for (int t = 0; t < PS; ++t) {
+                        const int e = lane + 32 * t;
+                        unsigned h = (unsigned)(e + 1) * 2654435761u ^ (seed * 40503u + 0x9e3779b9u);
+                        h ^= h >> 15; h *= 2246822519u; h ^= h >> 13; h *= 3266489917u; h ^= h >> 16;
+                        z.v[t] = e < p ? (double)(h >> 8) * (1.0 / 8388608.0) - 1.0 : 0.0;
+                    }
+                    {
+                        const double inv = rsqrt(vdot<PS>(z, z));
+#pragma unroll
+                        for (int t = 0; t < PS; ++t) z.v[t] *= inv;
+                    }
+                    double dz_old = 1.0;
+                    bool conv = false;
+                    for (int it = 0; it < 12 && !conv; ++it) {
+                        ++nsteps;
+                        Vec<PS> zz = solve_upper_t<PS>(z, W, rinv, ld, p, lane);
+                        yt = zz;                                       // R^-T z: the left singular direction
+                        zz = solve_upper<PS>(zz, W, rinv, ld, p, lane);
+                        const double zMz = vdot<PS>(zz, z);
+                        const double inv = rsqrt(vdot<PS>(zz, zz));
+                        const double sg = zMz >= 0.0 ? 1.0 : -1.0;
+                        double dz = 0.0;
+#pragma unroll
+                        for (int t = 0; t < PS; ++t) {
+                            const double zn = zz.v[t] * inv;
+                            const double df = zn - sg * z.v[t];
+                            dz = fma(df, df, dz);
+                            z.v[t] = zn;
+                        }
+                        dz = sqrt(warp_sum(dz));
+                        if ((dz < 1e-6 && dz > 0.9 * dz_old) || dz < 1e-12) conv = true;          // at the rounding floor
+                        // linear convergence with ratio q = dz / dz_old: the iterate just computed is within dz q / (1 - q) of
+                        // the limit -- stop once that is at the 5e-14 level
+                        else if (it >= 2 && dz < 0.25 * dz_old && dz * dz < 4e-14 * dz_old) conv = true;
+                        else if (it >= 3 && dz > 0.3 * dz_old) break;                                // close values: a block is the better tool
+                        dz_old = dz;
+                    }
+                    if (conv) {
+                        // s_1 = 1 / |R^-T z| (an upper bound of the singular value, tight to second order in the error of z),
+                        // u = R^-T z / |R^-T z| from the last step (z moved by less than the stopping level since)
+                        const double ny = sqrt(vdot<PS>(yt, yt));
+                        sv = 1.0 / ny;
+                        double smax_lo = dmax;
+                        if (!(sv < P.rank_tol * smax_lo * (1.0 - 1e-3))) {       // sharpen the lower bound of s_max: two power steps
+                            Vec<PS> v;
+                            const double v0 = rsqrt((double)p);
+#pragma unroll
+                            for (int t = 0; t < PS; ++t) v.v[t] = (lane + 32 * t < p) ? v0 : 0.0;
+                            for (int pw = 0; pw < 2; ++pw) {
+                                const Vec<PS> y = mul_upper<PS>(v, W, ld, p, lane);
+                                v = mul_upper_t<PS>(y, W, ld, p, lane);
+                                const double nv = sqrt(vdot<PS>(v, v));
+                                smax_lo = fmax(smax_lo, sqrt(nv));
+                                const double inv = 1.0 / nv;
+#pragma unroll
+                                for (int t = 0; t < PS; ++t) v.v[t] *= inv;
+                            }
+                        }
+                        // X carries a relative error of at most about c eps cond(R): added to what is left, so that the bound
+                        // stays a lower bound
+                        const double noise = 2.2e-14 * (fro * ny);
+                        const double rem = tail2 - ny * ny;
+                        const double up2 = fmax(rem, 0.0) + noise * tail2;
+                        single = sv < P.rank_tol * smax_lo * (1.0 - 1e-3) && rem > -noise * tail2 && noise < 0.25 &&
+                                 1.0 / sqrt(up2) >= P.rank_tol * fro * (1.0 + 1e-3);
+                        if (single) {
+#pragma unroll
+                            for (int t = 0; t < PS; ++t) yt.v[t] *= sv;
+                            Vec<PS> b = vload<PS>(W + (size_t)p * ld, p, lane);
+                            const double pr = vdot<PS>(b, yt);                    // c -= u u^T c
+#pragma unroll
+                            for (int t = 0; t < PS; ++t) b.v[t] = fma(-pr, yt.v[t], b.v[t]);
+                            b = solve_upper<PS>(b, W, rinv, ld, p, lane);
+                            const double pz = vdot<PS>(b, z);                     // beta -= z z^T beta
+#pragma unroll
+                            for (int t = 0; t < PS; ++t) b.v[t] = fma(-pz, z.v[t], b.v[t]);
+                            double *Tout = P.T + (int64_t)f * P.nnz + r0;
+#pragma unroll
+                            for (int t = 0; t < PS; ++t) { const int e = lane + 32 * t; if (e < p) Tout[e] = -b.v[t]; }
+                            // |c - R beta|^2
+                            const Vec<PS> rb = mul_upper<PS>(b, W, ld, p, lane);
+                            const Vec<PS> c0 = vload<PS>(W + (size_t)p * ld, p, lane);
+                            double rest2 = 0.0;
+#pragma unroll
+                            for (int t = 0; t < PS; ++t) { const double df = c0.v[t] - rb.v[t]; rest2 = fma(df, df, rest2); }
+                            rest2 = warp_sum(rest2);
+                            if (lane == 0) {
+                                const double d = (e2 + rest2) / denom;
+                                P.D[(int64_t)f * P.nloc + q] = fmax(d, P.variance_floor);
+                                if (P.flags) P.flags[(int64_t)f * P.nloc + q] = 2 | 32 | (d < P.variance_floor ? 8 : 0) | ((nsteps < 255 ? nsteps : 255) << 8);
+                            }
+                            __syncwarp();
+                            continue;
+                        }
+                    }
+                }
             }
         }
         if (!clean) {
@@ -615,7 +726,7 @@ __global__ void __launch_bounds__(512, 1) regress_clean_kernel(const RegressPara
 #pragma unroll
         for (int t = 0; t < PS; ++t) { const int e = lane + 32 * t; if (e < p) Tout[e] = -b.v[t]; }
         if (lane == 0) {
-            const double d = in[packed_col_offset(p, K) + K] / denom;
+            const double d = e2 / denom;
             P.D[(int64_t)f * P.nloc + q] = fmax(d, P.variance_floor);
             if (P.flags) P.flags[(int64_t)f * P.nloc + q] = d < P.variance_floor ? 8 : 0;
         }
