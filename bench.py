@@ -13,9 +13,11 @@ figure); `roofline_k2a` and `roofline_solve` give K2a alone and K3.
 `--impl reference` times the CPU oracle port (the reference is pure Python and cannot travel to the
 GPU box) on a bounded sample with all host cores.
 
-N > 1 (torchrun): sub-domains are sharded by contiguous block rows across ranks; per step rank 0's
-background is broadcast (NCCL), every rank analyses its tiles, the interiors are all-gathered.
-Total work is fixed as N grows ("strong").
+N > 1: `python bench.py --gpus N` re-executes itself under torch.distributed.run with N ranks (one per GPU); under
+torchrun WORLD_SIZE must equal --gpus.  Sub-domains are sharded by contiguous block rows across ranks; per step rank 0
+scatters to every rank the background rows and perturbed-observation rows its tiles read (NCCL point-to-point), every
+rank analyses its tiles, the interiors are all-gathered.  Total work is fixed as N grows ("strong").  `e2e` at N > 1 is
+`assimilate_parallel_sharded` (host buffers on rank 0 -> upload -> scatter -> compute -> gather -> download).
 """
 
 from __future__ import annotations
@@ -34,8 +36,25 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-NCU_TRAFFIC_K2 = 15.15e9         # dram bytes read + written per bench launch: K2a 3.59 + 5.55 GB, K2b 5.65 + 0.35 GB (ncu --set full)
-NCU_TRAFFIC_SOURCE = "profiles/r1_ncu_full_k2_bench_launch.csv"
+NCU_TRAFFIC_SOURCE = "profiles/r2_ncu_full_bench_launch.csv"   # written by tools/make_profiles.py from one ncu --set full capture
+
+
+def ncu_traffic():
+    """{kernel name prefix: dram bytes read + written per launch} from the committed ncu summary (None if absent)."""
+    path = os.path.join(ROOT, NCU_TRAFFIC_SOURCE)
+    if not os.path.exists(path):
+        return None
+    import csv
+    out = {}
+    with open(path) as fh:
+        for row in csv.DictReader(fh):
+            try:
+                out[row["kernel"]] = float(row["dram_bytes_read"]) + float(row["dram_bytes_write"])
+            except (KeyError, ValueError):
+                continue
+    return out or None
+
+
 METRIC = "EnKF-MC analysis grid-points/sec (B^-1 est + local solve)"
 UNIT = "grid-points/s"
 
@@ -57,7 +76,7 @@ def _cpu_tile(t):
 
 def cpu_sample_setup(w, field=0):
     from oracle import enkf_mc_oracle as orc
-    grid = orc.Grid(w.nx, w.ny, True, w.boundary == "periodic")
+    grid = orc.grid_for(w.nx, w.ny, w.boundary)
     lo, hi = field * w.n2d, (field + 1) * w.n2d
     sel = np.flatnonzero((w.obs_indices >= lo) & (w.obs_indices < hi))
     tiles = orc.decompose(grid, w.delta, w.zeta)
@@ -181,15 +200,15 @@ def run_b200(args, rank, world, local_rank):
 
     import paper_1606_00807_b200 as mck
     from paper_1606_00807_b200 import _lib, device, distributed
-    from paper_1606_00807_b200.plan import get_plan
+    from paper_1606_00807_b200.plan import Plan, get_plan
 
     torch.cuda.set_device(local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     geo = mck.GridGeometry("ring1d" if w.ny == 1 else "grid2d", w.nx, w.ny, boundary=w.boundary, nfields=w.nfields)
-    plan = get_plan(geo, w.delta, w.zeta)
+    plan = get_plan(geo, w.delta, w.zeta) if world == 1 else Plan.decomposed(geo, w.delta, w.zeta)
     plan.set_observations(w.obs_indices)
-    shard = distributed.TileShard(plan, geo, rank, world)
+    shard = distributed.TileShard(plan, geo, rank, world, w.obs_indices)
     shard.apply()
 
     dX = device.to_device(w.X)
@@ -202,7 +221,7 @@ def run_b200(args, rank, world, local_rank):
         if flush is not None:
             flush.zero_()
         if world > 1:
-            shard.broadcast_background(dX)
+            shard.scatter_background(dX, dYs)
         device.analysis_device(plan, dX, dR, dYs, dXa)
         if world > 1:
             shard.gather_analysis(dXa)
@@ -245,32 +264,50 @@ def run_b200(args, rank, world, local_rank):
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
         ms = float(tmax.item())
 
-    # ---- parity spot check of the timed output against the CPU sample (field 0) ----------------
-    parity = None
+    # ---- outcome of the timed analyses: per-tile status (a failed tile must not be timed as a success) and a parity
+    #      spot check of the timed output against the CPU sample (field 0), gated by the oracle's measured noise floor ---
+    clamped = device.check_status(plan)          # raises NumericalError naming the sub-domain
+    parity, parity_gate = None, None
     if cpu_field0 is not None:
         got = dXa[: w.n2d].cpu().numpy()
         parity = float(np.linalg.norm(got - cpu_field0) / np.linalg.norm(cpu_field0))
+        floors_path = os.path.join(ROOT, "tests", "golden", "noise_floors.json")
+        key = args.workload + ("_nugget" if args.nugget > 0 else "")
+        floor = json.load(open(floors_path)).get(key, {}).get("Xa") if os.path.exists(floors_path) else None
+        parity_gate = max(1e-8, 10.0 * floor) if floor is not None else None
+        if parity_gate is not None and not parity < parity_gate:
+            raise SystemExit(f"bench: analysis differs from the CPU oracle by {parity:.3e} (gate {parity_gate:.1e}): number not reported")
 
-    # ---- end to end through the public API with pinned host buffers ------------------------
-    Xh, _keep1 = pinned(w.X)
-    Ysh, _keep2 = pinned(w.Ys)
+    # ---- end to end through the public API: host buffers in, host analysis out -----------------------
     net = mck.ObservationNetwork(w.obs_indices, w.r_diag, w.y)
     cfg = mck.AssimilationConfig(zeta=w.zeta, delta=w.delta)
-    xb = mck.EnsembleState(Xh)
-    for _ in range(max(args.warmup, 3)):   # same ownership pattern as the timed loop: the pinned result pool reaches its
-        xa, rep = mck.assimilate_parallel(xb, net, cfg, geo, Ys=Ysh)   # steady state (two buffers) before timing starts
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        xa, rep = mck.assimilate_parallel(xb, net, cfg, geo, Ys=Ysh)
-    torch.cuda.synchronize()
-    t_e2e = (time.perf_counter() - t0) / args.steps
-    if world > 1:
-        tmax = torch.tensor([t_e2e], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-        t_e2e = float(tmax.item())
+
+    def e2e_loop(xb, ys):
+        if world == 1:
+            call = lambda: mck.assimilate_parallel(xb, net, cfg, geo, Ys=ys)
+        else:
+            call = lambda: mck.assimilate_parallel_sharded(xb if rank == 0 else None, net, cfg, geo,
+                                                            Ys=ys if rank == 0 else None, nens=w.nens)
+        for _ in range(max(args.warmup, 3)):   # same ownership pattern as the timed loop: the pinned result pool reaches its
+            xa, rep = call()                   # steady state (two buffers) before timing starts
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            xa, rep = call()
+        torch.cuda.synchronize()
+        t = (time.perf_counter() - t0) / args.steps
+        if world > 1:
+            tmax = torch.tensor([t], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+            t = float(tmax.item())
+        return t, rep
+
+    Xh, _keep1 = pinned(w.X)
+    Ysh, _keep2 = pinned(w.Ys)
+    t_e2e, rep = e2e_loop(mck.EnsembleState(Xh), Ysh)                    # page-locked inputs: asynchronous, pipelined copies
+    t_e2e_pageable, _ = e2e_loop(mck.EnsembleState(w.X), w.Ys)           # ordinary numpy arrays: staged copies
     stop.set()
     if sampler is not None:
         sampler.join(timeout=2.0)
@@ -291,6 +328,17 @@ def run_b200(args, rank, world, local_rank):
         ach = fl_reg / t_reg * 1e-12 if t_reg > 0 else 0.0
         ach_sol = fl_sol / t_sol * 1e-12 if t_sol > 0 else 0.0
         nstate = w.nstate
+        tr = ncu_traffic()
+
+        def traffic_of(*prefixes):
+            if not tr:
+                return None
+            tot = sum(v for k, v in tr.items() if any(k.startswith(px) for px in prefixes))
+            return tot or None
+
+        peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+        hbm_measured = os.path.exists(peaks_path)
+        hbm_peak = float(json.load(open(peaks_path)).get("hbm_gbs", 6551.0)) if hbm_measured else 6551.0
         out = {
             "metric": METRIC, "value": nstate / (ms * 1e-3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
@@ -299,10 +347,10 @@ def run_b200(args, rank, world, local_rank):
             # the regression stage is one unit of work split over two kernels: K2a executes the credited flops
             # (Householder-QR least squares), K2b (the longer of the two) turns the QR into the reference's
             # truncated-SVD answer and is uncredited -- `roofline` therefore charges both kernels' time to the QR flops
-            "roofline": {"kernel": "regress_qr_mma_kernel + regress_solve_kernel (K2a + K2b: one regression stage)",
+            "roofline": {"kernel": "regress_qr_mma_kernel + regress_clean_kernel + regress_trunc_kernel (K2a + K2b: one regression stage)",
                          "bound": "tensor", "achieved": ach, "peak": pk,
                          "unit": "TFLOP/s", "frac": ach / pk if pk > 0 else None,
-                         "traffic": NCU_TRAFFIC_K2 if args.workload == "cfg3" and world == 1 else None,
+                         "traffic": traffic_of("regress_") if args.workload == "cfg3" and world == 1 else None,
                          "traffic_source": NCU_TRAFFIC_SOURCE,
                          "peak_source": peak_note,
                          "ms_per_launch": t_reg * 1e3, "algorithmic_flops_per_launch": fl_reg,
@@ -311,10 +359,17 @@ def run_b200(args, rank, world, local_rank):
                          "reference_equivalent_flops": fl_reg_ref},
             "roofline_k2a": {"kernel": "regress_qr_mma_kernel (K2a alone)", "bound": "tensor", "achieved": ach_qr, "peak": pk,
                              "unit": "TFLOP/s", "frac": ach_qr / pk if pk > 0 else None, "ms_per_launch": t_qr * 1e3,
-                             "algorithmic_flops_per_launch": fl_reg},
+                             "algorithmic_flops_per_launch": fl_reg,
+                             "traffic": traffic_of("regress_qr") if args.workload == "cfg3" and world == 1 else None},
             "roofline_solve": {"kernel": "assemble_band_tile_kernel + local_solve_kernel (K3)", "bound": "tensor", "achieved": ach_sol,
                                "peak": pk, "unit": "TFLOP/s", "frac": ach_sol / pk if pk > 0 else None,
-                               "ms_per_launch": t_sol * 1e3, "algorithmic_flops_per_launch": fl_sol},
+                               "ms_per_launch": t_sol * 1e3, "algorithmic_flops_per_launch": fl_sol,
+                               "traffic": traffic_of("assemble_band", "local_solve") if args.workload == "cfg3" and world == 1 else None},
+            "roofline_center": {"kernel": "center_rows_kernel (K0)", "bound": "hbm",
+                                "achieved": 16.0 * w.nstate * w.nens / (stage_ms[0] / nc * 1e-3) * 1e-9 if stage_ms[0] > 0 else None,
+                                "peak": hbm_peak, "unit": "GB/s",
+                                "frac": (16.0 * w.nstate * w.nens / (stage_ms[0] / nc * 1e-3) * 1e-9 / hbm_peak) if stage_ms[0] > 0 and hbm_peak else None,
+                                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if hbm_measured else "fallback 6551 GB/s (MEASURED_PEAKS.json absent)"},
             "stage_ms": {"center": stage_ms[0] / nc, "regress_qr": t_qr * 1e3, "regress_solve": t_prb * 1e3,
                          "local_solve": t_sol * 1e3},
             "cpu_baseline": cpu_baseline,
@@ -324,13 +379,19 @@ def run_b200(args, rank, world, local_rank):
                     "breakdown_ms": {"h2d": rep.t_h2d * 1e3, "estimation": float(rep.t_estimation.sum()) * 1e3,
                                      "analysis": float(rep.t_analysis.sum()) * 1e3, "d2h": rep.t_d2h * 1e3,
                                      "call_wall": rep.t_total * 1e3},
-                    "pipelined": "5 groups of fields: H2D of group g+1 and D2H of group g-1 overlap the kernels of group g",
+                    "pipelined": ("5 groups of fields: H2D of group g+1 and D2H of group g-1 overlap the kernels of group g" if world == 1
+                                  else "rank 0 uploads, scatters the slabs, all ranks compute, all-gather, rank 0 downloads"),
                     "h2d_bytes_per_step": int(w.X.nbytes + w.Ys.nbytes + w.r_diag.nbytes),
                     "d2h_bytes_per_step": int(w.X.nbytes),
-                    "api": "assimilate_parallel(EnsembleState, ObservationNetwork, AssimilationConfig, GridGeometry, Ys=)"},
+                    "api": ("assimilate_parallel" if world == 1 else "assimilate_parallel_sharded") +
+                           "(EnsembleState, ObservationNetwork, AssimilationConfig, GridGeometry, Ys=)",
+                    "inputs": "page-locked host arrays"},
+            "e2e_pageable": {"value": nstate / t_e2e_pageable, "unit": UNIT, "ms_per_step": t_e2e_pageable * 1e3,
+                             "inputs": "ordinary (pageable) numpy arrays: the driver stages the copies, nothing overlaps"},
             "gpu_launches": int(launches),
             "clocks": summarize_clocks(samples),
-            "parity_vs_cpu_sample": parity,
+            "parity_vs_cpu_sample": parity, "parity_gate": parity_gate, "clamped_pivots": int(clamped),
+            "rank_memory_fraction": shard.memory_fraction(),
         }
         print(json.dumps(out))
     if world > 1:
@@ -348,9 +409,22 @@ def main():
     ap.add_argument("--nugget", type=float, default=0.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # one process per GPU: re-execute under torch.distributed.run (what the driver does itself for N > 1)
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        os.execv(sys.executable, [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+                                  "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:])
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}: launch with --nproc-per-node {args.gpus}")
+    if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")          # the communicator / transport log goes to stderr
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     if args.impl == "reference":
         run_reference(args, rank, world)
     else:

@@ -39,6 +39,11 @@ const char *enkfmc_last_error(void);
 
 /* ---- index maps (integer, bit-exact) ------------------------------------------- */
 
+/* `periodic`: 0 clipped, 1 periodic on both axes (the reference's boundary flag, geometry.py:43),
+ * 2 periodic along x only (columns: longitude periodic, latitude clipped), 3 along y only.  Codes 2
+ * and 3 apply the reference's per-axis window / band rules (geometry.py:132-142) with one flag per
+ * axis; the reference itself cannot express them. */
+
 /* Near-square block grid pr x pc of `delta` tiles: geometry.py:179-193. */
 int enkfmc_tiling(int64_t nx, int64_t ny, int64_t delta, int64_t *pr, int64_t *pc);
 
@@ -119,6 +124,13 @@ int enkfmc_analysis_device(enkfmc_plan *plan, const double *d_X, const double *d
                            const double *d_Ys, int64_t nens, double rank_tol,
                            double variance_floor, double *d_Xa, void *stream);
 
+/* Outcome of the last analysis on this plan (either entry point): synchronises, reads the per-tile
+ * status words and the clamped-pivot count (enkfmc_plan_counter(plan, 5)); a failed tile returns
+ * ENKFMC_E_NUMERIC naming the sub-domain, as analysis_primal raises NumericalError when the
+ * factorisation fails (kernels.py:192-195).  enkfmc_analysis_device is asynchronous and
+ * does not look at the status itself; callers check here once the step is done. */
+int enkfmc_plan_check_status(enkfmc_plan *plan);
+
 /* ---- host-buffer entry point (what assimilate_parallel binds; driver.py:159-253) -- */
 
 /* Copies X, r_diag, Ys to the device, runs the analysis, copies Xa back.  The fields (independent
@@ -189,6 +201,14 @@ int enkfmc_assemble_band(enkfmc_plan *plan, const double *d_T, const double *d_D
  * PrecisionFactors.precision_apply, factors.py:86-96. */
 int enkfmc_precision_apply(enkfmc_plan *plan, const double *d_T, const double *d_D, const double *d_V,
                            int64_t ncols, double *d_tmp, double *d_out, void *stream);
+
+/* Unit-triangular solves with many right-hand sides on a single-tile plan, in place on d_B [n][ncols]:
+ *   transposed = 0: (I + L) X = diag(d_scale_in) B    -- PrecisionFactors.sqrt_solve (factors.py:116-134, scale_in =
+ *                   sqrt(D)) and the second half of covariance_apply (factors.py:98-114);
+ *   transposed = 1: (I + L)^T X = B, X *= d_scale_out -- the first half of covariance_apply (scale_out = D).
+ * Either scale may be NULL. */
+int enkfmc_unit_tri_solve(enkfmc_plan *plan, const double *d_T, int transposed, const double *d_scale_in,
+                          const double *d_scale_out, double *d_B, int64_t ncols, void *stream);
 
 #ifdef __cplusplus
 }

@@ -48,6 +48,17 @@ class Grid:
     row_major: bool = True
     periodic: bool = False
     nfields: int = 1
+    # extension (no reference counterpart, "parity unpinned by the reference"): one flag per axis; None = `periodic`
+    periodic_x: bool | None = None
+    periodic_y: bool | None = None
+
+    @property
+    def px(self) -> bool:
+        return self.periodic if self.periodic_x is None else self.periodic_x
+
+    @property
+    def py(self) -> bool:
+        return self.periodic if self.periodic_y is None else self.periodic_y
 
     @property
     def n2d(self) -> int:
@@ -56,6 +67,13 @@ class Grid:
     @property
     def nstate(self) -> int:
         return self.n2d * self.nfields
+
+
+def grid_for(nx: int, ny: int, boundary: str, nfields: int = 1, row_major: bool = True) -> Grid:
+    """Grid of a boundary name: "clipped" / "periodic" (reference), "periodic_x" / "periodic_y" (per-axis extension)."""
+    if boundary in ("clipped", "periodic"):
+        return Grid(nx, ny, row_major, boundary == "periodic", nfields)
+    return Grid(nx, ny, row_major, False, nfields, periodic_x=boundary == "periodic_x", periodic_y=boundary == "periodic_y")
 
 
 def coords(grid: Grid, label: int) -> tuple[int, int]:
@@ -93,8 +111,8 @@ def local_box(grid: Grid, center: int, zeta: int) -> np.ndarray:
     r, c = coords(grid, center)
     return _label_grid(
         grid,
-        axis_window(r, zeta, grid.ny, grid.periodic),
-        axis_window(c, zeta, grid.nx, grid.periodic),
+        axis_window(r, zeta, grid.ny, grid.py),
+        axis_window(c, zeta, grid.nx, grid.px),
     )
 
 
@@ -149,8 +167,8 @@ def decompose(grid: Grid, delta: int, zeta: int) -> list[Tile]:
             interior = _label_grid(grid, np.arange(r0, r1), np.arange(c0, c1))
             covered = _label_grid(
                 grid,
-                axis_band(r0, r1, zeta, grid.ny, grid.periodic),
-                axis_band(c0, c1, zeta, grid.nx, grid.periodic),
+                axis_band(r0, r1, zeta, grid.ny, grid.py),
+                axis_band(c0, c1, zeta, grid.nx, grid.px),
             )
             halo = np.setdiff1d(covered, interior, assume_unique=True)
             tiles.append(Tile(bi * pc + bj, interior, halo, np.union1d(interior, halo)))
@@ -175,12 +193,15 @@ def predecessor_csr(grid: Grid, zeta: int, local_order: np.ndarray):
     off = np.arange(-zeta, zeta + 1)
     rr = (r[:, None, None] + off[None, :, None]) + 0 * off[None, None, :]
     cc = (c[:, None, None] + off[None, None, :]) + 0 * off[None, :, None]
-    if grid.periodic:
+    ok = np.ones(rr.shape, dtype=bool)
+    if grid.py:
         rr %= grid.ny
-        cc %= grid.nx
-        ok = np.ones(rr.shape, dtype=bool)
     else:
-        ok = (rr >= 0) & (rr < grid.ny) & (cc >= 0) & (cc < grid.nx)
+        ok &= (rr >= 0) & (rr < grid.ny)
+    if grid.px:
+        cc %= grid.nx
+    else:
+        ok &= (cc >= 0) & (cc < grid.nx)
     lab = np.where(grid.row_major, rr * grid.nx + cc, cc * grid.ny + rr)
     ok &= lab < lo[:, None, None]
     row_id = np.broadcast_to(np.arange(n)[:, None, None], lab.shape)[ok]
@@ -228,12 +249,43 @@ def center_rows(X: np.ndarray) -> np.ndarray:
     return U
 
 
+_SVD_DRIVER = ["gesdd"]      # what the reference calls (numpy.linalg.svd); "gesvd" only for the noise-floor probe
+
+
+class svd_driver:
+    """Context manager for the noise-floor probe of SURVEY.md section 8c: the same solve with LAPACK dgesvd
+    (scipy.linalg.svd, lapack_driver="gesvd", item by item) instead of the reference's dgesdd."""
+
+    def __init__(self, name: str):
+        assert name in ("gesdd", "gesvd")
+        self.name = name
+
+    def __enter__(self):
+        self.prev = _SVD_DRIVER[0]
+        _SVD_DRIVER[0] = self.name
+
+    def __exit__(self, *exc):
+        _SVD_DRIVER[0] = self.prev
+
+
+def _batched_svd(A: np.ndarray):
+    if _SVD_DRIVER[0] == "gesdd":
+        return np.linalg.svd(A, full_matrices=False)       # estimator.py:53
+    from scipy.linalg import svd as _svd
+    k, p, m = A.shape
+    r = min(p, m)
+    u, s, vt = np.empty((k, p, r)), np.empty((k, r)), np.empty((k, r, m))
+    for i in range(k):
+        u[i], s[i], vt[i] = _svd(A[i], full_matrices=False, lapack_driver="gesvd")
+    return u, s, vt
+
+
 def svd_min_norm(A: np.ndarray, y: np.ndarray, rank_tol: float = RANK_TOL):
     """Batched truncated-SVD minimum-norm LS (estimator.py:46-61).
 
     A: (k, p, m), y: (k, m) -> beta (k, p), residual (k, m).
     """
-    u, s, vt = np.linalg.svd(A, full_matrices=False)
+    u, s, vt = _batched_svd(A)
     tol = rank_tol * s[:, :1]
     with np.errstate(divide="ignore", invalid="ignore"):
         inv_s = np.where((s >= tol) & (s > 0), 1.0 / s, 0.0)

@@ -57,6 +57,8 @@ struct DeviceState {
     std::vector<cudaEvent_t> hev;    // events of the pipelined host path
 };
 
+void enkfmc_device_release(enkfmc_plan *p);
+
 namespace {
 
 template <class T>
@@ -71,8 +73,7 @@ int upload(T *&dst, const std::vector<T> &src) {
 template <class T>
 void release(T *&p) { if (p) { cudaFree(p); p = nullptr; } }
 
-int ensure_device(enkfmc_plan *p) {
-    if (p->dev) return ENKFMC_OK;
+int init_device(enkfmc_plan *p) {
     int count = 0;
     cudaError_t e = cudaGetDeviceCount(&count);
     if (e != cudaSuccess || count == 0) {
@@ -92,7 +93,7 @@ int ensure_device(enkfmc_plan *p) {
     }
     d->sm_count = prop.multiProcessorCount;
     d->smem_limit = prop.sharedMemPerBlockOptin;
-    p->dev = d;
+    p->dev = d;       // (ensure_device releases it again if anything below fails)
     int rc;
     if ((rc = upload(d->tile_ptr, p->tile_ptr))) return rc;
     if ((rc = upload(d->row_ptr, p->row_ptr))) return rc;
@@ -121,6 +122,15 @@ int ensure_device(enkfmc_plan *p) {
     CK(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&d->copy_stream, cudaStreamNonBlocking));
     return ENKFMC_OK;
+}
+
+// Device mirror of the plan, created on first use.  A failure part-way (out of memory) leaves no half-initialised state
+// behind: the next call starts from scratch instead of launching with null buffers.
+int ensure_device(enkfmc_plan *p) {
+    if (p->dev) return ENKFMC_OK;
+    const int rc = init_device(p);
+    if (rc != ENKFMC_OK && p->dev) enkfmc_device_release(p);
+    return rc;
 }
 
 int ensure_orders(enkfmc_plan *p) {
@@ -304,6 +314,30 @@ int do_solve(enkfmc_plan *p, const double *d_X, const double *d_T, const double 
     return ENKFMC_OK;
 }
 
+// Reads the per-tile status words of the last analysis (0 ok, 1 not positive definite, 2 non-finite) and the clamped-pivot
+// count; a failed tile becomes ENKFMC_E_NUMERIC naming the sub-domain (kernels.py:194-195).  Synchronises.
+int scan_status(enkfmc_plan *p) {
+    DeviceState *d = p->dev;
+    CK(cudaDeviceSynchronize());
+    unsigned int clamped = 0;
+    CK(cudaMemcpy(&clamped, d->counters + 3, sizeof(unsigned int), cudaMemcpyDeviceToHost));
+    p->counters[5] = clamped;
+    std::vector<int32_t> st((size_t)(p->ntiles * p->nfields));
+    if (!st.empty()) CK(cudaMemcpy(st.data(), d->status, st.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    p->counters[4] = -1;
+    for (size_t it = 0; it < st.size(); ++it) {
+        if (st[it] != 0) {
+            const int64_t f = (int64_t)it / p->ntiles, t = (int64_t)it % p->ntiles;
+            p->counters[4] = (int64_t)it;
+            enkfmc_set_error("primal analysis solve failed in subdomain " + std::to_string(t) + " (field " +
+                             std::to_string(f) + "): " +
+                             (st[it] == 1 ? "matrix not positive definite" : "non-finite pivot"));
+            return ENKFMC_E_NUMERIC;
+        }
+    }
+    return ENKFMC_OK;
+}
+
 }  // namespace
 
 void enkfmc_device_invalidate_obs(enkfmc_plan *p) { if (p->dev) p->dev->obs_current = false; }
@@ -370,6 +404,7 @@ extern "C" int enkfmc_analysis_device(enkfmc_plan *p, const double *d_X, const d
         d->prof_used += 5;
         CK(cudaEventRecord(ev[0], s));
     }
+    CK(cudaMemsetAsync(d->status, 0, std::max<size_t>(1, (size_t)p->ntiles * p->nfields) * sizeof(int32_t), s));
     CK(launch_center_rows(d_X, d->U, p->nstate2d * p->nfields, (int)nens, s));
     p->counters[0] += 1;
     if (ev) CK(cudaEventRecord(ev[1], s));
@@ -378,6 +413,11 @@ extern "C" int enkfmc_analysis_device(enkfmc_plan *p, const double *d_X, const d
     rc = do_solve(p, d_X, d->T, d->D, d_r, d_Ys, nens, d_Xa, d->status, s);
     if (ev) CK(cudaEventRecord(ev[4], s));
     return rc;
+}
+
+extern "C" int enkfmc_plan_check_status(enkfmc_plan *p) {
+    if (!p->dev || !p->dev->status) return ENKFMC_OK;
+    return scan_status(p);
 }
 
 extern "C" int enkfmc_plan_profile(enkfmc_plan *p, int enable) {
@@ -489,6 +529,8 @@ extern "C" int enkfmc_analysis_host(enkfmc_plan *p, const double *X, const doubl
     // Pipelined over groups of fields: the copy stream uploads group g + 1 and downloads the analysis of group
     // g - 1 while the compute stream works on group g (fields are independent: PAPER.md:201).
     cudaStream_t s = d->stream, cs = d->copy_stream;
+    // tiles outside the owned range are never written: start every analysis from a clean status array
+    CK(cudaMemsetAsync(d->status, 0, std::max<size_t>(1, (size_t)p->ntiles * p->nfields) * sizeof(int32_t), s));
     // Five groups for a dozen fields or more, the first and the last small (the kernels start after a short upload and
     // only a short download is exposed; smaller groups than this cost more in kernel tails than they hide).
     std::vector<int64_t> cuts;
@@ -538,10 +580,12 @@ extern "C" int enkfmc_analysis_host(enkfmc_plan *p, const double *X, const doubl
         CK(cudaEventRecord(EV(g, 2), s));
         CK(launch_center_rows(d->dX + r0 * nens, d->U + r0 * nens, (int64_t)(r1 - r0), (int)nens, s));
         p->counters[0] += 1;
-        if ((rc = do_regress(p, d->U, nens, rank_tol, floor_, d->T, d->D, d->flags, s, nullptr, f0, f1))) return rc;
+        if ((rc = do_regress(p, d->U, nens, rank_tol, floor_, d->T, d->D, d->flags, s, nullptr, f0, f1))) { cudaStreamSynchronize(cs); cudaStreamSynchronize(s); return rc; }
         CK(cudaEventRecord(EV(g, 3), s));
         CK(cudaStreamWaitEvent(s, EV(g, 7), 0));
-        if ((rc = do_solve(p, d->dX, d->T, d->D, d->dR, d->dYs, nens, d->dXa, d->status, s, f0, f1))) return rc;
+        if (p->tile_begin != 0 || p->tile_end != p->ntiles)   // a rank's share: rows it does not own come back as the background
+            CK(cudaMemcpyAsync(d->dXa + r0 * nens, d->dX + r0 * nens, (r1 - r0) * rowbytes, cudaMemcpyDeviceToDevice, s));
+        if ((rc = do_solve(p, d->dX, d->T, d->D, d->dR, d->dYs, nens, d->dXa, d->status, s, f0, f1))) { cudaStreamSynchronize(cs); cudaStreamSynchronize(s); return rc; }
         CK(cudaEventRecord(EV(g, 4), s));
         CK(cudaStreamWaitEvent(cs, EV(g, 4), 0));
         CK(cudaEventRecord(EV(g, 5), cs));
@@ -566,25 +610,7 @@ extern "C" int enkfmc_analysis_host(enkfmc_plan *p, const double *X, const doubl
             CK(span(EV(g, 5), EV(g, 6), timings_ms[3]));
         }
     }
-    {
-        unsigned int clamped = 0;
-        CK(cudaMemcpy(&clamped, d->counters + 3, sizeof(unsigned int), cudaMemcpyDeviceToHost));
-        p->counters[5] = clamped;
-    }
-    // per-tile status -> NumericalError naming the sub-domain
-    std::vector<int32_t> st((size_t)(p->ntiles * p->nfields));
-    if (!st.empty()) CK(cudaMemcpy(st.data(), d->status, st.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
-    p->counters[4] = -1;
-    for (size_t it = 0; it < st.size(); ++it) {
-        if (st[it] != 0) {
-            const int64_t f = (int64_t)it / p->ntiles, t = (int64_t)it % p->ntiles;
-            p->counters[4] = (int64_t)it;
-            enkfmc_set_error("primal analysis solve failed in subdomain " + std::to_string(t) + " (field " +
-                             std::to_string(f) + "): " +
-                             (st[it] == 1 ? "matrix not positive definite" : "non-finite pivot"));
-            return ENKFMC_E_NUMERIC;
-        }
-    }
+    if ((rc = scan_status(p))) return rc;
     return ENKFMC_OK;
 }
 
@@ -655,6 +681,25 @@ extern "C" int enkfmc_precision_apply(enkfmc_plan *p, const double *d_T, const d
     CK(launch_precision_apply(d->row_ptr, d->col_idx, d->csc_ptr, d->csc_row, d->csc_src, d_T, d_D, d_V, d_tmp,
                               d_out, p->sum_nlocal(), ncols, (cudaStream_t)stream));
     p->counters[0] += 2;
+    return ENKFMC_OK;
+}
+
+extern "C" int enkfmc_unit_tri_solve(enkfmc_plan *p, const double *d_T, int transposed, const double *d_scale_in,
+                                     const double *d_scale_out, double *d_B, int64_t ncols, void *stream) {
+    if (p->ntiles != 1 || p->nfields != 1) {
+        enkfmc_set_error("unit_tri_solve needs a single-tile plan");
+        return ENKFMC_E_VALUE;
+    }
+    int rc = ensure_device(p);
+    if (rc) return rc;
+    DeviceState *d = p->dev;
+    if (transposed)
+        CK(launch_unit_tri_solve(1, d->csc_ptr, d->csc_row, d->csc_src, d_T, d_scale_in, d_scale_out, d_B, p->sum_nlocal(), ncols,
+                                 (cudaStream_t)stream));
+    else
+        CK(launch_unit_tri_solve(0, d->row_ptr, d->col_idx, nullptr, d_T, d_scale_in, d_scale_out, d_B, p->sum_nlocal(), ncols,
+                                 (cudaStream_t)stream));
+    p->counters[0] += 1;
     return ENKFMC_OK;
 }
 

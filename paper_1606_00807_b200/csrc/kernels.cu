@@ -875,7 +875,11 @@ cudaError_t launch_regress(const RegressParams &p_in, int sm_count, size_t smem_
     const int S = (p.N + 31) / 32;
     // ensembles of up to 128 members: tensor-core form; larger ones (or ENKFMC_QR=smem, for comparisons): the
     // shared-memory SIMT form
+#ifdef ENKFMC_TUNING
     const char *qr_sel = getenv("ENKFMC_QR");
+#else
+    const char *qr_sel = nullptr;      // run-time knobs exist in tuning builds only (-DENKFMC_TUNING)
+#endif
     if (p.N <= 128 && !qr_sel) {
         const int nt = (p.N + 7) / 8;
         const int NTc = nt <= 4 ? 4 : nt <= 6 ? 6 : nt <= 10 ? 10 : 16;      // the instantiation used below
@@ -883,7 +887,9 @@ cudaError_t launch_regress(const RegressParams &p_in, int sm_count, size_t smem_
         int warps = (int)(smem_limit / ws);
         if (warps < 1) return cudaErrorInvalidConfiguration;
         if (warps > 8) warps = 8;
+#ifdef ENKFMC_TUNING
         if (const char *wenv = getenv("ENKFMC_QR_WARPS")) { const int wv = atoi(wenv); if (wv >= 1 && wv < warps) warps = wv; }
+#endif
         int64_t grid = sm_count;
         const int64_t need = (p.nwork + warps - 1) / warps;
         if (grid > need) grid = need;
@@ -937,7 +943,9 @@ cudaError_t launch_regress(const RegressParams &p_in, int sm_count, size_t smem_
     {
         const int b1 = p.pmax < 8 ? 0 : p.pmax <= 48 ? 8 : 16;
         int b2 = p.pmax < 8 ? 0 : p.pmax <= 16 ? 8 : p.pmax <= 64 ? 24 : 32;
+#ifdef ENKFMC_TUNING
         if (const char *benv = getenv("ENKFMC_K2B_BMAX")) { const int bv = atoi(benv); if (bv >= 8 && bv <= 32) b2 = bv & ~7; }
+#endif
         while (b2 > 8 && regress_trunc_ws_doubles(p.pmax, b2) * sizeof(double) > smem_limit) b2 -= 8;
         for (int level = 0; level < 2; ++level) {
             p.level = level;
@@ -948,7 +956,9 @@ cudaError_t launch_regress(const RegressParams &p_in, int sm_count, size_t smem_
             int warps = (int)(smem_limit / ws);
             if (warps < 1) return cudaErrorInvalidConfiguration;
             if (warps > 8) warps = 8;
+#ifdef ENKFMC_TUNING
             if (const char *wenv = getenv("ENKFMC_K2B_WARPS")) { const int wv = atoi(wenv); if (wv >= 1 && wv < warps) warps = wv; }
+#endif
             const int64_t grid = sm_count;
             if (p.pmax <= 32) e = launch_trunc_t<1>(p, (int)grid, warps, ws * warps, s);
             else if (p.pmax <= 64) e = launch_trunc_t<2>(p, (int)grid, warps, ws * warps, s);
@@ -1297,6 +1307,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
                 if (ea_r[k] < 8) {
                     int cc = rot + ea_e[k]; if (cc >= Wr) cc -= Wr;
                     Aw[(size_t)(rs + ea_r[k]) * pitch + cc] = fa[k];
+                    if (ea_e[k] == 8 * Wb + ea_r[k]) Aw[(size_t)(rs + ea_r[k]) * pitch + Wr] = fa[k];   // the row's original diagonal (pitch padding)
                 }
                 if (er_r[k] < 8)
                     Rw[(size_t)(rs + er_r[k]) * NR + er_m[k]] = (fr[k] != 0.0) ? (fy[k] - fx[k]) * (1.0 / fr[k]) : 0.0;
@@ -1311,6 +1322,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
                 const double v = (i < n) ? band[(int64_t)i * Wr + ee] : ((ee == 8 * Wb + rr) ? 1.0 : 0.0);
                 int cc = rot + ee; if (cc >= Wr) cc -= Wr;
                 Aw[(size_t)(rs + rr) * pitch + cc] = v;
+                if (ee == 8 * Wb + rr) Aw[(size_t)(rs + rr) * pitch + Wr] = v;
             }
             for (int e = tid; e < 8 * N; e += nthreads) {
                 const int rr = e / N, m = e - rr * N;
@@ -1337,16 +1349,22 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
             double a[8], v[8];
 #pragma unroll
             for (int c = 0; c < 8; ++c) { a[c] = (c <= r) ? Dg[(size_t)r * pitch + c] : 0.0; v[c] = (c == r) ? 1.0 : 0.0; }
+            const double d0 = Aw[(size_t)(sJ + r) * pitch + Wr];          // A_rr before any elimination
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
                 double piv = __shfl_sync(FULL, a[c], c);
-                // A = T~^T D^-1 T~ + H^T R^-1 H is positive semi-definite by construction, so a pivot at
-                // or below the rounding level of the largest pivot seen is cancellation noise, not
-                // indefiniteness: pin that variable (counted) instead of failing.  NaN / inf still fail.
+                const double orig = __shfl_sync(FULL, d0, c);
+                // A = T~^T D^-1 T~ + H^T R^-1 H is positive (semi-)definite by construction.
                 bool pin = false;
+                // The scale a pivot is judged against: the largest pivot so far, or the row's own diagonal before
+                // elimination (row scales differ by up to 1e10 when some D sit on the variance floor).  At or below the
+                // rounding level of that scale the pivot is cancellation noise of either sign: pinned.  A clearly negative
+                // pivot means the matrix handed in is indefinite (bad factors): fail like the reference's Cholesky
+                // (kernels.py:192-195).  NaN / inf fail.
+                const double scale = fmax(pivmax, orig);
                 if (!(piv == piv) || !(fabs(piv) < DBL_MAX)) { if (lane == 0) s_fail = 2; }
-                else if (!(piv > 1e-13 * pivmax)) {
-                    if (pivmax == 0.0) { if (lane == 0) s_fail = 1; }           // non-positive leading entry
+                else if (!(piv > 1e-13 * scale)) {
+                    if ((pivmax == 0.0 && !(piv > 0.0)) || piv < -1e-8 * scale) { if (lane == 0) s_fail = 1; }
                     else { pin = true; if (lane == 0) atomicAdd(P.counter + 1, 1u); }
                 }
                 pivmax = fmax(pivmax, piv);
@@ -1745,6 +1763,40 @@ cudaError_t launch_precision_apply(const int64_t *row_ptr, const int32_t *col_id
     if (blocks > 148 * 16) blocks = 148 * 16;
     precision_apply_kernel<<<(unsigned)blocks, 256, 0, s>>>(0, row_ptr, col_idx, nullptr, T, D, V, Wtmp, n, ncols);
     precision_apply_kernel<<<(unsigned)blocks, 256, 0, s>>>(1, csc_ptr, csc_row, csc_src, T, D, Wtmp, Out, n, ncols);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------------
+// Unit-triangular solves with many right-hand sides (factors.py:98-134: sqrt_solve, covariance_apply).
+// One thread per right-hand-side column walks the rows in dependency order; the row's sparse entries
+// are shared by all columns (broadcast loads), B is [n][ncols] (column index fastest: coalesced).
+//   transposed = 0:  (I + L) X = diag(scale_in) B          forward substitution over CSR rows
+//   transposed = 1:  (I + L)^T X = B, then X *= scale_out   backward substitution over CSC columns
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) unit_tri_solve_kernel(int transposed, const int64_t *__restrict__ ptr,
+                                                            const int32_t *__restrict__ idx, const int64_t *__restrict__ src,
+                                                            const double *__restrict__ T, const double *__restrict__ scale_in,
+                                                            const double *__restrict__ scale_out, double *__restrict__ B,
+                                                            int64_t n, int64_t ncols) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= ncols) return;
+    for (int64_t k = 0; k < n; ++k) {
+        const int64_t r = transposed ? n - 1 - k : k;
+        double acc = B[r * ncols + c];
+        if (scale_in) acc *= scale_in[r];
+        for (int64_t e = ptr[r]; e < ptr[r + 1]; ++e)
+            acc = fma(-T[src ? src[e] : e], B[(int64_t)idx[e] * ncols + c], acc);
+        B[r * ncols + c] = acc;
+    }
+    if (scale_out)
+        for (int64_t r = 0; r < n; ++r) B[r * ncols + c] *= scale_out[r];
+}
+
+cudaError_t launch_unit_tri_solve(int transposed, const int64_t *ptr, const int32_t *idx, const int64_t *src, const double *T,
+                                  const double *scale_in, const double *scale_out, double *B, int64_t n, int64_t ncols,
+                                  cudaStream_t s) {
+    if (n == 0 || ncols == 0) return cudaSuccess;
+    unit_tri_solve_kernel<<<(unsigned)((ncols + 127) / 128), 128, 0, s>>>(transposed, ptr, idx, src, T, scale_in, scale_out, B, n, ncols);
     return cudaGetLastError();
 }
 

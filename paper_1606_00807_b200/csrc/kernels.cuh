@@ -79,5 +79,9 @@ cudaError_t launch_scatter_rows(double *dst, const int64_t *dst_rows, const doub
 cudaError_t launch_precision_apply(const int64_t *row_ptr, const int32_t *col_idx, const int64_t *csc_ptr,
                                    const int32_t *csc_row, const int64_t *csc_src, const double *T, const double *D,
                                    const double *V, double *Wtmp, double *Out, int64_t n, int64_t ncols, cudaStream_t s);
+// unit-triangular solves with the strictly-lower pattern of a single-tile plan (see unit_tri_solve_kernel)
+cudaError_t launch_unit_tri_solve(int transposed, const int64_t *ptr, const int32_t *idx, const int64_t *src, const double *T,
+                                  const double *scale_in, const double *scale_out, double *B, int64_t n, int64_t ncols,
+                                  cudaStream_t s);
 cudaError_t launch_fp64_peak(double *out, int iters, int sm_count, cudaStream_t s);
 cudaError_t launch_dmma_peak(double *out, int iters, int sm_count, cudaStream_t s);

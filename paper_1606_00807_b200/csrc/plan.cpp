@@ -27,9 +27,15 @@ extern "C" const char *enkfmc_version(void) { return "enkfmc 0.1 (sm_100a)"; }
 
 namespace {
 
+// periodic flag of the C-ABI: 0 clipped, 1 periodic on both axes (the reference's two boundaries, geometry.py:43), 2 periodic
+// along x only (columns: longitude periodic, latitude clipped -- BASELINE.json config 1 as worded), 3 along y only.  The
+// per-axis forms have no reference counterpart: they apply the reference's per-axis rules (geometry.py:132-142) with one
+// flag per axis.
 struct Geo {
     int64_t nx, ny;
-    bool row_major, periodic;
+    bool row_major, periodic_x, periodic_y;
+    Geo(int64_t nx_, int64_t ny_, bool rm, int periodic)
+        : nx(nx_), ny(ny_), row_major(rm), periodic_x(periodic == 1 || periodic == 2), periodic_y(periodic == 1 || periodic == 3) {}
     int64_t label(int64_t r, int64_t c) const { return row_major ? r * nx + c : c * ny + r; }
     void coords(int64_t lab, int64_t &r, int64_t &c) const {
         if (row_major) { r = lab / nx; c = lab % nx; } else { c = lab / ny; r = lab % ny; }
@@ -87,8 +93,8 @@ void box_members(const Geo &g, int64_t center, int64_t zeta, std::vector<int64_t
                  std::vector<int64_t> &rows, std::vector<int64_t> &cols) {
     int64_t r, c;
     g.coords(center, r, c);
-    axis_window(r, zeta, g.ny, g.periodic, rows);
-    axis_window(c, zeta, g.nx, g.periodic, cols);
+    axis_window(r, zeta, g.ny, g.periodic_y, rows);
+    axis_window(c, zeta, g.nx, g.periodic_x, cols);
     label_product(g, rows, cols, out);
 }
 
@@ -144,7 +150,7 @@ int64_t find_sorted(const int64_t *a, int64_t n, int64_t v) {
 
 // Everything downstream of (tile_ptr, local_order, phys): rows, bandwidths, column lists, orders.
 void build_rows_from_geometry(enkfmc_plan &p) {
-    Geo g{p.nx, p.ny, p.row_major != 0, p.periodic != 0};
+    Geo g{p.nx, p.ny, p.row_major != 0, p.periodic};
     const int64_t total = p.sum_nlocal();
     p.row_ptr.assign(1, 0);
     p.col_idx.clear();
@@ -358,7 +364,7 @@ extern "C" int enkfmc_local_box(int64_t nx, int64_t ny, int row_major, int perio
         enkfmc_set_error("index " + std::to_string(center) + " outside [0, " + std::to_string(nx * ny) + ")");
         return ENKFMC_E_VALUE;
     }
-    Geo g{nx, ny, row_major != 0, periodic != 0};
+    Geo g{nx, ny, row_major != 0, periodic};
     std::vector<int64_t> box, rows, cols;
     box_members(g, center, zeta, box, rows, cols);
     std::copy(box.begin(), box.end(), out);
@@ -392,7 +398,7 @@ extern "C" int enkfmc_plan_create(int64_t nx, int64_t ny, int row_major, int per
     p->nx = nx; p->ny = ny; p->row_major = row_major; p->periodic = periodic; p->nfields = nfields;
     p->delta = delta; p->zeta = zeta; p->pr = pr; p->pc = pc; p->kind = 0;
     p->ntiles = delta; p->n2d = nx * ny; p->nstate2d = nx * ny;
-    Geo g{nx, ny, row_major != 0, periodic != 0};
+    Geo g{nx, ny, row_major != 0, periodic};
 
     std::vector<std::pair<int64_t, int64_t>> rb, cb;
     bands(ny, pr, rb);
@@ -408,8 +414,8 @@ extern "C" int enkfmc_plan_create(int64_t nx, int64_t ny, int row_major, int per
             for (int64_t r = rb[bi].first; r < rb[bi].second; ++r) rows_in.push_back(r);
             for (int64_t c = cb[bj].first; c < cb[bj].second; ++c) cols_in.push_back(c);
             label_product(g, rows_in, cols_in, inter);
-            axis_band(rb[bi].first, rb[bi].second, zeta, ny, g.periodic, rows_s, rows_w);
-            axis_band(cb[bj].first, cb[bj].second, zeta, nx, g.periodic, cols_s, cols_w);
+            axis_band(rb[bi].first, rb[bi].second, zeta, ny, g.periodic_y, rows_s, rows_w);
+            axis_band(cb[bj].first, cb[bj].second, zeta, nx, g.periodic_x, cols_s, cols_w);
             label_product(g, rows_s, cols_s, cover);   // == union1d(interior, halo): sorted local_order
             const int64_t base = (int64_t)p->local_order.size();
             p->local_order.insert(p->local_order.end(), cover.begin(), cover.end());
@@ -544,18 +550,18 @@ extern "C" int enkfmc_plan_set_observations(enkfmc_plan *p, int64_t nobs, const 
         for (int64_t k = 0; k < nobs; ++k) lists[0].push_back({obs[k], k});
     } else {
         // which block rows / block columns have coordinate v inside their extended band
-        Geo g{p->nx, p->ny, p->row_major != 0, p->periodic != 0};
+        Geo g{p->nx, p->ny, p->row_major != 0, p->periodic};
         std::vector<std::pair<int64_t, int64_t>> rb, cb;
         bands(p->ny, p->pr, rb);
         bands(p->nx, p->pc, cb);
         std::vector<std::vector<int32_t>> row_blocks(p->ny), col_blocks(p->nx);
         std::vector<int64_t> s, w;
         for (int64_t bi = 0; bi < p->pr; ++bi) {
-            axis_band(rb[bi].first, rb[bi].second, p->zeta, p->ny, g.periodic, s, w);
+            axis_band(rb[bi].first, rb[bi].second, p->zeta, p->ny, g.periodic_y, s, w);
             for (int64_t v : s) row_blocks[v].push_back((int32_t)bi);
         }
         for (int64_t bj = 0; bj < p->pc; ++bj) {
-            axis_band(cb[bj].first, cb[bj].second, p->zeta, p->nx, g.periodic, s, w);
+            axis_band(cb[bj].first, cb[bj].second, p->zeta, p->nx, g.periodic_x, s, w);
             for (int64_t v : s) col_blocks[v].push_back((int32_t)bj);
         }
         for (int64_t k = 0; k < nobs; ++k) {

@@ -81,6 +81,13 @@ def analysis_device(plan, dX, dR, dYs, dXa, rank_tol: float = 1e-8, variance_flo
     return dXa
 
 
+def check_status(plan) -> int:
+    """Outcome of the last analysis on this plan: synchronises; raises NumericalError naming the sub-domain if a
+    tile's factorisation failed (kernels.py:192-195); returns the number of clamped Cholesky pivots."""
+    _lib.check(_lib.lib().enkfmc_plan_check_status(plan.handle))
+    return plan.counter(5)
+
+
 _PINNED_POOL: list = []   # [tensor, weakref-to-the-array-handed-out]
 
 

@@ -14,7 +14,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import device
-from .errors import ConfigurationError, ConsistencyError
+from .errors import ConfigurationError, ConsistencyError, NumericalError
 from .geometry import GridGeometry, Subdomain
 from .kernels import EnsembleState, ObservationNetwork, perturb_observations
 from .plan import get_plan
@@ -136,4 +136,103 @@ def assimilate_parallel(Xb: EnsembleState, net: ObservationNetwork, cfg: Assimil
     out = object.__new__(EnsembleState)
     object.__setattr__(out, "X", Xa)
     object.__setattr__(out, "role", "analysis")
+    return out, report
+
+
+_SHARDED: dict = {}     # (geometry, delta, zeta, rank, world) -> (plan, shard, device buffers)
+
+
+def assimilate_parallel_sharded(Xb: EnsembleState | None, net: ObservationNetwork, cfg: AssimilationConfig,
+                                geometry: GridGeometry, *, Ys: np.ndarray | None = None, cycle: int = 0,
+                                root: int = 0, nens: int | None = None):
+    """assimilate_parallel (driver.py:159-253) over the ranks of an initialised torch.distributed process group, one
+    process per GPU.  The sub-domains are split by contiguous block rows (distributed.TileShard); ``root`` holds the
+    background and the perturbed observations on the host (the other ranks pass ``Xb=None`` and ``nens``), uploads
+    them, scatters to every rank the state rows and observation rows its tiles read, every rank analyses its tiles,
+    and the interior rows are all-gathered.  Returns ``(EnsembleState, CycleReport)`` on ``root`` and ``(None, report)``
+    elsewhere.  A failing sub-domain raises NumericalError on every rank."""
+    import torch
+    import torch.distributed as dist
+
+    from . import distributed
+
+    t_start = time.perf_counter()
+    rank, world = dist.get_rank(), dist.get_world_size()
+    if cfg.method != "enkf_mc_primal":
+        raise ConfigurationError(f"method {cfg.method!r} is outside the B200 hot path; only 'enkf_mc_primal' is built")
+    if rank == root:
+        if Xb is None:
+            raise ValueError("the root rank must pass the background ensemble")
+        if Xb.nstate != geometry.nstate:
+            raise ValueError(f"state dimension {Xb.nstate} does not match geometry {geometry.nstate}")
+        nens = Xb.nens
+        if Ys is None:
+            Ys = perturb_observations(net, nens, cfg.seed, cycle).Ys
+        Ys = np.ascontiguousarray(Ys, dtype=np.float64)
+        if Ys.shape != (net.nobs, nens):
+            raise ValueError(f"Ys has shape {Ys.shape}, expected {(net.nobs, nens)}")
+    elif nens is None:
+        raise ValueError("ranks other than the root must pass nens")
+    if nens < 2:
+        raise ConfigurationError(f"ensemble size must be at least 2, got {nens}")
+    if net.nobs and net.obs_indices[-1] >= geometry.nstate:
+        raise ValueError("observation indices exceed the state dimension")
+
+    key = (geometry, cfg.delta, cfg.zeta, rank, world)
+    ent = _SHARDED.get(key)
+    if ent is None or ent[2]["nens"] != nens or ent[2]["nobs"] != net.nobs:
+        from .plan import Plan
+        plan = Plan.decomposed(geometry, cfg.delta, cfg.zeta)
+        shard = distributed.TileShard(plan, geometry, rank, world)
+        shard.apply()
+        bufs = {"nens": nens, "nobs": net.nobs,
+                "X": torch.empty((geometry.nstate, nens), dtype=torch.float64, device="cuda"),
+                "Xa": torch.empty((geometry.nstate, nens), dtype=torch.float64, device="cuda"),
+                "Ys": torch.empty((max(net.nobs, 1), nens), dtype=torch.float64, device="cuda")}
+        ent = _SHARDED[key] = (plan, shard, bufs)
+    plan, shard, bufs = ent
+    plan.set_observations(net.obs_indices)
+    if shard.need_obs is None or bufs.get("obs_key") != plan._obs_key:
+        shard.set_observations(net.obs_indices)
+        bufs["obs_key"] = plan._obs_key
+        bufs["R"] = device.to_device(np.ascontiguousarray(net.r_diag))
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    ev[0].record()
+    if rank == root:
+        bufs["X"].copy_(torch.from_numpy(np.ascontiguousarray(Xb.X)), non_blocking=True)
+        if net.nobs:
+            bufs["Ys"][: net.nobs].copy_(torch.from_numpy(Ys), non_blocking=True)
+    shard.scatter_background(bufs["X"], bufs["Ys"], root=root)
+    ev[1].record()
+    device.analysis_device(plan, bufs["X"], bufs["R"], bufs["Ys"], bufs["Xa"])
+    ev[2].record()
+    shard.gather_analysis(bufs["Xa"])
+    failed = torch.zeros(1, dtype=torch.int32, device="cuda")
+    err = None
+    try:
+        device.check_status(plan)
+    except NumericalError as exc:           # raise on every rank, naming the sub-domain where one is known
+        err = exc
+        failed += 1
+    dist.all_reduce(failed, op=dist.ReduceOp.MAX)
+    if int(failed.item()):
+        raise err if err is not None else NumericalError("primal analysis solve failed in a sub-domain of another rank")
+    out = None
+    if rank == root:
+        Xa = device.pinned_empty((geometry.nstate, nens))
+        torch.from_numpy(Xa).copy_(bufs["Xa"], non_blocking=True)
+    ev[3].record()
+    torch.cuda.synchronize()
+    if rank == root:
+        out = object.__new__(EnsembleState)
+        object.__setattr__(out, "X", Xa)
+        object.__setattr__(out, "role", "analysis")
+    delta = plan.ntiles
+    t_est = ev[1].elapsed_time(ev[2]) * 1e-3
+    report = CycleReport(
+        cycle=int(cycle), method=cfg.method, delta=cfg.delta, workers=cfg.workers,
+        t_estimation=np.full(delta, t_est / delta), t_analysis=np.zeros(delta),
+        t_merge=ev[2].elapsed_time(ev[3]) * 1e-3, t_total=time.perf_counter() - t_start,
+        t_h2d=ev[0].elapsed_time(ev[1]) * 1e-3, t_d2h=0.0,
+    )
     return out, report

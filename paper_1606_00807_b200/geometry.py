@@ -18,7 +18,11 @@ from .errors import ConfigurationError
 
 KINDS = ("ring1d", "grid2d")
 ORDERINGS = ("row_major", "column_major")
-BOUNDARIES = ("clipped", "periodic")
+# "clipped" / "periodic" are the reference's two boundaries (geometry.py:43).  "periodic_x" (longitude periodic, latitude
+# clipped: BASELINE.json config 1 as worded) and "periodic_y" apply the reference's per-axis rules (geometry.py:132-142) with
+# one flag per axis; they have no reference counterpart (parity unpinned by the reference, checked against the extended oracle).
+BOUNDARIES = ("clipped", "periodic", "periodic_x", "periodic_y")
+_PERIODIC_CODE = {"clipped": 0, "periodic": 1, "periodic_x": 2, "periodic_y": 3}
 
 
 @dataclass(frozen=True)
@@ -55,8 +59,9 @@ class GridGeometry:
         return self.nx * self.ny * self.nfields
 
     @property
-    def periodic(self) -> bool:
-        return self.boundary == "periodic"
+    def periodic(self) -> int:
+        """Boundary code of the C-ABI: 0 clipped, 1 periodic (both axes), 2 periodic along x only, 3 along y only."""
+        return _PERIODIC_CODE[self.boundary]
 
     @property
     def row_major(self) -> bool:

@@ -140,3 +140,31 @@ def analysis_primal(Xb: EnsembleState, factors: PrecisionFactors, net: Observati
         why = "matrix not positive definite" if status == 1 else "non-finite pivot"
         raise NumericalError(f"primal analysis solve failed: {why}")
     return EnsembleState(dXa.cpu().numpy(), role="analysis")
+
+
+def analysis_dual(Xb: EnsembleState, factors: PrecisionFactors, net: ObservationNetwork, Ys: np.ndarray) -> EnsembleState:
+    """Observation-space analysis through the covariance square root (kernels.py:221-248): with T X = D^{1/2} I and
+    V = H X, Xa = Xb + X V^T (R + V V^T)^-1 (Ys - H Xb) -- the primal route by Sherman-Morrison-Woodbury.
+
+    The square root comes from the device unit-triangular solve (``enkfmc_unit_tri_solve``); the nobs x nobs
+    observation-space system is a plain dense symmetric solve and goes through the library (torch.linalg on the
+    device).  This is the second, independent route of the primal == dual self-check, not the timed hot path."""
+    import torch
+
+    Ys = _check_analysis_inputs(Xb, factors, net, Ys)
+    if net.nobs == 0:
+        return EnsembleState(Xb.X.copy(), role="analysis")
+    n = factors.n
+    dXs = factors._tri_solve(device.to_device(np.eye(n)), False, scale_in=device.to_device(np.sqrt(factors.variances)))
+    obs = torch.from_numpy(np.ascontiguousarray(net.obs_indices)).cuda()
+    v = dXs.index_select(0, obs)
+    g = v @ v.T
+    g.diagonal().add_(device.to_device(net.r_diag))
+    dX = device.to_device(Xb.X)
+    innovations = device.to_device(np.ascontiguousarray(Ys)) - dX.index_select(0, obs)
+    chol, info = torch.linalg.cholesky_ex(g)
+    if int(info.item()) != 0:
+        raise NumericalError(f"dual observation-space solve failed: leading minor {int(info.item())} is not positive definite")
+    w = torch.cholesky_solve(innovations, chol)
+    dx = dXs @ (v.T @ w)
+    return EnsembleState((dX + dx).cpu().numpy(), role="analysis")

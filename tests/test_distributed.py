@@ -31,9 +31,30 @@ def _worker(rank, world, port, nfields, out):
     shard = distributed.TileShard(plan, geo, rank, world)
     shard.apply()
     assert sum(b - a for a, b in shard.tile_ranges) == plan.ntiles
-    X = torch.from_numpy(w.X.copy()) if rank == 0 else torch.zeros(w.X.shape, dtype=torch.float64)
-    shard.broadcast_background(X)
-    assert np.array_equal(X.numpy(), w.X)
+    # slab scatter: every rank receives exactly the rows its tiles read (interiors + halos, all fields) and the rows of
+    # the perturbed observations inside them; everything else stays untouched
+    from paper_1606_00807_b200.plan import LOCAL_ORDER, TILE_PTR
+    shard.set_observations(w.obs_indices)
+    X = torch.from_numpy(w.X.copy()) if rank == 0 else torch.full(w.X.shape, float("nan"), dtype=torch.float64)
+    Ys = torch.from_numpy(w.Ys.copy()) if rank == 0 else torch.full(w.Ys.shape, float("nan"), dtype=torch.float64)
+    shard.scatter_background(X, Ys)
+    tp, lo = plan.get(TILE_PTR), plan.get(LOCAL_ORDER)
+    t0, t1 = shard.tile_ranges[rank]
+    read2d = np.unique(lo[tp[t0]:tp[t1]])
+    read = (np.arange(nfields)[:, None] * geo.n2d + read2d[None, :]).ravel()
+    assert np.array_equal(shard.need[rank], read)
+    assert np.array_equal(X.numpy()[read], w.X[read])
+    obs_read = np.flatnonzero(np.isin(w.obs_indices, read))
+    assert np.array_equal(shard.need_obs[rank], obs_read)
+    assert np.array_equal(Ys.numpy()[obs_read], w.Ys[obs_read])
+    if rank != 0:
+        untouched = np.setdiff1d(np.arange(geo.nstate), read)
+        assert np.all(np.isnan(X.numpy()[untouched]))
+        assert read.size < geo.nstate                      # a slab, not the whole ensemble
+    for _ in range(2):                                     # buffers are reused: a second exchange gives the same result
+        shard.scatter_background(X, Ys)
+    assert np.array_equal(X.numpy()[read], w.X[read])
+    assert 0.0 < shard.memory_fraction() < 1.0
     # owned tiles analysed by the oracle, everything else poisoned
     grid = orc.Grid(w.nx, w.ny, nfields=nfields)
     full = orc.assimilate(w.X, w.obs_indices, w.r_diag, w.Ys, grid, w.delta, w.zeta)

@@ -1,8 +1,7 @@
 """-m gpu: the BASELINE.json configurations at their full sizes.
 
-cfg1 / cfg2 / cfg4(r=2) are small enough for the CPU oracle (seconds), so they are compared with it
-directly: strict gates on the 1 % nugget variants, the documented input noise floor on the smooth
-ones.  cfg3 (534 528 components, the benchmark workload) is checked through
+Every configuration is compared with the CPU oracle in tests/test_gpu_baseline.py (gates from the oracle's
+measured noise floor).  Here cfg3 (534 528 components, the benchmark workload, all 29 fields) is checked through
 size-independent properties of the analysis: exact fixed point at zero innovation, bitwise
 run-to-run determinism, independence of the stacked fields, linearity in the innovations and
 untouched interiors where a tile sees no observation."""
@@ -31,36 +30,6 @@ def _run(mck, w, Ys=None, X=None, obs=None):
     xa, rep = mck.assimilate_parallel(mck.EnsembleState(w.X if X is None else X), net,
                                       mck.AssimilationConfig(zeta=w.zeta, delta=w.delta), geo, Ys=Ys)
     return xa.X, geo
-
-
-@pytest.mark.parametrize("name,kw,gates", [
-    ("cfg1", {}, (1e-9, 1e-9, 1e-8)),
-    ("cfg1", {"nugget": 0.01}, (1e-9, 1e-9, 1e-8)),
-    # periodic seams have p = 24 > N - 1 = 19 predecessors: rank deficient by construction, D on the 1e-10
-    # floor, cond(A) ~ 1e15 -- Xa is only defined to the input noise floor there
-    ("cfg1", {"boundary": "periodic", "nugget": 0.01}, (1e-9, 1e-8, 1e-2)),
-    ("cfg2", {"nugget": 0.01}, (1e-9, 1e-9, 1e-8)),
-    ("cfg2", {}, (5e-9, 5e-9, 1e-2)),                 # smooth inputs: T/D at the cond*eps floor, Xa at the input noise floor
-    ("cfg4", {"zeta": 2}, (1e-9, 1e-9, 1e-8)),
-])
-def test_config_against_oracle(mck, name, kw, gates):
-    from oracle import enkf_mc_oracle as orc
-    from paper_1606_00807_b200 import device, synthetic
-    from paper_1606_00807_b200.plan import COL_IDX, LOCAL_ORDER, get_plan
-    w = synthetic.config(name, **kw)
-    xa, geo = _run(mck, w)
-    grid = orc.Grid(w.nx, w.ny, True, w.boundary == "periodic")
-    ref, kept = orc.assimilate(w.X, w.obs_indices, w.r_diag, w.Ys, grid, w.delta, w.zeta, keep_tiles=True)
-    plan = get_plan(geo, w.delta, w.zeta)
-    assert np.array_equal(plan.get(LOCAL_ORDER), np.concatenate([r.tile.local_order for r in kept[0]]))
-    assert np.array_equal(plan.get(COL_IDX), np.concatenate([r.factors.indices for r in kept[0]]))
-    T = device.workspace_tensor(plan, 1, (plan.nnz,))
-    D = device.workspace_tensor(plan, 2, (plan.sum_nlocal,))
-    tref = np.concatenate([r.factors.data for r in kept[0]])
-    dref = np.concatenate([r.factors.d for r in kept[0]])
-    assert relerr(T, tref) < gates[0], relerr(T, tref)
-    assert np.max(np.abs(D - dref) / dref) < gates[1]
-    assert relerr(xa, ref) < gates[2], relerr(xa, ref)
 
 
 @pytest.fixture(scope="module")

@@ -16,9 +16,23 @@ from conftest import relerr
 pytestmark = pytest.mark.gpu
 
 T_GATE, D_GATE, XA_GATE = 1e-9, 1e-9, 1e-8
-# case -> (T gate, D gate, Xa gate); a0,a1,a3 carry a 1 % nugget (well conditioned, strict gates)
-CASE_GATES = {0: (T_GATE, D_GATE, XA_GATE), 1: (T_GATE, D_GATE, XA_GATE), 2: (T_GATE, D_GATE, XA_GATE),
-              3: (T_GATE, D_GATE, XA_GATE), 4: (T_GATE, D_GATE, 1e-6), 5: (1e-8, D_GATE, 1e-3)}
+# case -> (T gate, D gate, Xa gate) = max(north_star gate, 10 x the oracle's measured noise floor on that input)
+# (tests/golden/noise_floors.json, tools/make_floors.py); a0, a1, a3 carry a 1 % nugget and a2 is small: strict gates.
+import json
+import os
+
+from conftest import GOLDEN
+
+_FL = json.load(open(os.path.join(GOLDEN, "noise_floors.json")))
+
+
+def _gate(key):
+    f = _FL[key]
+    return max(T_GATE, 10.0 * f["T"]), max(D_GATE, 10.0 * f["D"]), max(XA_GATE, 10.0 * f["Xa"])
+
+
+CASE_GATES = {0: (T_GATE, D_GATE, XA_GATE), 1: (T_GATE, D_GATE, XA_GATE), 2: _gate("golden_a2"),
+              3: (T_GATE, D_GATE, XA_GATE), 4: _gate("golden_a4"), 5: _gate("golden_a5")}
 
 
 @pytest.fixture(scope="module")
@@ -404,3 +418,105 @@ def test_changing_networks_orderings_and_empty_fields(mck):
                                                                                     boundary="periodic"), 6, 2)[2:5]])
         rows = (np.arange(nf)[:, None] * w.n2d + own[None, :]).ravel()
         assert np.array_equal(part.X[rows], full.X[rows])
+
+
+def test_tile_range_on_a_fresh_plan_and_indefinite_factors(mck):
+    """(i) A tile range set on a brand-new plan before its first analysis: the unowned tiles' status words must not
+    leak into the result (they are cleared at the start of every analysis).  (ii) Factors that make A indefinite
+    (negative D through the C-ABI) fail with NumericalError like the reference's Cholesky (kernels.py:192-195)
+    instead of being pinned silently."""
+    import torch
+    from oracle import enkf_mc_oracle as orc
+    from paper_1606_00807_b200 import device, synthetic
+    from paper_1606_00807_b200.plan import Plan
+    w = synthetic.make_workload("fresh", nx=24, ny=16, nens=30, corr_len=3.0, zeta=2, delta=8, obs="lattice", obs_arg=2,
+                                r_rel=None, r_abs=0.05, seed=21, nugget=0.01)
+    geo = mck.GridGeometry("grid2d", w.nx, w.ny)
+    ref = orc.assimilate(w.X, w.obs_indices, w.r_diag, w.Ys, orc.Grid(w.nx, w.ny), w.delta, w.zeta)
+    for attempt in range(3):                      # fresh device allocations each time
+        plan = Plan.decomposed(geo, w.delta, w.zeta)
+        plan.set_observations(w.obs_indices)
+        plan.set_tile_range(3, 6)
+        Xa, _ = device.analysis_host(plan, w.X, w.r_diag, w.Ys)
+        own = np.concatenate([sd.interior for sd in mck.decompose(geo, w.delta, w.zeta)[3:6]])
+        assert relerr(Xa[own], ref[own]) < XA_GATE
+        assert device.check_status(plan) == 0
+        del plan
+    # (ii)
+    plan = Plan.decomposed(geo, w.delta, w.zeta)
+    plan.set_observations(w.obs_indices)
+    dX = device.to_device(w.X)
+    dU = device.center_rows_device(dX)
+    dT, dD, _ = device.regress_device(plan, dU, 1e-8, 1e-10)
+    dR, dYs = device.to_device(w.r_diag), device.to_device(w.Ys)
+    _, st = device.local_solve_device(plan, dX, dT, dD, dR, dYs)
+    torch.cuda.synchronize()
+    assert int(st.abs().sum().item()) == 0
+    bad = dD.clone()
+    bad[5] = -1e-8                                 # row 5 of tile 0: a negative "variance" that dominates A[5, 5]
+    _, st = device.local_solve_device(plan, dX, dT, bad, dR, dYs)
+    torch.cuda.synchronize()
+    st = st.cpu().numpy()
+    assert st[0] != 0 and np.all(st[1:] == 0), st
+
+
+def test_sqrt_solve_covariance_apply_and_primal_equals_dual(mck):
+    """the unit-triangular multi-right-hand-side solves behind PrecisionFactors.sqrt_solve /
+    covariance_apply (factors.py:98-134) against dense formulas, and the reference's own self-check that the primal
+    and the dual analysis agree (pkg/tests/test_acceptance.py:81-109) -- both routes on the device."""
+    from oracle import enkf_mc_oracle as orc
+    from paper_1606_00807_b200 import synthetic
+    w = synthetic.make_workload("dual", nx=18, ny=12, nens=24, corr_len=3.0, zeta=2, delta=1, obs="random", obs_arg=0.35,
+                                r_rel=None, r_abs=0.1, seed=31, nugget=0.05)
+    geo = mck.GridGeometry("grid2d", w.nx, w.ny)
+    f = mck.fit_factors(orc.center_rows(w.X), geo, w.zeta)
+    n = f.n
+    t = np.eye(n) + f.lower.toarray()
+    d = f.variances
+    rng = np.random.default_rng(3)
+    rhs = rng.standard_normal((n, 7))
+    x = f.sqrt_solve(rhs)
+    assert relerr(x, np.linalg.solve(t, np.sqrt(d)[:, None] * rhs)) < 1e-12
+    assert relerr(f.sqrt_solve(rhs[:, 0]), x[:, 0]) < 1e-15                      # 1-D right-hand side
+    sq = f.sqrt_solve(np.eye(n))
+    cov = np.linalg.solve(t, np.linalg.solve(t, np.diag(d)).T).T                  # T^-1 D T^-T
+    assert relerr(sq @ sq.T, cov) < 1e-11
+    assert relerr(f.covariance_apply(rhs), cov @ rhs) < 1e-11
+    assert relerr(f.precision_apply(f.covariance_apply(rhs)), rhs) < 1e-9        # B^-1 B = I
+    with pytest.raises(ValueError, match="leading dimension"):
+        f.sqrt_solve(np.zeros(n + 1))
+    net = mck.ObservationNetwork(w.obs_indices, w.r_diag, w.y)
+    xb = mck.EnsembleState(w.X)
+    xp = mck.analysis_primal(xb, f, net, w.Ys)
+    xd = mck.analysis_dual(xb, f, net, w.Ys)
+    assert relerr(xd.X, xp.X) < 1e-8, relerr(xd.X, xp.X)
+    empty = mck.ObservationNetwork(np.zeros(0, dtype=np.int64), np.zeros(0), np.zeros(0))
+    assert np.array_equal(mck.analysis_dual(xb, f, empty, np.zeros((0, w.nens))).X, w.X)
+
+
+def test_dump_factors_round_trip(mck, tmp_path):
+    """the triplet files of factors.py:148-166 written from device results, read back exactly."""
+    from oracle import enkf_mc_oracle as orc
+    from paper_1606_00807_b200 import device, synthetic
+    from paper_1606_00807_b200.plan import Plan
+    w = synthetic.make_workload("dump", nx=12, ny=8, nens=16, corr_len=2.0, zeta=1, delta=4, obs="lattice", obs_arg=2,
+                                r_rel=None, r_abs=0.1, seed=8, nugget=0.02)
+    geo = mck.GridGeometry("grid2d", w.nx, w.ny)
+    plan = Plan.decomposed(geo, w.delta, w.zeta)
+    plan.set_observations(w.obs_indices)
+    device.analysis_host(plan, w.X, w.r_diag, w.Ys)
+    paths = mck.dump_plan_factors(plan, str(tmp_path))
+    assert len(paths) == 4 and paths[2][0].endswith("T_subdomain2.txt")
+    tiles = orc.decompose(orc.Grid(w.nx, w.ny), w.delta, w.zeta)
+    for k, (tp, dp) in enumerate(paths):
+        ref = orc.fit_factors(orc.center_rows(w.X[tiles[k].local_order]), orc.Grid(w.nx, w.ny), w.zeta, tiles[k].local_order)
+        rows = [ln.split() for ln in open(tp)]
+        n = ref.n
+        dense = np.zeros((n, n))
+        for r, c, v in rows:
+            dense[int(r), int(c)] = float(v)
+        assert np.array_equal(np.diag(dense), np.ones(n)) and len(rows) == ref.indices.size + n
+        assert relerr(dense, ref.dense_unit_lower()) < 1e-9
+        assert [int(r[0]) for r in rows] == sorted(int(r[0]) for r in rows)            # row-major, diagonal last in its row
+        dvals = np.array([float(ln) for ln in open(dp)])
+        assert np.max(np.abs(dvals - ref.d) / ref.d) < 1e-9

@@ -162,3 +162,35 @@ def test_shared_regressions_are_identical_problems():
         owned = (tile_of >= 2) & (tile_of < 5)
         assert np.all(rep[~owned] == -1) and np.all(owned[rep[owned]])
         assert plan.n_owned_rows == int(owned.sum())
+
+
+def test_per_axis_boundary_against_extended_oracle():
+    """Longitude periodic / latitude clipped (BASELINE.json config 1 as worded) and the transposed case: the plan's index
+    maps against the extended oracle (the reference's per-axis rules, geometry.py:132-142, with one flag per axis).  The
+    reference has a single boundary flag: parity for the mixed cases is unpinned by the reference; the two reference
+    boundaries keep their bit-exact golden tests above."""
+    import paper_1606_00807_b200 as mck
+    from oracle import enkf_mc_oracle as orc
+    from paper_1606_00807_b200.plan import COL_IDX, LOCAL_ORDER, Plan
+    for boundary in ("periodic_x", "periodic_y"):
+        for ordering in ("row_major", "column_major"):
+            geo = mck.GridGeometry("grid2d", 20, 12, ordering=ordering, boundary=boundary)
+            grid = orc.grid_for(20, 12, boundary, row_major=ordering == "row_major")
+            assert grid.px == (boundary == "periodic_x") and grid.py == (boundary == "periodic_y")
+            plan = Plan.decomposed(geo, 6, 2)
+            tiles = orc.decompose(grid, 6, 2)
+            assert np.array_equal(plan.get(LOCAL_ORDER), np.concatenate([t.local_order for t in tiles]))
+            assert np.array_equal(plan.get(COL_IDX),
+                                  np.concatenate([orc.predecessor_csr(grid, 2, t.local_order)[1] for t in tiles]))
+            for sd, t in zip(mck.decompose(geo, 6, 2), tiles):
+                assert np.array_equal(sd.interior, t.interior) and np.array_equal(sd.halo, t.halo)
+            for c in (0, 19, 20 * 11, 239, 125):
+                assert np.array_equal(mck.predecessors(geo, c, 2), orc.predecessors(grid, c, 2))
+                assert np.array_equal(mck.local_box(geo, c, 2).members, orc.local_box(grid, c, 2))
+    # the seam: the last column sees the first two through the wrap (row-major labels, zeta = 2)
+    lon = mck.GridGeometry("grid2d", 20, 12, boundary="periodic_x")
+    assert mck.predecessors(lon, 19 + 20 * 5, 2).size == 14 and mck.predecessors(mck.GridGeometry("grid2d", 20, 12), 19 + 20 * 5, 2).size == 8
+    # brute-force definition of the box for one cell
+    r0, c0 = 5, 19
+    want = sorted(r * 20 + (c % 20) for r in range(max(0, r0 - 2), min(12, r0 + 3)) for c in range(c0 - 2, c0 + 3))
+    assert mck.local_box(lon, c0 + 20 * r0, 2).members.tolist() == sorted(set(want))

@@ -131,7 +131,7 @@ if __name__ == "__main__":
     ]
     for name, kw in cases:
         w = synthetic.make_workload("x", **kw)
-        grid = orc.Grid(w.nx, w.ny, True, w.boundary == "periodic")
+        grid = orc.grid_for(w.nx, w.ny, w.boundary)
         t = orc.decompose(grid, w.delta, w.zeta)[0]
         U = orc.center_rows(w.X[t.local_order])
         terr, rowerr, derr, st = compare_tile(U, grid, w.zeta, t.local_order)

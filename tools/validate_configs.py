@@ -46,7 +46,7 @@ def run(name, w, oracle_fields):
               f"no oracle; K2a {ms[1]:.2f} K2b {ms[2]:.2f} ms; listed {100 * tr.mean():.1f} %, sweeps mean {sw[tr].mean() if tr.any() else 0:.2f} max {sw.max()}, "
               f"block/8 hist {np.bincount(((flags >> 22) & 7)[tr]).tolist() if tr.any() else []}, why hist {np.bincount(((flags >> 5) & 7)[(flags & 16) > 0]).tolist()} |", flush=True)
         return
-    grid = orc.Grid(w.nx, w.ny, True, w.boundary == "periodic", w.nfields)
+    grid = orc.grid_for(w.nx, w.ny, w.boundary, w.nfields)
     t0 = time.perf_counter()
     ref, kept = orc.assimilate(w.X, w.obs_indices, w.r_diag, w.Ys, grid, w.delta, w.zeta, keep_tiles=True,
                                fields=oracle_fields)
@@ -83,6 +83,7 @@ for which in a.which.split(","):
         run("cfg1 clipped", synthetic.config("cfg1"), [0])
     elif which == "cfg1p":
         run("cfg1 periodic", synthetic.config("cfg1", boundary="periodic"), [0])
+        run("cfg1 longitude periodic, latitude clipped (as worded)", synthetic.config("cfg1", boundary="periodic_x"), [0])
     elif which == "cfg2":
         run("cfg2", synthetic.config("cfg2"), [0])
     elif which == "cfg2n":
