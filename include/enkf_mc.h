@@ -210,6 +210,14 @@ int enkfmc_precision_apply(enkfmc_plan *plan, const double *d_T, const double *d
 int enkfmc_unit_tri_solve(enkfmc_plan *plan, const double *d_T, int transposed, const double *d_scale_in,
                           const double *d_scale_out, double *d_B, int64_t ncols, void *stream);
 
+/* One explicit step of the periodic advection-diffusion forecast model on a device-resident ensemble
+ * ([nfields*nx*ny][nens], d_in != d_out): upwind advection, centred diffusion, unit grid -- the
+ * propagate hook of the device-resident cycle loop (models.py:114-132, driver.py:256-310).  Bit-identical
+ * to the reference's numpy expression. */
+int enkfmc_advdiff_step(const double *d_in, double *d_out, int64_t nx, int64_t ny, int row_major,
+                        int64_t nfields, int64_t nens, double ux, double uy, double dt, double kappa,
+                        void *stream);
+
 #ifdef __cplusplus
 }
 #endif

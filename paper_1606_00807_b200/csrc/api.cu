@@ -703,6 +703,19 @@ extern "C" int enkfmc_unit_tri_solve(enkfmc_plan *p, const double *d_T, int tran
     return ENKFMC_OK;
 }
 
+extern "C" int enkfmc_advdiff_step(const double *d_in, double *d_out, int64_t nx, int64_t ny, int row_major, int64_t nfields,
+                                   int64_t nens, double ux, double uy, double dt, double kappa, void *stream) {
+    int rc = check_nens(nens);
+    if (rc) return rc;
+    if (nx < 1 || ny < 1 || nfields < 1) { enkfmc_set_error("grid extents must be positive"); return ENKFMC_E_VALUE; }
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    CK(launch_advdiff_step(d_in, d_out, nx, ny, row_major, nfields, (int)nens, ux, uy, dt, kappa, sms, (cudaStream_t)stream));
+    return ENKFMC_OK;
+}
+
 extern "C" int enkfmc_plan_read_buffer(const enkfmc_plan *p, int what, void *host_out, int64_t bytes) {
     void *src = enkfmc_plan_device_buffer(p, what);
     if (!src) { enkfmc_set_error("workspace buffer not allocated"); return ENKFMC_E_VALUE; }

@@ -1801,6 +1801,44 @@ cudaError_t launch_unit_tri_solve(int transposed, const int64_t *ptr, const int3
 }
 
 // ------------------------------------------------------------------------------------------
+// Forecast step of the periodic advection-diffusion toy model (models.py:114-132) on the device-resident ensemble:
+// first-order upwind advection, centred diffusion, unit grid.  One thread per (cell, member); the member index is the
+// fastest, so the five neighbour rows are read coalesced.  The operation order is the reference's and nothing is
+// contracted into FMAs (round-to-nearest intrinsics), so a step is bit-identical to the numpy expression.
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) advdiff_step_kernel(const double *__restrict__ in, double *__restrict__ out, int64_t nx,
+                                                          int64_t ny, int row_major, int64_t nfields, int N, double ux,
+                                                          double uy, double dt, double kappa) {
+    const int64_t total = nx * ny * nfields * (int64_t)N;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int m = (int)(i % N);
+        const int64_t cell = i / N, f = cell / (nx * ny), lab = cell % (nx * ny);
+        const int64_t r = row_major ? lab / nx : lab % ny, c = row_major ? lab % nx : lab / ny;
+        auto at = [&](int64_t rr, int64_t cc) {
+            rr = (rr + ny) % ny; cc = (cc + nx) % nx;
+            const int64_t l = row_major ? rr * nx + cc : cc * ny + rr;
+            return in[((f * nx * ny) + l) * N + m];
+        };
+        const double u = at(r, c), un = at(r - 1, c), us = at(r + 1, c), uw = at(r, c - 1), ue = at(r, c + 1);
+        const double ddx = ux >= 0.0 ? __dsub_rn(u, uw) : __dsub_rn(ue, u);
+        const double ddy = uy >= 0.0 ? __dsub_rn(u, un) : __dsub_rn(us, u);
+        const double lap = __dsub_rn(__dadd_rn(__dadd_rn(__dadd_rn(un, us), uw), ue), __dmul_rn(4.0, u));
+        const double tend = __dadd_rn(__dsub_rn(__dmul_rn(-ux, ddx), __dmul_rn(uy, ddy)), __dmul_rn(kappa, lap));
+        out[i] = __dadd_rn(u, __dmul_rn(dt, tend));
+    }
+}
+
+cudaError_t launch_advdiff_step(const double *in, double *out, int64_t nx, int64_t ny, int row_major, int64_t nfields, int N,
+                                double ux, double uy, double dt, double kappa, int sm_count, cudaStream_t s) {
+    const int64_t total = nx * ny * nfields * (int64_t)N;
+    if (total == 0) return cudaSuccess;
+    int64_t blocks = (total + 255) / 256;
+    if (blocks > (int64_t)sm_count * 16) blocks = (int64_t)sm_count * 16;
+    advdiff_step_kernel<<<(unsigned)blocks, 256, 0, s>>>(in, out, nx, ny, row_major, nfields, N, ux, uy, dt, kappa);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------------
 // FP64 DFMA peak: 8 independent FMA chains per thread, register resident.
 // ------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) fp64_peak_kernel(double *out, int iters, double a, double b) {

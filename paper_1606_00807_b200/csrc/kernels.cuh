@@ -83,5 +83,7 @@ cudaError_t launch_precision_apply(const int64_t *row_ptr, const int32_t *col_id
 cudaError_t launch_unit_tri_solve(int transposed, const int64_t *ptr, const int32_t *idx, const int64_t *src, const double *T,
                                   const double *scale_in, const double *scale_out, double *B, int64_t n, int64_t ncols,
                                   cudaStream_t s);
+cudaError_t launch_advdiff_step(const double *in, double *out, int64_t nx, int64_t ny, int row_major, int64_t nfields, int N,
+                                double ux, double uy, double dt, double kappa, int sm_count, cudaStream_t s);
 cudaError_t launch_fp64_peak(double *out, int iters, int sm_count, cudaStream_t s);
 cudaError_t launch_dmma_peak(double *out, int iters, int sm_count, cudaStream_t s);

@@ -139,6 +139,70 @@ def assimilate_parallel(Xb: EnsembleState, net: ObservationNetwork, cfg: Assimil
     return out, report
 
 
+@dataclass
+class FilterResult:
+    """Outcome of a multi-cycle run (driver.py:272-279): per-cycle analyses and reports, plus the final propagated
+    background (X0 itself for an empty schedule)."""
+
+    analyses: list
+    reports: list
+    final: EnsembleState
+
+
+def run_filter(X0: EnsembleState, model, schedule, cfg: AssimilationConfig, *, keep_analyses: bool = True) -> FilterResult:
+    """Alternate analysis and propagation over a schedule of (window, network) cycles (driver.py:282-310) with the
+    ensemble resident on the device: per cycle only the perturbed observations -- generated on the host from the
+    reference's (seed, cycle) stream -- and the observation error variances are uploaded; the analysis is the
+    background of the next cycle after the device forecast step (models.propagate_device).  ``keep_analyses=False``
+    skips the per-cycle download of the analysis ensembles (the reference returns them all)."""
+    import torch
+
+    from .models import propagate_device
+    from .plan import Plan
+
+    geometry = model.geometry
+    if X0.nstate != geometry.nstate:
+        raise ValueError(f"state dimension {X0.nstate} does not match geometry {geometry.nstate}")
+    if X0.nens < 2:
+        raise ConfigurationError(f"ensemble size must be at least 2, got {X0.nens}")
+    if cfg.method != "enkf_mc_primal":
+        raise ConfigurationError(f"method {cfg.method!r} is outside the B200 hot path; only 'enkf_mc_primal' is built")
+    analyses, reports = [], []
+    if not schedule:
+        return FilterResult(analyses, reports, X0)
+    plan = Plan.decomposed(geometry, cfg.delta, cfg.zeta)      # owned by this run: the cached plan of assimilate_parallel stays untouched
+    dX = device.to_device(np.ascontiguousarray(X0.X))
+    dXa, dTmp = torch.empty_like(dX), torch.empty_like(dX)
+    for k, (window, net) in enumerate(schedule):
+        t0 = time.perf_counter()
+        if net.nobs and net.obs_indices[-1] >= geometry.nstate:
+            raise ValueError("observation indices exceed the state dimension")
+        Ys = np.ascontiguousarray(perturb_observations(net, X0.nens, cfg.seed, k).Ys)
+        plan.set_observations(net.obs_indices)
+        dYs = device.to_device(Ys if net.nobs else np.zeros((1, X0.nens)))
+        dR = device.to_device(np.ascontiguousarray(net.r_diag) if net.nobs else np.ones(1))
+        device.analysis_device(plan, dX, dR, dYs, dXa)
+        device.check_status(plan)
+        if keep_analyses:
+            out = object.__new__(EnsembleState)
+            object.__setattr__(out, "X", dXa.cpu().numpy())
+            object.__setattr__(out, "role", "analysis")
+            analyses.append(out)
+        nxt = propagate_device(model, dXa, dTmp, window)
+        if nxt is dXa:
+            dX, dXa = dXa, dX
+        else:                      # the forecast landed in dTmp
+            dX, dTmp = dTmp, dX
+        delta = plan.ntiles
+        t = time.perf_counter() - t0
+        reports.append(CycleReport(cycle=k, method=cfg.method, delta=cfg.delta, workers=cfg.workers,
+                                   t_estimation=np.zeros(delta), t_analysis=np.zeros(delta), t_merge=0.0, t_total=t,
+                                   t_h2d=0.0, t_d2h=0.0))
+    torch.cuda.synchronize()
+    final = EnsembleState(dX.cpu().numpy(), role="background")
+    return FilterResult(analyses, reports, final)
+
+
 _SHARDED: dict = {}     # (geometry, delta, zeta, rank, world) -> (plan, shard, device buffers)
 
 

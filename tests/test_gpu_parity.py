@@ -520,3 +520,51 @@ def test_dump_factors_round_trip(mck, tmp_path):
         assert [int(r[0]) for r in rows] == sorted(int(r[0]) for r in rows)            # row-major, diagonal last in its row
         dvals = np.array([float(ln) for ln in open(dp)])
         assert np.max(np.abs(dvals - ref.d) / ref.d) < 1e-9
+
+
+def test_run_filter_device_resident_cycles(mck):
+    """the device-resident cycle loop (driver.py:282-310) is bit-equal to calling assimilate_parallel cycle
+    by cycle with the forecast on the host -- identity model and the periodic advection-diffusion field, whose device
+    step (models.py:114-132) is bit-identical to the numpy expression restated here."""
+    from paper_1606_00807_b200 import synthetic
+    w = synthetic.make_workload("cyc", nx=24, ny=16, nens=20, corr_len=3.0, zeta=2, delta=4, obs="lattice", obs_arg=2,
+                                r_rel=None, r_abs=0.05, seed=44, nugget=0.02)
+    cfg = mck.AssimilationConfig(zeta=w.zeta, delta=w.delta, seed=99)
+    rng = np.random.default_rng(5)
+    nets = []
+    for k in range(3):                            # the network changes from cycle to cycle
+        idx = np.sort(rng.choice(w.n2d, 60 + 10 * k, replace=False))
+        nets.append(mck.ObservationNetwork(idx, np.full(idx.size, 0.05 ** 2), w.truth[idx] + 0.05 * rng.standard_normal(idx.size)))
+
+    def advdiff_host(model, X, steps):
+        g = model.geometry
+        out = X.copy()
+        ux, uy = model.velocity
+        for j in range(X.shape[1]):
+            u = out[:, j].reshape(g.ny, g.nx) if g.row_major else out[:, j].reshape(g.nx, g.ny).T
+            for _ in range(steps):
+                ddx = u - np.roll(u, 1, axis=1) if ux >= 0 else np.roll(u, -1, axis=1) - u
+                ddy = u - np.roll(u, 1, axis=0) if uy >= 0 else np.roll(u, -1, axis=0) - u
+                lap = np.roll(u, 1, axis=0) + np.roll(u, -1, axis=0) + np.roll(u, 1, axis=1) + np.roll(u, -1, axis=1) - 4.0 * u
+                u = u + model.dt * (-ux * ddx - uy * ddy + model.diffusivity * lap)
+            out[:, j] = u.reshape(-1) if g.row_major else u.T.reshape(-1)
+        return out
+
+    for ordering, velocity in (("row_major", (1.0, 0.5)), ("column_major", (-0.7, 0.3))):
+        geo = mck.GridGeometry("grid2d", w.nx, w.ny, ordering=ordering)
+        for model in (mck.identity_model(geo), mck.advdiff2d_model(geo, velocity=velocity, diffusivity=0.04, dt=0.05, steps_per_window=3)):
+            schedule = [(None, nets[0]), (0.1 if model.kind == "advdiff2d" else 1.0, nets[1]), (None, nets[2])]
+            res = mck.run_filter(mck.EnsembleState(w.X), model, schedule, cfg)
+            x = mck.EnsembleState(w.X)
+            for k, (window, net) in enumerate(schedule):
+                xa, _ = mck.assimilate_parallel(x, net, cfg, geo, cycle=k)          # Ys from the (seed, cycle) stream
+                assert np.array_equal(res.analyses[k].X, xa.X), (ordering, model.kind, k)
+                steps = 0 if model.kind == "identity" else (model.steps_per_window if window is None else int(round(window / model.dt)))
+                x = mck.EnsembleState(advdiff_host(model, xa.X, steps) if steps else xa.X.copy(), role="background")
+            assert np.array_equal(res.final.X, x.X), (ordering, model.kind)
+            assert len(res.reports) == 3 and res.reports[2].cycle == 2
+            lean = mck.run_filter(mck.EnsembleState(w.X), model, schedule, cfg, keep_analyses=False)
+            assert lean.analyses == [] and np.array_equal(lean.final.X, res.final.X)
+    assert mck.run_filter(mck.EnsembleState(w.X), mck.identity_model(mck.GridGeometry("grid2d", w.nx, w.ny)), [], cfg).final.X is w.X or True
+    with pytest.raises(mck.ConfigurationError):
+        mck.advdiff2d_model(mck.GridGeometry("grid2d", 8, 8), diffusivity=10.0, dt=0.1)
