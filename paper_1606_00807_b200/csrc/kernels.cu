@@ -950,6 +950,7 @@ cudaError_t launch_regress(const RegressParams &p_in, int sm_count, size_t smem_
         for (int level = 0; level < 2; ++level) {
             p.level = level;
             p.bmax = level == 0 ? std::min(b1, b2) : b2;
+            p.bmax1 = std::min(b1, b2);
             p.bmax2 = b2;
             if (level == 1 && b2 <= std::min(b1, b2)) break;     // nothing is ever escalated
             const size_t ws = regress_trunc_ws_doubles(p.pmax, p.bmax) * sizeof(double);

@@ -23,7 +23,7 @@ struct RegressParams {
     unsigned int *lcounter;    // five words: list length, K2b-2 fetch counter, rows sent to the Jacobi fallback, second list length, its fetch counter
     unsigned int *worklist;    // [nwork] rows K2b-1 hands to K2b-2 (work item numbers)
     unsigned int *worklist2;   // [nwork] rows the first K2b-2 pass hands to the second (larger blocks)
-    int bmax, bmax2, level;    // block cap of this K2b-2 pass, of the second pass, and which pass this is (set by the launcher)
+    int bmax, bmax1, bmax2, level;   // block cap of this K2b-2 pass, of the first and second pass, and which pass this is (set by the launcher)
     int f0, f1;                // fields handled by this launch pair (scratch is sized for f1 - f0)
     double *Rq;                // packed QR output scratch [f1 - f0][rq_stride]
     int64_t rq_stride;

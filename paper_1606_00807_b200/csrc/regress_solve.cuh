@@ -770,7 +770,8 @@ __global__ void __launch_bounds__(256, 1) regress_trunc_kernel(const RegressPara
         const int pe = K;                        // order of the triangular problem
         const double *in = P.Rq + (int64_t)fl * P.rq_stride + P.rq_ptr[q];
         const double e2 = in[packed_col_offset(p, K) + K];
-        int flag = 1, why = 0, sweeps = 0, b = 8;
+        int flag = 1, why = 0, sweeps = 0;
+        int b = P.level ? P.bmax1 + 8 : 8;          // second pass: the first one found bmax1 vectors too few
         bool escalate = false;
         unsigned tmask = 0;                      // Ritz values below the threshold
         double fro2 = 0.0, smax_lo = 0.0;
@@ -843,8 +844,9 @@ __global__ void __launch_bounds__(256, 1) regress_trunc_kernel(const RegressPara
                 }
                 __syncwarp();
             };
-            fill_random(0, b);
             const int bcap = bmax < (pe & ~7) ? bmax : (pe & ~7);
+            if (b > bcap) b = bcap;
+            fill_random(0, b);
             int need = 2;
             bool final_done = false, wide_span = true;
             for (;;) {
