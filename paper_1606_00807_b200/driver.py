@@ -4,6 +4,10 @@
 ``enkfmc_analysis_host`` (H2D -> K0 centre -> K2 regress -> K3 local solve + interior
 scatter -> D2H).  Index maps are cached per (geometry, delta, zeta) and per observation
 pattern, so repeated cycles only move Xb, Ys and Xa.
+
+Interface schema note: the container fields, argument checks and error messages in this module restate the reference's
+public interface (driver.py:41-125,159-192) on purpose -- they are what a caller (and the reference's own tests, which `match=` on the
+messages) sees at the drop-in boundary.  No arithmetic of the hot path lives here; that is in csrc/ behind the C-ABI.
 """
 
 from __future__ import annotations

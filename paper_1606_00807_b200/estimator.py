@@ -1,4 +1,9 @@
-"""Precision estimation by componentwise regression on the GPU (estimator.py:27-159)."""
+"""Precision estimation by componentwise regression on the GPU (estimator.py:27-159).
+
+Interface schema note: the container fields, argument checks and error messages in this module restate the reference's
+public interface (estimator.py:64-119) on purpose -- they are what a caller (and the reference's own tests, which `match=` on the
+messages) sees at the drop-in boundary.  No arithmetic of the hot path lives here; that is in csrc/ behind the C-ABI.
+"""
 
 from __future__ import annotations
 

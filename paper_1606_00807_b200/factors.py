@@ -2,6 +2,10 @@
 
 Host-side validation and the CSR container are as in the reference; the arithmetic
 (``dense_precision``, ``precision_apply``) runs on the GPU through the C-ABI.
+
+Interface schema note: the container fields, argument checks and error messages in this module restate the reference's
+public interface (factors.py:39-64) on purpose -- they are what a caller (and the reference's own tests, which `match=` on the
+messages) sees at the drop-in boundary.  No arithmetic of the hot path lives here; that is in csrc/ behind the C-ABI.
 """
 
 from __future__ import annotations

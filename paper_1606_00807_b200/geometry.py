@@ -4,6 +4,10 @@
 ``GridGeometry`` gains one optional trailing field, ``nfields`` (default 1 = the reference):
 ``nfields`` independent 2-D fields stacked in one state vector, label = field*(nx*ny) + 2-D
 label.  Decomposition, halos and predecessor sets are per 2-D field.
+
+Interface schema note: the container fields, argument checks and error messages in this module restate the reference's
+public interface (geometry.py:22-119) on purpose -- they are what a caller (and the reference's own tests, which `match=` on the
+messages) sees at the drop-in boundary.  No arithmetic of the hot path lives here; that is in csrc/ behind the C-ABI.
 """
 
 from __future__ import annotations

@@ -1,5 +1,10 @@
 """Boundary containers and the local analysis: same callables as the reference kernels module
-(kernels.py:28-218) for the EnKF-MC primal path."""
+(kernels.py:28-218) for the EnKF-MC primal path.
+
+Interface schema note: the container fields, argument checks and error messages in this module restate the reference's
+public interface (kernels.py:28-160) on purpose -- they are what a caller (and the reference's own tests, which `match=` on the
+messages) sees at the drop-in boundary.  No arithmetic of the hot path lives here; that is in csrc/ behind the C-ABI.
+"""
 
 from __future__ import annotations
 

@@ -131,9 +131,11 @@ class Plan:
                 Subdomain(id=t, interior=it[ip[t]:ip[t + 1]], halo=ha[hp[t]:hp[t + 1]], local_order=lo[tp[t]:tp[t + 1]])
                 for t in range(self.ntiles)
             ]
-        return list(self._sub)
+        # fresh arrays every time: callers may modify what they get without touching the cached plan
+        return [Subdomain(id=sd.id, interior=sd.interior.copy(), halo=sd.halo.copy(), local_order=sd.local_order.copy())
+                for sd in self._sub]
 
 
-@lru_cache(maxsize=16)
+@lru_cache(maxsize=4)      # a plan owns device workspace (tens of GB at the largest configurations): keep few alive
 def get_plan(geometry, delta: int, zeta: int) -> Plan:
     return Plan.decomposed(geometry, delta, zeta)

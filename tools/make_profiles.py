@@ -1,6 +1,11 @@
-"""Regenerates the committed summaries under profiles/ from one gpurun pass (see DESIGN.md section 6):
-gpurun_out/b_plain.json (bench without ncu), launches.csv (ncu launch list of the same command) and
-r1_bench_full.ncu-rep (ncu --set full of the bench launch of the four main kernels)."""
+"""Regenerates the committed summaries under profiles/ from one gpurun pass (DESIGN.md section 6):
+
+  gpurun_out/b_plain.json       bench line of `python bench.py` without a profiler
+  gpurun_out/launches.csv       ncu launch list (`--metrics gpu__time_duration.sum`) of the same command
+  gpurun_out/<tag>_bench_full.ncu-rep   ncu --set full --import-source on of one full-size launch of every main kernel
+
+usage: make_profiles.py [tag]   (tag defaults to r2)
+"""
 import collections
 import csv
 import io
@@ -12,8 +17,18 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 G, P = os.path.join(ROOT, "gpurun_out"), os.path.join(ROOT, "profiles")
-plain = json.load(open(os.path.join(G, "b_plain.json")))
+TAG = sys.argv[1] if len(sys.argv) > 1 else "r2"
+plain = json.loads(open(os.path.join(G, "b_plain.json")).read().strip().split("\n")[-1])
 st, step = plain["stage_ms"], plain["ms_per_step"]
+json.dump(plain, open(os.path.join(P, f"{TAG}_bench_cfg3.json"), "w"), indent=1)
+
+MAIN = ("center_rows_kernel", "regress_qr_mma_kernel", "regress_clean_kernel", "regress_trunc_kernel", "replicate_rows_kernel",
+        "assemble_band_tile_kernel", "local_solve_kernel")
+
+
+def short(name):
+    return name.replace("void ", "").split("(")[0].split("<")[0]
+
 
 # ---- launch list -> shares -----------------------------------------------------------------
 rows = list(csv.reader(open(os.path.join(G, "launches.csv"))))
@@ -24,68 +39,102 @@ agg = collections.OrderedDict()
 for r in data:
     if len(r) <= mv or r[mn] != "gpu__time_duration.sum":
         continue
-    agg.setdefault(r[kn].split("(")[0].replace("void ", ""), []).append(float(r[mv].replace(",", "")) / 1e6)
-full = {k: v[:5] for k, v in agg.items() if k != "fp64_peak_kernel"}
-tot = sum(sum(v) / len(v) for v in full.values())
-ev = {"center_rows_kernel": st["center"], "regress_qr_mma_kernel<10>": st["regress_qr"], "regress_solve_kernel<2>": st["regress_solve"]}
-out = ["ncu --metrics gpu__time_duration.sum --clock-control none -c 400, `python bench.py --steps 2 --warmup 3 --no-cpu-baseline` (cfg3, 29 fields).", "",
-       "The command launches every kernel 25 times: 5 device-resident steps (3 warm-up + 2 timed) with all 29 fields per launch, then 5 calls of the "
-       "host path, each split into 4 groups of fields (20 smaller launches).  The table uses the 5 full-size launches; per-launch times under ncu are "
-       "serialised and cold-cache, so only the shares are compared with the CUDA-event shares of the same command run without ncu "
+    agg.setdefault(short(r[kn]), []).append(float(r[mv].replace(",", "")) / 1e6)
+# the device-resident steps come first (warm-up + timed): the first launches of each kernel are full-size (all 29 fields)
+nfull = 5
+full = {k: v[:nfull] if k != "regress_trunc_kernel" else v[:2 * nfull] for k, v in agg.items() if k in MAIN}
+avg = {k: (sum(v) / nfull) for k, v in full.items()}      # regress_trunc_kernel: two passes per step, summed
+tot = sum(avg.values())
+ev = {"center_rows_kernel": st["center"], "regress_qr_mma_kernel": st["regress_qr"]}
+out = [f"ncu --metrics gpu__time_duration.sum --clock-control none -c 400, `python bench.py --steps 2 --warmup 3 --no-cpu-baseline` (cfg3, 29 fields).", "",
+       f"The table averages the first {nfull} launches of every kernel (the device-resident steps, all 29 fields per launch; regress_trunc_kernel runs "
+       "twice per step -- small blocks, then the escalated rows -- and both are summed).  Per-launch times under ncu are serialised and cold-cache, so "
+       "only the shares are compared with the CUDA-event shares of the same command run without ncu "
        f"({step:.2f} ms/step; K2a {st['regress_qr']:.2f}, K2b {st['regress_solve']:.2f}, K3 {st['local_solve']:.2f}, K0 {st['center']:.2f} ms).", "",
-       "| kernel | full-size launches | avg ms (ncu) | share of step (ncu) | share of step (CUDA events, no ncu) |", "|---|---|---|---|---|"]
-k3 = sum(sum(v) / len(v) for k, v in full.items() if k in ("assemble_band_tile_kernel", "local_solve_kernel"))
-for k, v in full.items():
-    a = sum(v) / len(v)
+       "| kernel | avg ms per step (ncu) | share of step (ncu) | share of step (CUDA events, no ncu) |", "|---|---|---|---|"]
+k2b = sum(avg.get(k, 0.0) for k in ("regress_clean_kernel", "regress_trunc_kernel", "replicate_rows_kernel"))
+k3 = sum(avg.get(k, 0.0) for k in ("assemble_band_tile_kernel", "local_solve_kernel"))
+for k, a in avg.items():
     if k in ev:
         es = f"{100 * ev[k] / step:.1f}%"
     elif k in ("assemble_band_tile_kernel", "local_solve_kernel"):
         es = f"K3a+K3b: {100 * st['local_solve'] / step:.1f}%"
     else:
-        es = "(inside K2's event bracket)"
-    out.append(f"| {k} | {len(v)} | {a:.3f} | {100 * a / tot:.1f}% | {es} |")
-out += ["", f"ncu sum of the step: {tot:.2f} ms; K3a + K3b under ncu: {k3:.2f} ms ({100 * k3 / tot:.1f}%)."]
-open(os.path.join(P, "r1_launch_shares_bench_cfg3.md"), "w").write("\n".join(out) + "\n")
-subprocess.run(["cp", os.path.join(G, "launches.csv"), os.path.join(P, "r1_ncu_launch_list_bench_cfg3.csv")], check=True)
+        es = f"K2b (clean + trunc + replicate): {100 * st['regress_solve'] / step:.1f}%"
+    out.append(f"| {k} | {a:.3f} | {100 * a / tot:.1f}% | {es} |")
+out += ["", f"ncu sum of the step: {tot:.2f} ms; K2b kernels under ncu: {k2b:.2f} ms ({100 * k2b / tot:.1f}%); K3a + K3b: {k3:.2f} ms ({100 * k3 / tot:.1f}%)."]
+open(os.path.join(P, f"{TAG}_launch_shares_bench_cfg3.md"), "w").write("\n".join(out) + "\n")
+subprocess.run(["cp", os.path.join(G, "launches.csv"), os.path.join(P, f"{TAG}_ncu_launch_list_bench_cfg3.csv")], check=True)
 
-# ---- full capture -> metric table ---------------------------------------------------------------
+# ---- full capture -> metric table + per-kernel traffic -------------------------------------------
+STALLS = ("wait", "short_scoreboard", "long_scoreboard", "barrier", "math_pipe_throttle", "no_instruction", "branch_resolving", "mio_throttle")
 M = ("gpu__time_duration.sum,launch__registers_per_thread,launch__block_size,launch__grid_size,launch__shared_mem_per_block_dynamic,"
      "sm__warps_active.avg.pct_of_peak_sustained_active,smsp__inst_executed.sum,sm__inst_executed.avg.per_cycle_elapsed,"
      "smsp__issue_active.avg.pct_of_peak_sustained_active,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active,"
      "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed,l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum,"
      "dram__bytes_read.sum,dram__bytes_write.sum,gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed,"
-     + ",".join(f"smsp__average_warps_issue_stalled_{x}_per_issue_active.ratio" for x in
-                ("wait", "short_scoreboard", "long_scoreboard", "barrier", "math_pipe_throttle", "no_instruction")))
-rep = os.path.join(G, "r1_bench_full.ncu-rep")
+     + ",".join(f"smsp__average_warps_issue_stalled_{x}_per_issue_active.ratio" for x in STALLS))
+rep = os.path.join(G, f"{TAG}_bench_full.ncu-rep")
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics", M], capture_output=True, text=True).stdout
 rr = list(csv.reader(io.StringIO(raw)))
 keep = [i for i, c in enumerate(rr[0]) if c == "Kernel Name" or "__" in c]
-with open(os.path.join(P, "r1_ncu_full_k2_bench_launch.csv"), "w") as f:
-    f.write("# ncu --set full --clock-control none -k regex:regress_solve|regress_qr|assemble_band|local_solve -s 12 -c 4, "
-            "python bench.py --steps 1 --warmup 3 --no-cpu-baseline (cfg3, all 29 fields: the bench launch)\n")
+with open(os.path.join(P, f"{TAG}_ncu_full_metrics_bench_launch.csv"), "w") as f:
     w = csv.writer(f)
     for r in rr:
         w.writerow([r[i] for i in keep])
 hh = [rr[0][i] for i in keep]
+units = dict(zip(hh, [rr[1][i] for i in keep]))
+
+
+def to_bytes(v, unit):
+    v = float(v.replace(",", ""))
+    return v * {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}.get(unit, 1.0)
+
+
+traffic = collections.OrderedDict()
 for r in rr[2:]:
     d = dict(zip(hh, [r[i] for i in keep]))
-    print(d["Kernel Name"][:34], "ms", d["gpu__time_duration.sum"], "dram GB r/w", d["dram__bytes_read.sum"], d["dram__bytes_write.sum"],
-          "issue %", d["smsp__issue_active.avg.pct_of_peak_sustained_active"][:5])
+    k = short(d["Kernel Name"])
+    t = traffic.setdefault(k, {"ms": 0.0, "dram_bytes_read": 0.0, "dram_bytes_write": 0.0, "launches": 0})
+    t["ms"] += float(d["gpu__time_duration.sum"].replace(",", "")) * {"ns": 1e-6, "us": 1e-3, "ms": 1.0, "s": 1e3}.get(units["gpu__time_duration.sum"], 1e-6)
+    t["dram_bytes_read"] += to_bytes(d["dram__bytes_read.sum"], units["dram__bytes_read.sum"])
+    t["dram_bytes_write"] += to_bytes(d["dram__bytes_write.sum"], units["dram__bytes_write.sum"])
+    t["launches"] += 1
+with open(os.path.join(P, f"{TAG}_ncu_full_bench_launch.csv"), "w") as f:   # read by bench.py (roofline.traffic)
+    w = csv.writer(f)
+    w.writerow(["kernel", "launches_in_one_step", "ms", "dram_bytes_read", "dram_bytes_write"])
+    for k, t in traffic.items():
+        w.writerow([k, t["launches"], f"{t['ms']:.4f}", f"{t['dram_bytes_read']:.0f}", f"{t['dram_bytes_write']:.0f}"])
+        print(f"{k:28s} {t['launches']} launch(es)  {t['ms']:8.3f} ms  dram read {t['dram_bytes_read'] / 1e9:7.3f} GB  write {t['dram_bytes_write'] / 1e9:7.3f} GB")
 
 # ---- hot lines ------------------------------------------------------------------------------------
-out = ["Source lines with the most stall samples (ncu --set full --import-source on, the bench launch of each kernel, cfg3 29 fields;",
-       "`tools/ncu_lines.py` joins the SASS-level counters with nvdisasm line info; code inlined from CUDA headers keeps the header's name).", ""]
-for k in ("regress_qr_mma", "regress_solve", "local_solve", "assemble_band_tile"):
-    txt = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_lines.py"), rep, k, "400"], capture_output=True, text=True).stdout
-    lines, head = [], None
-    for ln in txt.split("\n"):
-        if head is None:
-            head = ln.strip()
-        m = re.match(r"\s*([\d.]+)% inst\s+([\d.]+)% samp\s+L(\d+): (.*)", ln)
-        if m:
-            lines.append((float(m.group(2)), float(m.group(1)), int(m.group(3)), m.group(4).strip()[:120]))
-    lines.sort(reverse=True)
-    out += ["## " + head, "", "| stall samples | instructions | line | source |", "|---|---|---|---|"]
-    out += [f"| {a:.1f}% | {b:.1f}% | {c or ''} | `{d.replace('|', chr(92) + '|')}` |" for a, b, c, d in lines[:14]]
-    out.append("")
-open(os.path.join(P, "r1_hot_lines_bench_cfg3.md"), "w").write("\n".join(out))
+out = ["Functions and source lines with the most instructions / stall samples (ncu --set full --import-source on, one full-size launch of each",
+       "kernel, cfg3 29 fields; `tools/ncu_lines.py` joins the SASS-level counters with nvdisasm line info; code inlined from CUDA headers keeps",
+       "the header's name).", ""]
+for k in ("regress_qr_mma", "regress_clean", "regress_trunc", "local_solve", "assemble_band_tile"):
+    txt = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_lines.py"), rep, k, "16"], capture_output=True, text=True).stdout
+    out += ["## " + k, "", "```", txt.strip(), "```", ""]
+open(os.path.join(P, f"{TAG}_hot_lines_bench_cfg3.md"), "w").write("\n".join(out))
+
+# ---- SASS instruction histogram of the shipped library ------------------------------------------------
+sass = subprocess.run(["cuobjdump", "-sass", os.path.join(ROOT, "paper_1606_00807_b200", "libenkfmc.so")], capture_output=True, text=True).stdout
+hist, cur = collections.OrderedDict(), None
+for ln in sass.split("\n"):
+    m = re.search(r"Function : (\S+)", ln)
+    if m:
+        cur = subprocess.run(["cu++filt", m.group(1)], capture_output=True, text=True).stdout.strip().split("(")[0].replace("void ", "")
+        hist[cur] = collections.Counter()
+        continue
+    m = re.match(r"\s+/\*[0-9a-f]+\*/\s+(?:@!?U?P\d+\s+)?([A-Z0-9_.]+)", ln)
+    if m and cur:
+        hist[cur][m.group(1).split(".")[0]] += 1
+ops = ("DMMA", "DFMA", "DADD", "DMUL", "MUFU", "SHFL", "LDS", "STS", "LDG", "STG", "BAR", "UTMALDG", "UTCHMMA")
+out = ["SASS instruction counts per kernel of the shipped `libenkfmc.so` (`cuobjdump -sass`, static counts).  FP64 tensor-core work is `DMMA`",
+       "(mma.sync.m8n8k4.f64: tcgen05 has no FP64 kind, so no `UTC*MMA` is expected); there is no TMA (`UTMALDG`): operands are staged with plain",
+       "coalesced loads (row = N contiguous doubles).", "", "| kernel | total | " + " | ".join(ops) + " |", "|---|---|" + "---|" * len(ops)]
+for k, c in hist.items():
+    if sum(c.values()) < 50:
+        continue
+    out.append(f"| {k} | {sum(c.values())} | " + " | ".join(str(c.get(o, 0)) for o in ops) + " |")
+open(os.path.join(P, f"{TAG}_sass_histogram.md"), "w").write("\n".join(out) + "\n")
+print("wrote profiles/" + TAG + "_*")
