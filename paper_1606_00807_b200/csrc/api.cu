@@ -42,6 +42,9 @@ struct DeviceState {
     size_t prof_used = 0;
     // workspace
     int64_t ws_nens = 0;
+    // T / D / flags / band cover the owned tiles only: first owned local row, CSR position and band offset, and the field strides
+    int64_t ws_row0 = 0, ws_nnz0 = 0, ws_rows = 0, ws_nnz = 0, ws_tb = -1, ws_te = -1;
+    int64_t band_off0 = 0, band_own = 0, band_tb = -1, band_te = -1;
     double *U = nullptr, *T = nullptr, *D = nullptr, *scratch = nullptr;
     int32_t *flags = nullptr, *status = nullptr;
     unsigned int *counters = nullptr;
@@ -194,33 +197,58 @@ int ensure_solve_layout(enkfmc_plan *p, int64_t nens) {
 int ensure_band(enkfmc_plan *p) {
     DeviceState *d = p->dev;
     const int64_t budget = (int64_t)16 << 30;
-    const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(p->nfields, budget / std::max<int64_t>(8 * d->band_stride, 1)));
+    if (d->band_tb != p->tile_begin || d->band_te != p->tile_end) {   // the owned tiles' share of the band
+        std::vector<int64_t> bp((size_t)p->ntiles + 1);
+        CK(cudaMemcpy(bp.data(), d->band_ptr, bp.size() * sizeof(int64_t), cudaMemcpyDeviceToHost));
+        d->band_off0 = bp[(size_t)p->tile_begin];
+        d->band_own = bp[(size_t)p->tile_end] - bp[(size_t)p->tile_begin];
+        d->band_tb = p->tile_begin;
+        d->band_te = p->tile_end;
+        d->band_fields = 0;
+    }
+    const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(p->nfields, budget / std::max<int64_t>(8 * d->band_own, 1)));
     if (d->band && d->band_fields >= chunk) return ENKFMC_OK;
     release(d->band);
-    CK(cudaMalloc(&d->band, std::max<size_t>((size_t)chunk * d->band_stride, 1) * sizeof(double)));
+    CK(cudaMalloc(&d->band, std::max<size_t>((size_t)chunk * d->band_own, 1) * sizeof(double)));
     d->band_fields = chunk;
     return ENKFMC_OK;
 }
 
 int ensure_workspace(enkfmc_plan *p, int64_t nens) {
     DeviceState *d = p->dev;
-    if (d->ws_nens == nens && d->U) return ENKFMC_OK;
+    if (d->ws_nens == nens && d->U && d->ws_tb == p->tile_begin && d->ws_te == p->tile_end) return ENKFMC_OK;
     release(d->U); release(d->T); release(d->D); release(d->flags); release(d->status);
     const int64_t nstate = p->nstate2d * p->nfields;
+    // factors of the owned tiles only (one rank's share): contiguous local rows, contiguous CSR positions
+    d->ws_row0 = p->tile_ptr[(size_t)p->tile_begin];
+    d->ws_rows = p->tile_ptr[(size_t)p->tile_end] - d->ws_row0;
+    d->ws_nnz0 = p->row_ptr[(size_t)d->ws_row0];
+    d->ws_nnz = p->row_ptr[(size_t)(d->ws_row0 + d->ws_rows)] - d->ws_nnz0;
     CK(cudaMalloc(&d->U, std::max<size_t>(1, (size_t)nstate * nens) * sizeof(double)));
-    CK(cudaMalloc(&d->T, std::max<size_t>(1, (size_t)p->nnz() * p->nfields) * sizeof(double)));
-    CK(cudaMalloc(&d->D, std::max<size_t>(1, (size_t)p->sum_nlocal() * p->nfields) * sizeof(double)));
-    CK(cudaMalloc(&d->flags, std::max<size_t>(1, (size_t)p->sum_nlocal() * p->nfields) * sizeof(int32_t)));
+    CK(cudaMalloc(&d->T, std::max<size_t>(1, (size_t)d->ws_nnz * p->nfields) * sizeof(double)));
+    CK(cudaMalloc(&d->D, std::max<size_t>(1, (size_t)d->ws_rows * p->nfields) * sizeof(double)));
+    CK(cudaMalloc(&d->flags, std::max<size_t>(1, (size_t)d->ws_rows * p->nfields) * sizeof(int32_t)));
     CK(cudaMalloc(&d->status, std::max<size_t>(1, (size_t)p->ntiles * p->nfields) * sizeof(int32_t)));
     d->ws_nens = nens;
+    d->ws_tb = p->tile_begin;
+    d->ws_te = p->tile_end;
     return ENKFMC_OK;
 }
 
 // fields [fbeg, fend) (fend < 0: all)
+// d_T / d_D / d_flags are indexed by the plan's global CSR position / local row with field strides tstride / dstride:
+// caller-owned full-size buffers (tstride = nnz, dstride = sum_nlocal) or the plan's workspace, biased by the first owned
+// position (own = true).
 int do_regress(enkfmc_plan *p, const double *d_U, int64_t nens, double rank_tol, double floor_, double *d_T,
                double *d_D, int32_t *d_flags, cudaStream_t s, cudaEvent_t mid = nullptr, int64_t fbeg = 0,
-               int64_t fend = -1) {
+               int64_t fend = -1, bool own = false) {
     if (fend < 0) fend = p->nfields;
+    const int64_t tstride = own ? p->dev->ws_nnz : p->nnz(), dstride = own ? p->dev->ws_rows : p->sum_nlocal();
+    if (own) {
+        d_T -= p->dev->ws_nnz0;
+        d_D -= p->dev->ws_row0;
+        if (d_flags) d_flags -= p->dev->ws_row0;
+    }
     DeviceState *d = p->dev;
     int rc0 = ensure_orders(p);
     if (rc0) return rc0;
@@ -230,7 +258,7 @@ int do_regress(enkfmc_plan *p, const double *d_U, int64_t nens, double rank_tol,
     R.nwork = (int64_t)p->regress_order.size() * p->nfields;
     R.row_ptr = d->row_ptr; R.pred_state = d->pred_state; R.state_row = d->state_row; R.work_order = d->regress_order;
     R.rank_tol = rank_tol; R.variance_floor = floor_; R.fast_ratio = 1e-6;
-    R.T = d_T; R.D = d_D; R.flags = d_flags; R.counter = d->counters; R.lcounter = d->counters + 8;
+    R.T = d_T; R.D = d_D; R.flags = d_flags; R.tstride = tstride; R.dstride = dstride; R.counter = d->counters; R.lcounter = d->counters + 8;
     R.rq_ptr = d->rq_ptr; R.rq_stride = d->rq_stride;
     // QR scratch: as many fields per launch pair as fit in the budget (default 16 GiB)
     const int64_t budget = (int64_t)16 << 30;
@@ -265,8 +293,8 @@ int do_regress(enkfmc_plan *p, const double *d_U, int64_t nens, double rank_tol,
     }
     if (!p->alias_row.empty()) {   // copy each distinct regression to the other tiles holding the same row
         CK(launch_replicate_rows(d->alias_row, d->alias_rep, (int64_t)p->alias_row.size(), d->row_ptr, fend - fbeg,
-                                 p->nnz(), p->sum_nlocal(), d_T + fbeg * p->nnz(), d_D + fbeg * p->sum_nlocal(),
-                                 d_flags ? d_flags + fbeg * p->sum_nlocal() : nullptr, s));
+                                 tstride, dstride, d_T + fbeg * tstride, d_D + fbeg * dstride,
+                                 d_flags ? d_flags + fbeg * dstride : nullptr, s));
         p->counters[0] += 1;
     }
     return ENKFMC_OK;
@@ -274,8 +302,9 @@ int do_regress(enkfmc_plan *p, const double *d_U, int64_t nens, double rank_tol,
 
 int do_solve(enkfmc_plan *p, const double *d_X, const double *d_T, const double *d_D, const double *d_r,
              const double *d_Ys, int64_t nens, double *d_Xa, int32_t *d_status, cudaStream_t s, int64_t fbeg = 0,
-             int64_t fend = -1) {
+             int64_t fend = -1, bool own = false) {
     if (fend < 0) fend = p->nfields;
+    if (own) { d_T -= p->dev->ws_nnz0; d_D -= p->dev->ws_row0; }
     DeviceState *d = p->dev;
     int rc = ensure_obs(p);
     if (rc) return rc;
@@ -285,11 +314,12 @@ int do_solve(enkfmc_plan *p, const double *d_X, const double *d_T, const double 
     S.ntiles_owned = (int)p->tile_order.size();
     S.X = d_X; S.T = d_T; S.D = d_D; S.rdiag = d_r; S.Ys = d_Ys; S.Xa = d_Xa;
     S.nloc = p->sum_nlocal(); S.nnz = p->nnz(); S.nstate2d = p->nstate2d;
+    S.tstride = own ? d->ws_nnz : p->nnz(); S.dstride = own ? d->ws_rows : p->sum_nlocal();
     S.tile_ptr = d->tile_ptr; S.row_ptr = d->row_ptr; S.csc_ptr = d->csc_ptr; S.csc_src = d->csc_src;
     S.col_idx = d->col_idx; S.csc_row = d->csc_row; S.phys = d->phys; S.iphys = d->iphys; S.bw = d->bw;
     S.state_row = d->state_row; S.obs_slot = d->obs_slot; S.tile_nobs = d->tile_nobs; S.tile_order = d->tile_order;
     S.is_interior = d->is_interior; S.tile_mono = d->tile_mono; S.scratch = d->scratch; S.status = d_status; S.counter = d->counters + 2;
-    S.band_ptr = d->band_ptr; S.band_stride = d->band_stride; S.row_tile = d->row_tile; S.work_order = d->work_order;
+    S.band_ptr = d->band_ptr; S.row_tile = d->row_tile; S.work_order = d->work_order;
     S.nrows_owned = (int64_t)p->work_order.size();
     S.asm_nmax = (int)p->max_nlocal;
     S.asm_nnzmax = 0;
@@ -297,7 +327,8 @@ int do_solve(enkfmc_plan *p, const double *d_X, const double *d_T, const double 
         S.asm_nnzmax = std::max<int>(S.asm_nnzmax, (int)(p->row_ptr[p->tile_ptr[t + 1]] - p->row_ptr[p->tile_ptr[t]]));
     int rc2 = ensure_band(p);
     if (rc2) return rc2;
-    S.band = d->band;
+    S.band = d->band - d->band_off0;          // band_ptr[t] counts from tile 0: biased by the first owned tile's offset
+    S.band_stride = d->band_own;
     if (fbeg == 0) CK(cudaMemsetAsync(d->counters + 3, 0, sizeof(unsigned int), s));   // clamped-pivot counter
     for (int64_t f0 = fbeg; f0 < fend; f0 += d->band_fields) {
         S.f0 = (int)f0;
@@ -408,9 +439,9 @@ extern "C" int enkfmc_analysis_device(enkfmc_plan *p, const double *d_X, const d
     CK(launch_center_rows(d_X, d->U, p->nstate2d * p->nfields, (int)nens, s));
     p->counters[0] += 1;
     if (ev) CK(cudaEventRecord(ev[1], s));
-    if ((rc = do_regress(p, d->U, nens, rank_tol, floor_, d->T, d->D, d->flags, s, ev ? ev[2] : nullptr))) return rc;
+    if ((rc = do_regress(p, d->U, nens, rank_tol, floor_, d->T, d->D, d->flags, s, ev ? ev[2] : nullptr, 0, -1, true))) return rc;
     if (ev) CK(cudaEventRecord(ev[3], s));
-    rc = do_solve(p, d_X, d->T, d->D, d_r, d_Ys, nens, d_Xa, d->status, s);
+    rc = do_solve(p, d_X, d->T, d->D, d_r, d_Ys, nens, d_Xa, d->status, s, 0, -1, true);
     if (ev) CK(cudaEventRecord(ev[4], s));
     return rc;
 }
@@ -580,12 +611,12 @@ extern "C" int enkfmc_analysis_host(enkfmc_plan *p, const double *X, const doubl
         CK(cudaEventRecord(EV(g, 2), s));
         CK(launch_center_rows(d->dX + r0 * nens, d->U + r0 * nens, (int64_t)(r1 - r0), (int)nens, s));
         p->counters[0] += 1;
-        if ((rc = do_regress(p, d->U, nens, rank_tol, floor_, d->T, d->D, d->flags, s, nullptr, f0, f1))) { cudaStreamSynchronize(cs); cudaStreamSynchronize(s); return rc; }
+        if ((rc = do_regress(p, d->U, nens, rank_tol, floor_, d->T, d->D, d->flags, s, nullptr, f0, f1, true))) { cudaStreamSynchronize(cs); cudaStreamSynchronize(s); return rc; }
         CK(cudaEventRecord(EV(g, 3), s));
         CK(cudaStreamWaitEvent(s, EV(g, 7), 0));
         if (p->tile_begin != 0 || p->tile_end != p->ntiles)   // a rank's share: rows it does not own come back as the background
             CK(cudaMemcpyAsync(d->dXa + r0 * nens, d->dX + r0 * nens, (r1 - r0) * rowbytes, cudaMemcpyDeviceToDevice, s));
-        if ((rc = do_solve(p, d->dX, d->T, d->D, d->dR, d->dYs, nens, d->dXa, d->status, s, f0, f1))) { cudaStreamSynchronize(cs); cudaStreamSynchronize(s); return rc; }
+        if ((rc = do_solve(p, d->dX, d->T, d->D, d->dR, d->dYs, nens, d->dXa, d->status, s, f0, f1, true))) { cudaStreamSynchronize(cs); cudaStreamSynchronize(s); return rc; }
         CK(cudaEventRecord(EV(g, 4), s));
         CK(cudaStreamWaitEvent(cs, EV(g, 4), 0));
         CK(cudaEventRecord(EV(g, 5), cs));
@@ -651,6 +682,7 @@ extern "C" int enkfmc_assemble_band(enkfmc_plan *p, const double *d_T, const dou
     SolveParams S{};
     S.T = d_T; S.D = d_D; S.nfields = 1; S.ntiles = 1; S.ntiles_owned = 1; S.bmax = (int)p->max_bw;
     S.nloc = p->sum_nlocal(); S.nnz = p->nnz(); S.nstate2d = p->nstate2d;
+    S.tstride = p->nnz(); S.dstride = p->sum_nlocal();
     S.tile_ptr = d->tile_ptr; S.row_ptr = d->row_ptr; S.csc_ptr = d->csc_ptr; S.csc_src = d->csc_src;
     S.col_idx = d->col_idx; S.csc_row = d->csc_row; S.phys = d->phys; S.bw = d->bw;
     S.band_ptr = d->band_ptr; S.band_stride = d->band_stride; S.row_tile = d->row_tile; S.work_order = d->work_order;
@@ -719,6 +751,16 @@ extern "C" int enkfmc_advdiff_step(const double *d_in, double *d_out, int64_t nx
 extern "C" int enkfmc_plan_read_buffer(const enkfmc_plan *p, int what, void *host_out, int64_t bytes) {
     void *src = enkfmc_plan_device_buffer(p, what);
     if (!src) { enkfmc_set_error("workspace buffer not allocated"); return ENKFMC_E_VALUE; }
+    {   // T, D and flags cover the owned tiles only: [nfields][owned count], in the plan's order
+        const DeviceState *d = p->dev;
+        const int64_t have = what == 0 ? p->nstate2d * p->nfields * d->ws_nens * 8 : what == 1 ? d->ws_nnz * p->nfields * 8 :
+                             what == 2 ? d->ws_rows * p->nfields * 8 : what == 3 ? d->ws_rows * p->nfields * 4 : p->ntiles * p->nfields * 4;
+        if (bytes > have) {
+            enkfmc_set_error("workspace buffer holds " + std::to_string(have) + " bytes (the owned tiles' share), " +
+                             std::to_string(bytes) + " requested");
+            return ENKFMC_E_VALUE;
+        }
+    }
     CK(cudaDeviceSynchronize());
     CK(cudaMemcpy(host_out, src, (size_t)bytes, cudaMemcpyDeviceToHost));
     return ENKFMC_OK;

@@ -539,8 +539,8 @@ __global__ void __launch_bounds__(256, 1) regress_qr_kernel(const RegressParams 
             for (int i = lane; i < N; i += 32) { const double v = yrow[i]; s += v * v; }
             s = warp_sum(s) / denom;
             if (lane == 0) {
-                P.D[(int64_t)f * P.nloc + q] = fmax(s, P.variance_floor);
-                if (P.flags) P.flags[(int64_t)f * P.nloc + q] = (s < P.variance_floor) ? 8 : 0;
+                P.D[(int64_t)f * P.dstride + q] = fmax(s, P.variance_floor);
+                if (P.flags) P.flags[(int64_t)f * P.dstride + q] = (s < P.variance_floor) ? 8 : 0;
             }
             continue;
         }
@@ -641,8 +641,8 @@ __global__ void __launch_bounds__(256, 1) regress_qr_mma_kernel(const RegressPar
             for (int i = lane; i < N; i += 32) { const double v = yrow[i]; s += v * v; }
             s = warp_sum(s) / denom;
             if (lane == 0) {
-                P.D[(int64_t)f * P.nloc + q] = fmax(s, P.variance_floor);
-                if (P.flags) P.flags[(int64_t)f * P.nloc + q] = (s < P.variance_floor) ? 8 : 0;
+                P.D[(int64_t)f * P.dstride + q] = fmax(s, P.variance_floor);
+                if (P.flags) P.flags[(int64_t)f * P.dstride + q] = (s < P.variance_floor) ? 8 : 0;
             }
             continue;
         }
@@ -1050,8 +1050,8 @@ __global__ void __launch_bounds__(ASM_WARPS * 32) assemble_band_kernel(const Sol
         const int32_t *phys = P.phys + base;
         const int I = phys[i];
         const int col0 = 8 * ((I >> 3) - Wb);          // column of band entry e = 0
-        const double *Tf = P.T + (int64_t)f * P.nnz;
-        const double *Df = P.D + (int64_t)f * P.nloc + base;
+        const double *Tf = P.T + (int64_t)f * P.tstride;
+        const double *Df = P.D + (int64_t)f * P.dstride + base;
         for (int e = lane; e < Wr; e += 32) acc[e] = 0.0;
         __syncwarp();
         const int64_t c0 = P.csc_ptr[base + i], c1 = P.csc_ptr[base + i + 1];
@@ -1114,8 +1114,8 @@ __global__ void __launch_bounds__(ASMT_THREADS) assemble_band_tile_kernel(const 
     uint16_t *sK = reinterpret_cast<uint16_t *>(sRow + P.asm_nmax + 1);
     uint16_t *sPhys = sK + P.asm_nnzmax;
 
-    const double *Tf = P.T + (int64_t)f * P.nnz + e0;
-    const double *Df = P.D + (int64_t)f * P.nloc + base;
+    const double *Tf = P.T + (int64_t)f * P.tstride + e0;
+    const double *Df = P.D + (int64_t)f * P.dstride + base;
     const int32_t *phys = P.phys + base;
     for (int i = tid; i < n; i += ASMT_THREADS) { sD[i] = 1.0 / Df[i]; sPhys[i] = (uint16_t)phys[i]; }
     for (int i = tid; i <= n; i += ASMT_THREADS) sRow[i] = (int32_t)(P.row_ptr[base + i] - e0);

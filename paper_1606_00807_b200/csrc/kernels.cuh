@@ -16,9 +16,10 @@ struct RegressParams {
     const int32_t *state_row;  // [nloc]
     const int32_t *work_order; // distinct regressions (plan.h regress_order), most predecessors first
     double rank_tol, variance_floor, fast_ratio;
-    double *T;                 // [nfields][nnz]  (-beta)
-    double *D;                 // [nfields][nloc] floored
-    int32_t *flags;            // [nfields][nloc] or null
+    double *T;                 // [nfields][tstride] (-beta), indexed by the plan's global CSR position: the pointer is biased by the
+    double *D;                 // [nfields][dstride] floored    first owned position when the workspace covers the owned tiles only
+    int32_t *flags;            // [nfields][dstride] or null
+    int64_t tstride, dstride;  // field strides of T and of D / flags (nnz / nloc, or the owned counts)
     unsigned int *counter;     // two work-fetch counters (zeroed by the launcher)
     unsigned int *lcounter;    // five words: list length, K2b-2 fetch counter, rows sent to the Jacobi fallback, second list length, its fetch counter
     unsigned int *worklist;    // [nwork] rows K2b-1 hands to K2b-2 (work item numbers)
@@ -35,6 +36,7 @@ struct SolveParams {
     double *Xa;
     int N, nfields, ntiles, ntiles_owned;   // ntiles: global count (indexing); owned: work items
     int64_t nloc, nnz, nstate2d;
+    int64_t tstride, dstride;  // field strides of T and D (see RegressParams)
     const int64_t *tile_ptr, *row_ptr, *csc_ptr, *csc_src;
     const int32_t *col_idx, *csc_row, *phys, *iphys, *bw, *state_row, *obs_slot, *tile_nobs, *tile_order;
     const uint8_t *is_interior;

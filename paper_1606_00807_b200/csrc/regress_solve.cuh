@@ -694,7 +694,7 @@ __global__ void __launch_bounds__(512, 1) regress_clean_kernel(const RegressPara
                             const double pz = vdot<PS>(b, z);                     // beta -= z z^T beta
 #pragma unroll
                             for (int t = 0; t < PS; ++t) b.v[t] = fma(-pz, z.v[t], b.v[t]);
-                            double *Tout = P.T + (int64_t)f * P.nnz + r0;
+                            double *Tout = P.T + (int64_t)f * P.tstride + r0;
 #pragma unroll
                             for (int t = 0; t < PS; ++t) { const int e = lane + 32 * t; if (e < p) Tout[e] = -b.v[t]; }
                             // |c - R beta|^2
@@ -706,8 +706,8 @@ __global__ void __launch_bounds__(512, 1) regress_clean_kernel(const RegressPara
                             rest2 = warp_sum(rest2);
                             if (lane == 0) {
                                 const double d = (e2 + rest2) / denom;
-                                P.D[(int64_t)f * P.nloc + q] = fmax(d, P.variance_floor);
-                                if (P.flags) P.flags[(int64_t)f * P.nloc + q] = 2 | 32 | (d < P.variance_floor ? 8 : 0) | ((nsteps < 255 ? nsteps : 255) << 8);
+                                P.D[(int64_t)f * P.dstride + q] = fmax(d, P.variance_floor);
+                                if (P.flags) P.flags[(int64_t)f * P.dstride + q] = 2 | 32 | (d < P.variance_floor ? 8 : 0) | ((nsteps < 255 ? nsteps : 255) << 8);
                             }
                             __syncwarp();
                             continue;
@@ -722,13 +722,13 @@ __global__ void __launch_bounds__(512, 1) regress_clean_kernel(const RegressPara
         }
         Vec<PS> b = vload<PS>(W + (size_t)p * ld, p, lane);
         b = solve_upper<PS>(b, W, rinv, ld, p, lane);
-        double *Tout = P.T + (int64_t)f * P.nnz + r0;
+        double *Tout = P.T + (int64_t)f * P.tstride + r0;
 #pragma unroll
         for (int t = 0; t < PS; ++t) { const int e = lane + 32 * t; if (e < p) Tout[e] = -b.v[t]; }
         if (lane == 0) {
             const double d = e2 / denom;
-            P.D[(int64_t)f * P.nloc + q] = fmax(d, P.variance_floor);
-            if (P.flags) P.flags[(int64_t)f * P.nloc + q] = d < P.variance_floor ? 8 : 0;
+            P.D[(int64_t)f * P.dstride + q] = fmax(d, P.variance_floor);
+            if (P.flags) P.flags[(int64_t)f * P.dstride + q] = d < P.variance_floor ? 8 : 0;
         }
         __syncwarp();
     }
@@ -1007,13 +1007,13 @@ __global__ void __launch_bounds__(256, 1) regress_trunc_kernel(const RegressPara
                 vstore<PS>(aux, bt, p, lane);
                 __syncwarp();
             }
-            double *Tout = P.T + (int64_t)f * P.nnz + r0;
+            double *Tout = P.T + (int64_t)f * P.tstride + r0;
             for (int j = lane; j < p; j += 32) Tout[j] = -aux[j];
             if (lane == 0) {
                 const double d = (e2 + rest2) / denom;
                 if (d < P.variance_floor) flag |= 8;
-                P.D[(int64_t)f * P.nloc + q] = fmax(d, P.variance_floor);
-                if (P.flags) P.flags[(int64_t)f * P.nloc + q] = flag | ((sweeps < 255 ? sweeps : 255) << 8);
+                P.D[(int64_t)f * P.dstride + q] = fmax(d, P.variance_floor);
+                if (P.flags) P.flags[(int64_t)f * P.dstride + q] = flag | ((sweeps < 255 ? sweeps : 255) << 8);
             }
             __syncwarp();
             continue;
@@ -1025,7 +1025,7 @@ __global__ void __launch_bounds__(256, 1) regress_trunc_kernel(const RegressPara
         __syncwarp();
         double dropped2;
         flag |= jacobi_solve(W, ld, K, p, P.rank_tol, rinv, tmp, aux, &dropped2, lane);
-        double *Tout = P.T + (int64_t)f * P.nnz + r0;
+        double *Tout = P.T + (int64_t)f * P.tstride + r0;
         for (int j = lane; j < p; j += 32) Tout[j] = -aux[j];
         unpack_rc<PS>(in, W, ld, p, K, lane);
         __syncwarp();
@@ -1042,8 +1042,8 @@ __global__ void __launch_bounds__(256, 1) regress_trunc_kernel(const RegressPara
         if (lane == 0) {
             const double d = (e2 + rest2) / denom;
             if (d < P.variance_floor) flag |= 8;
-            P.D[(int64_t)f * P.nloc + q] = fmax(d, P.variance_floor);
-            if (P.flags) P.flags[(int64_t)f * P.nloc + q] = flag | ((sweeps < 255 ? sweeps : 255) << 8);
+            P.D[(int64_t)f * P.dstride + q] = fmax(d, P.variance_floor);
+            if (P.flags) P.flags[(int64_t)f * P.dstride + q] = flag | ((sweeps < 255 ? sweeps : 255) << 8);
             atomicAdd(P.lcounter + 2, 1u);
         }
         __syncwarp();

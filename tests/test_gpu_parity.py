@@ -441,6 +441,22 @@ def test_tile_range_on_a_fresh_plan_and_indefinite_factors(mck):
         own = np.concatenate([sd.interior for sd in mck.decompose(geo, w.delta, w.zeta)[3:6]])
         assert relerr(Xa[own], ref[own]) < XA_GATE
         assert device.check_status(plan) == 0
+        if attempt == 0:
+            # the factor workspace covers the owned tiles only: [owned positions], bitwise the full run's slice
+            from paper_1606_00807_b200.plan import ROW_PTR, TILE_PTR
+            tp, rp = plan.get(TILE_PTR), plan.get(ROW_PTR)
+            n_own, nnz_own = int(tp[6] - tp[3]), int(rp[tp[6]] - rp[tp[3]])
+            T_own = device.workspace_tensor(plan, 1, (nnz_own,))
+            D_own = device.workspace_tensor(plan, 2, (n_own,))
+            with pytest.raises(ValueError, match="owned tiles"):
+                device.workspace_tensor(plan, 1, (plan.nnz,))
+            full = Plan.decomposed(geo, w.delta, w.zeta)
+            full.set_observations(w.obs_indices)
+            device.analysis_host(full, w.X, w.r_diag, w.Ys)
+            T_full = device.workspace_tensor(full, 1, (full.nnz,))
+            D_full = device.workspace_tensor(full, 2, (full.sum_nlocal,))
+            assert np.array_equal(T_own, T_full[rp[tp[3]]:rp[tp[6]]]) and np.array_equal(D_own, D_full[tp[3]:tp[6]])
+            del full
         del plan
     # (ii)
     plan = Plan.decomposed(geo, w.delta, w.zeta)
