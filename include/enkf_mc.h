@@ -218,6 +218,16 @@ int enkfmc_advdiff_step(const double *d_in, double *d_out, int64_t nx, int64_t n
                         int64_t nfields, int64_t nens, double ux, double uy, double dt, double kappa,
                         void *stream);
 
+/* LETKF baseline at every grid component -- letkf_analysis_global / letkf_analysis_point (kernels.py:251-335), the
+ * paper's comparison method; a decomposed run gives the same rows (driver.py:128-156).  d_X, d_U (workspace), d_Xa:
+ * [nfields*nx*ny][nens]; d_mean: workspace [nfields*nx*ny]; d_obs_of_state: observation row of each state row or -1;
+ * *first_bad receives the first component whose weight matrix lost positive definiteness (-1: none; the call then
+ * returns ENKFMC_E_NUMERIC like the reference raises NumericalError).  Synchronises the stream. */
+int enkfmc_letkf_device(const double *d_X, double *d_U, double *d_mean, double *d_Xa,
+                        const int32_t *d_obs_of_state, const double *d_rdiag, const double *d_y,
+                        int64_t nx, int64_t ny, int row_major, int periodic, int64_t nfields,
+                        int64_t nens, int64_t zeta, double inflation, int64_t *first_bad, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -435,3 +435,51 @@ def assimilate(X, obs_indices, r_diag, Ys, grid: Grid, delta: int, zeta: int,
         if keep_tiles:
             kept.append(results)
     return (Xa, kept) if keep_tiles else Xa
+
+
+# --------------------------------------------------------------------------
+# LETKF baseline (kernels.py:251-335), the paper's comparison method
+# --------------------------------------------------------------------------
+EIG_FLOOR = 1e-12        # kernels.py:25
+
+
+def letkf_point(center: int, Ub: np.ndarray, xb_mean: np.ndarray, obs_pos, r_diag, y, inflation: float = 1.0) -> np.ndarray:
+    """Analysis row of one grid point from its local box (kernels.py:251-303)."""
+    nbox, nens = Ub.shape
+    obs_pos = np.asarray(obs_pos, dtype=np.int64)
+    if obs_pos.size == 0:
+        return xb_mean[center] + np.sqrt(inflation) * Ub[center]          # :282-284
+    z = Ub[obs_pos]
+    rinv = 1.0 / np.asarray(r_diag, dtype=np.float64)
+    m = z.T @ (z * rinv[:, None])
+    m = (m + m.T) * 0.5
+    m[np.arange(nens), np.arange(nens)] += (nens - 1) / inflation
+    lam, q = np.linalg.eigh(m)
+    if lam[0] < EIG_FLOOR:
+        raise RuntimeError(f"analysis weight matrix lost positive definiteness (min eig {lam[0]:.3e})")
+    innov = np.asarray(y, dtype=np.float64) - xb_mean[obs_pos]
+    zri = z.T @ (innov * rinv)
+    wa = q @ ((q.T @ zri) / lam)
+    sqrt_wa = (q * np.sqrt((nens - 1) / lam)) @ q.T
+    return xb_mean[center] + Ub[center] @ (wa[:, None] + sqrt_wa)
+
+
+def letkf_global(X: np.ndarray, grid: Grid, obs_indices, r_diag, y, zeta: int, inflation: float = 1.0) -> np.ndarray:
+    """The point kernel at every grid component, field by field (kernels.py:306-335)."""
+    X = np.asarray(X, dtype=np.float64)
+    obs_indices = np.asarray(obs_indices, dtype=np.int64)
+    r_diag = np.asarray(r_diag, dtype=np.float64)
+    y = np.asarray(y, dtype=np.float64)
+    xb_mean = X.mean(axis=1)
+    u = X - xb_mean[:, None]
+    out = X.copy()
+    for f in range(grid.nfields):
+        off = f * grid.n2d
+        for c in range(grid.n2d):
+            box = local_box(grid, c, zeta) + off
+            pos, rows = restrict_observations(obs_indices, box)
+            if pos.size == 0 and inflation == 1.0:
+                continue
+            cpos = int(np.searchsorted(box, c + off))
+            out[c + off] = letkf_point(cpos, u[box], xb_mean[box], pos, r_diag[rows], y[rows], inflation)
+    return out

@@ -24,7 +24,7 @@ SYMBOLS = (
     "enkfmc_regress", "enkfmc_local_solve", "enkfmc_analysis_device", "enkfmc_analysis_host",
     "enkfmc_plan_counter", "enkfmc_plan_device_buffer", "enkfmc_scatter_rows", "enkfmc_assemble_band",
     "enkfmc_precision_apply", "enkfmc_plan_read_buffer", "enkfmc_plan_set_tile_range", "enkfmc_plan_profile",
-    "enkfmc_plan_stage_times", "enkfmc_plan_work", "enkfmc_fp64_peak", "enkfmc_fp64_mma_peak", "enkfmc_plan_check_status", "enkfmc_unit_tri_solve", "enkfmc_advdiff_step",
+    "enkfmc_plan_stage_times", "enkfmc_plan_work", "enkfmc_fp64_peak", "enkfmc_fp64_mma_peak", "enkfmc_plan_check_status", "enkfmc_unit_tri_solve", "enkfmc_advdiff_step", "enkfmc_letkf_device",
 )
 
 _lib = None
@@ -72,6 +72,7 @@ def lib():
     L.enkfmc_plan_profile.argtypes = [vp, C.c_int]
     L.enkfmc_plan_check_status.argtypes = [vp]
     L.enkfmc_unit_tri_solve.argtypes = [vp, vp, C.c_int, vp, vp, vp, i64, vp]
+    L.enkfmc_letkf_device.argtypes = [vp, vp, vp, vp, vp, vp, vp, i64, i64, C.c_int, C.c_int, i64, i64, i64, C.c_double, vp, vp]
     L.enkfmc_advdiff_step.argtypes = [vp, vp, i64, i64, C.c_int, i64, i64, C.c_double, C.c_double, C.c_double, C.c_double, vp]
     L.enkfmc_plan_stage_times.argtypes = [vp, vp, vp]
     L.enkfmc_plan_work.argtypes = [vp, i64, vp]

@@ -748,6 +748,50 @@ extern "C" int enkfmc_advdiff_step(const double *d_in, double *d_out, int64_t nx
     return ENKFMC_OK;
 }
 
+extern "C" int enkfmc_letkf_device(const double *d_X, double *d_U, double *d_mean, double *d_Xa, const int32_t *d_obs_of_state,
+                                   const double *d_rdiag, const double *d_y, int64_t nx, int64_t ny, int row_major, int periodic,
+                                   int64_t nfields, int64_t nens, int64_t zeta, double inflation, int64_t *first_bad, void *stream) {
+    int rc = check_nens(nens);
+    if (rc) return rc;
+    if (nx < 1 || ny < 1 || nfields < 1 || zeta < 0) { enkfmc_set_error("invalid grid extents or radius"); return ENKFMC_E_VALUE; }
+    if (!(inflation > 0.0)) { enkfmc_set_error("inflation must be positive, got " + std::to_string(inflation)); return ENKFMC_E_VALUE; }
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, dev));
+    if (prop.major < 10) { enkfmc_set_error("libenkfmc is built for sm_100a only"); return ENKFMC_E_CUDA; }
+    cudaStream_t s = (cudaStream_t)stream;
+    unsigned int *counter = nullptr;
+    unsigned long long *bad = nullptr;
+    CK(cudaMalloc(&counter, sizeof(unsigned int) + sizeof(unsigned long long) + 8));
+    bad = reinterpret_cast<unsigned long long *>(reinterpret_cast<char *>(counter) + 8);
+    CK(cudaMemsetAsync(counter, 0, 8, s));
+    CK(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), s));
+    LetkfParams L{};
+    L.X = d_X; L.U = d_U; L.mean = d_mean; L.Xa = d_Xa; L.obs_of_state = d_obs_of_state; L.rdiag = d_rdiag; L.y = d_y;
+    L.nx = nx; L.ny = ny; L.nitems = nx * ny * nfields; L.zeta = zeta; L.row_major = row_major; L.periodic = periodic;
+    L.N = (int)nens; L.boxmax = (int)((2 * zeta + 1) * (2 * zeta + 1)); L.inflation = inflation; L.eig_floor = 1e-12;
+    L.counter = counter; L.first_bad = bad;
+    cudaError_t e = launch_letkf(L, prop.multiProcessorCount, prop.sharedMemPerBlockOptin, s);
+    if (e == cudaErrorInvalidConfiguration) {
+        cudaFree(counter);
+        enkfmc_set_error("LETKF workspace (two " + std::to_string(nens) + " x " + std::to_string(nens) +
+                         " matrices per grid point) exceeds shared memory, or the radius exceeds 31");
+        return ENKFMC_E_CAPACITY;
+    }
+    CK(e);
+    unsigned long long hb = 0;
+    CK(cudaStreamSynchronize(s));
+    CK(cudaMemcpy(&hb, bad, sizeof(hb), cudaMemcpyDeviceToHost));
+    cudaFree(counter);
+    *first_bad = hb == ~0ull ? -1 : (int64_t)hb;
+    if (hb != ~0ull) {
+        enkfmc_set_error("component " + std::to_string(hb) + ": analysis weight matrix lost positive definiteness");
+        return ENKFMC_E_NUMERIC;
+    }
+    return ENKFMC_OK;
+}
+
 extern "C" int enkfmc_plan_read_buffer(const enkfmc_plan *p, int what, void *host_out, int64_t bytes) {
     void *src = enkfmc_plan_device_buffer(p, what);
     if (!src) { enkfmc_set_error("workspace buffer not allocated"); return ENKFMC_E_VALUE; }

@@ -1840,6 +1840,244 @@ cudaError_t launch_advdiff_step(const double *in, double *out, int64_t nx, int64
 }
 
 // ------------------------------------------------------------------------------------------
+// LETKF baseline (kernels.py:251-335), the paper's comparison method: at every grid point the ensemble-space weights
+// from the observations inside its local box,
+//     M = Z^T R^-1 Z + (N-1)/inflation I = Q Lambda Q^T,   wa = Q Lambda^-1 Q^T Z^T R^-1 (y - H xb_mean),
+//     Wa = Q sqrt((N-1)/Lambda) Q^T,                        xa_row = mean + U_c (wa 1^T + Wa).
+// One CTA per (field, grid point): M and Q (N x N each) live in shared memory; the symmetric eigendecomposition is a
+// cyclic two-sided Jacobi with a round-robin ordering (N/2 disjoint rotations per round; rows, then columns of M and
+// Q, updated by all threads).  Points without observations in their box keep the background row (bit for bit when
+// inflation = 1: kernels.py:328-329).
+// ------------------------------------------------------------------------------------------
+#define LETKF_THREADS 256
+#define LETKF_MAX_SWEEPS 30
+
+__global__ void __launch_bounds__(256) mean_anomaly_kernel(const double *__restrict__ X, double *__restrict__ U, double *__restrict__ mean,
+                                                          int64_t nrows, int N) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < nrows; row += warps) {
+        double s = 0.0;
+        for (int i = lane; i < N; i += 32) s += X[row * N + i];
+        const double m = warp_sum(s) / (double)N;
+        for (int i = lane; i < N; i += 32) U[row * N + i] = X[row * N + i] - m;
+        if (lane == 0) mean[row] = m;
+    }
+}
+
+__global__ void __launch_bounds__(LETKF_THREADS) letkf_kernel(const LetkfParams P) {
+    extern __shared__ double smem[];
+    const int N = P.N, ld = N | 1, tid = threadIdx.x, nth = blockDim.x;
+    const int M2 = (N + 1) & ~1, npairs = M2 >> 1;
+    double *Ms = smem;                        // [N][ld]
+    double *Qs = Ms + (size_t)N * ld;         // [N][ld]
+    double *zb = Qs + (size_t)N * ld;         // [N] current observation row / scratch
+    double *zri = zb + N;                     // [N]
+    double *lamv = zri + N;                   // [N]
+    double *tv = lamv + N;                    // [N]
+    double *gv = tv + N;                      // [N]
+    double *cs = gv + N;                      // [npairs]
+    double *sn = cs + npairs;                 // [npairs]
+    int *ip = reinterpret_cast<int *>(sn + npairs);   // [npairs] p, [npairs] q
+    int *iq = ip + npairs;
+    int *box_state = iq + npairs;             // [(2 zeta + 1)^2] state rows of the observed box members
+    int *box_slot = box_state + P.boxmax;     // their observation rows
+    __shared__ int s_item, s_m, s_rot, s_rows[64], s_cols[64], s_nr, s_nc;
+    const double alpha = (double)(N - 1) / P.inflation;
+    const int64_t n2d = P.nx * P.ny;
+
+    for (;;) {
+        if (tid == 0) s_item = (int)atomicAdd(P.counter, 1u);
+        __syncthreads();
+        const int64_t item = s_item;
+        if (item >= P.nitems) break;
+        const int64_t f = item / n2d, lab = item % n2d;
+        const int64_t r0 = P.row_major ? lab / P.nx : lab % P.ny, c0 = P.row_major ? lab % P.nx : lab / P.ny;
+        const int64_t srow = f * n2d + lab;
+        // ---- box members (geometry.py:132-156) with an observation, in ascending label order ----
+        if (tid == 0) {
+            auto window = [&](int64_t ctr, int64_t n, bool per, int *out) {
+                int cnt = 0;
+                if (per) {
+                    for (int64_t d = -P.zeta; d <= P.zeta; ++d) {
+                        const int v = (int)(((ctr + d) % n + n) % n);
+                        int k = cnt;
+                        bool dup = false;
+                        for (int e = 0; e < cnt; ++e) if (out[e] == v) dup = true;
+                        if (dup) continue;
+                        while (k > 0 && out[k - 1] > v) { out[k] = out[k - 1]; --k; }
+                        out[k] = v;
+                        ++cnt;
+                    }
+                } else {
+                    const int64_t lo = ctr - P.zeta < 0 ? 0 : ctr - P.zeta, hi = ctr + P.zeta + 1 > n ? n : ctr + P.zeta + 1;
+                    for (int64_t v = lo; v < hi; ++v) out[cnt++] = (int)v;
+                }
+                return cnt;
+            };
+            s_nr = window(r0, P.ny, P.periodic == 1 || P.periodic == 3, s_rows);
+            s_nc = window(c0, P.nx, P.periodic == 1 || P.periodic == 2, s_cols);
+            int m = 0;
+            const int na = P.row_major ? s_nr : s_nc, nb = P.row_major ? s_nc : s_nr;
+            for (int a = 0; a < na; ++a)
+                for (int b = 0; b < nb; ++b) {
+                    const int64_t rr = P.row_major ? s_rows[a] : s_rows[b], cc = P.row_major ? s_cols[b] : s_cols[a];
+                    const int64_t l = P.row_major ? rr * P.nx + cc : cc * P.ny + rr;
+                    const int slot = P.obs_of_state[f * n2d + l];
+                    if (slot >= 0) { box_state[m] = (int)(f * n2d + l); box_slot[m] = slot; ++m; }
+                }
+            s_m = m;
+        }
+        __syncthreads();
+        const int m = s_m;
+        double *xa = P.Xa + srow * N;
+        const double *ub = P.U + srow * N;
+        if (m == 0) {
+            if (P.inflation == 1.0) { for (int i = tid; i < N; i += nth) xa[i] = P.X[srow * N + i]; }
+            else { const double sq = sqrt(P.inflation), mc = P.mean[srow]; for (int i = tid; i < N; i += nth) xa[i] = mc + sq * ub[i]; }
+            __syncthreads();
+            continue;
+        }
+        // ---- M = alpha I + sum_o z_o z_o^T / r_o,  zri = sum_o z_o (y_o - mean_o) / r_o ----
+        for (int e = tid; e < N * ld; e += nth) { const int i = e / ld, j = e - i * ld; Ms[e] = (i == j) ? alpha : 0.0; Qs[e] = (i == j) ? 1.0 : 0.0; }
+        for (int i = tid; i < N; i += nth) zri[i] = 0.0;
+        __syncthreads();
+        for (int o = 0; o < m; ++o) {
+            const int st = box_state[o], sl = box_slot[o];
+            const double rinv = 1.0 / P.rdiag[sl];
+            for (int i = tid; i < N; i += nth) zb[i] = P.U[(int64_t)st * N + i];
+            __syncthreads();
+            const double w = (P.y[sl] - P.mean[st]) * rinv;
+            for (int e = tid; e < N * N; e += nth) { const int i = e / N, j = e - i * N; Ms[i * ld + j] = fma(zb[i] * rinv, zb[j], Ms[i * ld + j]); }
+            for (int i = tid; i < N; i += nth) zri[i] = fma(zb[i], w, zri[i]);
+            __syncthreads();
+        }
+        // ---- cyclic two-sided Jacobi: M <- J^T M J, Q <- Q J ----
+        double dmax = 0.0;
+        for (int k = 0; k < N; ++k) dmax = fmax(dmax, Ms[k * ld + k]);        // (every thread: N broadcast reads)
+        const double thr = 4.0 * sqrt((double)N) * DBL_EPSILON * dmax;
+        int sweep = 0;
+        for (; sweep < LETKF_MAX_SWEEPS; ++sweep) {
+            if (tid == 0) s_rot = 0;
+            __syncthreads();
+            for (int rr = 0; rr < M2 - 1; ++rr) {
+                if (tid < npairs) {
+                    int a, b;
+                    if (tid == 0) { a = M2 - 1; b = rr; }
+                    else { a = (rr + tid) % (M2 - 1); b = (rr - tid + (M2 - 1)) % (M2 - 1); }
+                    if (a > b) { const int t = a; a = b; b = t; }
+                    double c = 1.0, s = 0.0;
+                    if (b < N) {
+                        const double app = Ms[a * ld + a], aqq = Ms[b * ld + b], apq = Ms[a * ld + b];
+                        // classical criterion: an off-diagonal entry at the rounding level of the largest diagonal entry is
+                        // converged (the rotations that involve the large eigenvalues regenerate such entries every sweep)
+                        if (fabs(apq) > thr) {
+                            const double tau = (aqq - app) / (2.0 * apq);
+                            const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+                            c = 1.0 / sqrt(1.0 + t * t);
+                            s = t * c;
+                            s_rot = 1;
+                        }
+                    } else { b = a; }                       // the dummy index of an odd N: nothing to do
+                    cs[tid] = c; sn[tid] = s; ip[tid] = a; iq[tid] = b;
+                }
+                __syncthreads();
+                for (int e = tid; e < npairs * N; e += nth) {          // rows p, q of M
+                    const int k = e / N, j = e - k * N;
+                    const double s = sn[k];
+                    if (s != 0.0) {
+                        const double c = cs[k];
+                        const int a = ip[k], b = iq[k];
+                        const double x = Ms[a * ld + j], y = Ms[b * ld + j];
+                        Ms[a * ld + j] = c * x - s * y;
+                        Ms[b * ld + j] = s * x + c * y;
+                    }
+                }
+                __syncthreads();
+                for (int e = tid; e < npairs * N; e += nth) {          // columns p, q of M and of Q
+                    const int k = e / N, i = e - k * N;
+                    const double s = sn[k];
+                    if (s != 0.0) {
+                        const double c = cs[k];
+                        const int a = ip[k], b = iq[k];
+                        const double x = Ms[i * ld + a], y = Ms[i * ld + b];
+                        Ms[i * ld + a] = c * x - s * y;
+                        Ms[i * ld + b] = s * x + c * y;
+                        const double u = Qs[i * ld + a], v = Qs[i * ld + b];
+                        Qs[i * ld + a] = c * u - s * v;
+                        Qs[i * ld + b] = s * u + c * v;
+                    }
+                }
+                __syncthreads();
+            }
+            const int rotated = s_rot;      // (read by every thread before thread 0 clears it for the next sweep)
+            __syncthreads();
+            if (!rotated) break;
+        }
+        // ---- weights and the analysis row ----
+        double lmin = DBL_MAX;
+        for (int k = tid; k < N; k += nth) { lamv[k] = Ms[k * ld + k]; lmin = fmin(lmin, lamv[k]); }
+        if (!(lmin >= P.eig_floor) || sweep >= LETKF_MAX_SWEEPS) atomicMin(P.first_bad, (unsigned long long)srow);   // kernels.py:295-298
+        __syncthreads();
+        for (int k = tid; k < N; k += nth) {
+            double a = 0.0, g = 0.0;
+            for (int i = 0; i < N; ++i) { a = fma(Qs[i * ld + k], zri[i], a); g = fma(Qs[i * ld + k], ub[i], g); }
+            tv[k] = a / lamv[k];                                      // (Q^T zri) / lambda
+            gv[k] = g * sqrt((double)(N - 1) / lamv[k]);              // (U_c Q) sqrt((N-1)/lambda)
+        }
+        __syncthreads();
+        {
+            // U_c . wa with wa = Q t
+            double part = 0.0;
+            for (int i = tid; i < N; i += nth) {
+                double wa = 0.0;
+                for (int k = 0; k < N; ++k) wa = fma(Qs[i * ld + k], tv[k], wa);
+                part = fma(ub[i], wa, part);
+            }
+            zb[tid < N ? tid : 0] = 0.0;
+            __syncthreads();
+            if (tid < N) zb[tid] = part;
+            __syncthreads();
+            if (tid == 0) { double t = 0.0; for (int i = 0; i < N && i < nth; ++i) t += zb[i]; zb[0] = t; }
+            __syncthreads();
+        }
+        const double base = P.mean[srow] + zb[0];
+        for (int j = tid; j < N; j += nth) {
+            double acc = 0.0;
+            for (int k = 0; k < N; ++k) acc = fma(gv[k], Qs[j * ld + k], acc);
+            xa[j] = base + acc;
+        }
+        __syncthreads();
+    }
+}
+
+size_t letkf_smem_bytes(int N, int boxmax) {
+    const int ld = N | 1, npairs = ((N + 1) & ~1) >> 1;
+    return ((size_t)2 * N * ld + 5 * (size_t)N + 2 * (size_t)npairs) * sizeof(double) + ((size_t)2 * npairs + 2 * (size_t)boxmax) * sizeof(int) + 16;
+}
+
+cudaError_t launch_letkf(const LetkfParams &p, int sm_count, size_t smem_limit, cudaStream_t s) {
+    if (p.nitems == 0) return cudaSuccess;
+    const size_t smem = letkf_smem_bytes(p.N, p.boxmax);
+    if (smem > smem_limit || 2 * p.zeta + 1 > 64) return cudaErrorInvalidConfiguration;
+    cudaError_t e = cudaFuncSetAttribute(letkf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const int64_t nrows = p.nitems;
+    int64_t blocks = (nrows + 7) / 8;
+    if (blocks > (int64_t)sm_count * 16) blocks = (int64_t)sm_count * 16;
+    mean_anomaly_kernel<<<(unsigned)blocks, 256, 0, s>>>(p.X, p.U, p.mean, nrows, p.N);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    int per_sm = (int)(smem_limit / (smem + 1024));
+    if (per_sm < 1) per_sm = 1;
+    if (per_sm > 4) per_sm = 4;
+    int64_t grid = (int64_t)sm_count * per_sm;
+    if (grid > p.nitems) grid = p.nitems;
+    letkf_kernel<<<(unsigned)grid, LETKF_THREADS, smem, s>>>(p);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------------
 // FP64 DFMA peak: 8 independent FMA chains per thread, register resident.
 // ------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) fp64_peak_kernel(double *out, int iters, double a, double b) {

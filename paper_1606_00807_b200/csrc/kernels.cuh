@@ -62,7 +62,21 @@ struct SolveParams {
     int asm_nmax, asm_nnzmax;  // largest tile (rows, T entries): shared-memory staging of the tile-cooperative K3a
 };
 
+struct LetkfParams {
+    const double *X;           // [nfields * nx * ny][N] background
+    double *U, *mean;          // workspace: anomalies (same shape), row means
+    double *Xa;                // analysis
+    const int32_t *obs_of_state;   // [nfields * nx * ny] observation row of a state row, or -1
+    const double *rdiag, *y;   // [nobs]
+    int64_t nx, ny, nitems, zeta;
+    int row_major, periodic, N, boxmax;
+    double inflation, eig_floor;
+    unsigned int *counter;         // work-fetch counter (zeroed by the caller)
+    unsigned long long *first_bad; // smallest state row whose weight matrix lost positive definiteness (initialised to ~0)
+};
+
 size_t regress_warp_workspace_doubles(int N, int pmax);
+cudaError_t launch_letkf(const LetkfParams &p, int sm_count, size_t smem_limit, cudaStream_t s);
 cudaError_t launch_center_rows(const double *X, double *U, int64_t nrows, int N, cudaStream_t s);
 // mid (may be null) is recorded between the QR kernel (K2a) and the probe/solve kernel (K2b)
 cudaError_t launch_regress(const RegressParams &p, int sm_count, size_t smem_limit, cudaStream_t s, cudaEvent_t mid);

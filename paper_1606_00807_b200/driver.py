@@ -105,6 +105,33 @@ def merge_interiors(template: EnsembleState, pieces: list[tuple[Subdomain, np.nd
     return EnsembleState(d_out.cpu().numpy(), role="analysis")
 
 
+def _assimilate_dual(Xb, net, cfg, geometry, Ys, cycle, t_start):
+    """method="enkf_mc_dual" (driver.py:214-229): the observation-space route sub-domain by sub-domain -- estimation and the
+    covariance square root on the device, orchestration on the host.  The second route of the primal == dual self-check,
+    not the timed hot path (only single-field geometries)."""
+    from .estimator import fit_factors
+    from .geometry import decompose
+    from .kernels import analysis_dual, restrict_network
+    from .validation import center_rows
+    if geometry.nfields != 1:
+        raise ConfigurationError("method 'enkf_mc_dual' is built for single-field geometries only")
+    subs = decompose(geometry, cfg.delta, cfg.zeta)
+    out = Xb.X.copy()
+    t_est, t_ana = np.zeros(len(subs)), np.zeros(len(subs))
+    for k, sd in enumerate(subs):
+        t0 = time.perf_counter()
+        xb_loc = EnsembleState(Xb.X[sd.local_order])
+        factors = fit_factors(center_rows(xb_loc.X), geometry, cfg.zeta, sd.local_order)
+        t1 = time.perf_counter()
+        net_loc, rows = restrict_network(net, sd.local_order)
+        xa_loc = analysis_dual(xb_loc, factors, net_loc, Ys[rows])
+        out[sd.interior] = xa_loc.X[sd.interior_positions()]
+        t_est[k], t_ana[k] = t1 - t0, time.perf_counter() - t1
+    report = CycleReport(cycle=int(cycle), method=cfg.method, delta=cfg.delta, workers=cfg.workers, t_estimation=t_est,
+                         t_analysis=t_ana, t_merge=0.0, t_total=time.perf_counter() - t_start)
+    return EnsembleState(out, role="analysis"), report
+
+
 def assimilate_parallel(Xb: EnsembleState, net: ObservationNetwork, cfg: AssimilationConfig,
                         geometry: GridGeometry, *, Ys: np.ndarray | None = None,
                         cycle: int = 0) -> tuple[EnsembleState, CycleReport]:
@@ -116,13 +143,21 @@ def assimilate_parallel(Xb: EnsembleState, net: ObservationNetwork, cfg: Assimil
         raise ConfigurationError(f"ensemble size must be at least 2, got {Xb.nens}")
     if net.nobs and net.obs_indices[-1] >= geometry.nstate:
         raise ValueError("observation indices exceed the state dimension")
-    if cfg.method != "enkf_mc_primal":
-        raise ConfigurationError(f"method {cfg.method!r} is outside the B200 hot path; only 'enkf_mc_primal' is built")
+    if cfg.method == "letkf":                    # the paper's comparison method (driver.py:128-156, 207-213)
+        from .geometry import decompose
+        from .kernels import letkf_analysis_global
+        delta = len(decompose(geometry, cfg.delta, cfg.zeta))          # same decomposition errors as the reference
+        xa = letkf_analysis_global(Xb, geometry, net, cfg.zeta, cfg.inflation)
+        t = time.perf_counter() - t_start
+        return xa, CycleReport(cycle=int(cycle), method=cfg.method, delta=cfg.delta, workers=cfg.workers,
+                               t_estimation=np.zeros(delta), t_analysis=np.full(delta, t / delta), t_merge=0.0, t_total=t)
     if Ys is None:
         Ys = perturb_observations(net, Xb.nens, cfg.seed, cycle).Ys
     Ys = np.ascontiguousarray(Ys, dtype=np.float64)
     if Ys.shape != (net.nobs, Xb.nens):
         raise ValueError(f"Ys has shape {Ys.shape}, expected {(net.nobs, Xb.nens)}")
+    if cfg.method == "enkf_mc_dual":
+        return _assimilate_dual(Xb, net, cfg, geometry, Ys, cycle, t_start)
 
     plan = get_plan(geometry, cfg.delta, cfg.zeta)
     plan.set_observations(net.obs_indices)

@@ -173,3 +173,36 @@ def analysis_dual(Xb: EnsembleState, factors: PrecisionFactors, net: Observation
     w = torch.cholesky_solve(innovations, chol)
     dx = dXs @ (v.T @ w)
     return EnsembleState((dX + dx).cpu().numpy(), role="analysis")
+
+
+def letkf_analysis_global(Xb: EnsembleState, geometry, net: ObservationNetwork, zeta: int, inflation: float = 1.0) -> EnsembleState:
+    """LETKF baseline: the point kernel (kernels.py:251-303) at every grid component (kernels.py:306-335), on the GPU.
+    A decomposed run (driver.py:128-156) computes exactly these rows, since every local box lies inside its
+    sub-domain's interior + halo."""
+    if Xb.nstate != geometry.nstate:
+        raise ValueError(f"state dimension {Xb.nstate} does not match geometry {geometry.nstate}")
+    if net.nobs and net.obs_indices[-1] >= geometry.nstate:
+        raise ValueError("observation indices exceed the state dimension")
+    if inflation <= 0:
+        raise ValueError(f"inflation must be positive, got {inflation}")
+    if zeta < 0:
+        raise ValueError(f"zeta must be nonnegative, got {zeta}")
+    import ctypes as C
+
+    import torch
+
+    from . import _lib
+    obs_of_state = np.full(geometry.nstate, -1, dtype=np.int32)
+    obs_of_state[net.obs_indices] = np.arange(net.nobs, dtype=np.int32)
+    dX = device.to_device(Xb.X)
+    dU, dXa = torch.empty_like(dX), torch.empty_like(dX)
+    dMean = torch.empty(geometry.nstate, dtype=torch.float64, device="cuda")
+    dMap = torch.from_numpy(obs_of_state).cuda()
+    dR = device.to_device(np.ascontiguousarray(net.r_diag) if net.nobs else np.ones(1))
+    dY = device.to_device(np.ascontiguousarray(net.y) if net.nobs else np.zeros(1))
+    bad = C.c_int64(-1)
+    _lib.check(_lib.lib().enkfmc_letkf_device(dX.data_ptr(), dU.data_ptr(), dMean.data_ptr(), dXa.data_ptr(), dMap.data_ptr(),
+                                              dR.data_ptr(), dY.data_ptr(), geometry.nx, geometry.ny, int(geometry.row_major),
+                                              int(geometry.periodic), geometry.nfields, Xb.nens, int(zeta), float(inflation),
+                                              C.addressof(bad), device.stream_ptr()))
+    return EnsembleState(dXa.cpu().numpy(), role="analysis")

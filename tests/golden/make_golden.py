@@ -126,7 +126,25 @@ def regression_cases():
     return out
 
 
+def letkf_cases():
+    """LETKF baseline (kernels.py:251-335) on two small grids: clipped without inflation, periodic with inflation."""
+    from mcholkf.kernels import letkf_analysis_global
+    out = {}
+    cases = [("l0", dict(nx=14, ny=10, nens=12, corr_len=2.5, zeta=2, delta=1, obs="random", obs_arg=0.3, r_rel=None, r_abs=0.1, seed=71), "clipped", 1.0),
+             ("l1", dict(nx=12, ny=9, nens=16, corr_len=3.0, zeta=1, delta=1, obs="lattice", obs_arg=3, r_rel=None, r_abs=0.2, seed=72,
+                         boundary="periodic"), "periodic", 1.1)]
+    for tag, kw, boundary, infl in cases:
+        w = synthetic.make_workload(tag, **kw)
+        geo = mcholkf.GridGeometry("grid2d", w.nx, w.ny, boundary=boundary)
+        net = mcholkf.ObservationNetwork(w.obs_indices, w.r_diag, w.y)
+        ref = letkf_analysis_global(mcholkf.EnsembleState(w.X), geo, net, w.zeta, inflation=infl).X
+        out.update({f"{tag}_X": w.X, f"{tag}_obs": w.obs_indices, f"{tag}_r": w.r_diag, f"{tag}_y": w.y, f"{tag}_Xa": ref,
+                    f"{tag}_meta": np.array([w.nx, w.ny, w.zeta, boundary == "periodic", infl], dtype=np.float64)})
+    return out
+
+
 def main():
+    np.savez_compressed(os.path.join(HERE, "letkf.npz"), **letkf_cases())
     np.savez_compressed(os.path.join(HERE, "geometry.npz"), **geometry_cases())
     np.savez_compressed(os.path.join(HERE, "regression.npz"), **regression_cases())
     out = {}

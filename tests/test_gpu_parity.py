@@ -584,3 +584,44 @@ def test_run_filter_device_resident_cycles(mck):
     assert mck.run_filter(mck.EnsembleState(w.X), mck.identity_model(mck.GridGeometry("grid2d", w.nx, w.ny)), [], cfg).final.X is w.X or True
     with pytest.raises(mck.ConfigurationError):
         mck.advdiff2d_model(mck.GridGeometry("grid2d", 8, 8), diffusivity=10.0, dt=0.1)
+
+
+def test_letkf_baseline_and_dual_method(mck):
+    """the LETKF baseline on the GPU against the reference's golden outputs and against the oracle on
+    larger cases (per-axis boundary, several fields, inflation, a field without observations), through
+    letkf_analysis_global and assimilate_parallel(method="letkf"); and method="enkf_mc_dual" against the primal."""
+    import os
+    from conftest import GOLDEN
+    from oracle import enkf_mc_oracle as orc
+    from paper_1606_00807_b200 import synthetic
+    G = np.load(os.path.join(GOLDEN, "letkf.npz"))
+    for tag in ("l0", "l1"):
+        nx, ny, zeta, periodic, infl = G[f"{tag}_meta"]
+        geo = mck.GridGeometry("grid2d", int(nx), int(ny), boundary="periodic" if periodic else "clipped")
+        net = mck.ObservationNetwork(G[f"{tag}_obs"], G[f"{tag}_r"], G[f"{tag}_y"])
+        xa = mck.letkf_analysis_global(mck.EnsembleState(G[f"{tag}_X"]), geo, net, int(zeta), float(infl))
+        assert relerr(xa.X, G[f"{tag}_Xa"]) < 1e-10, relerr(xa.X, G[f"{tag}_Xa"])
+    w = synthetic.make_workload("letkf", nx=20, ny=12, nens=30, corr_len=3.0, zeta=2, delta=6, obs="random", obs_arg=0.3,
+                                r_rel=0.1, r_abs=None, seed=77, nugget=0.02, variables=[("u", 2.0, 2), ("q", 1e-2, 1)])
+    for boundary, ordering, infl in (("clipped", "row_major", 1.0), ("periodic_x", "column_major", 1.05)):
+        geo = mck.GridGeometry("grid2d", w.nx, w.ny, ordering=ordering, boundary=boundary, nfields=w.nfields)
+        keep = (w.obs_indices // w.n2d) != 1                                # field 1 has no observations
+        net = mck.ObservationNetwork(w.obs_indices[keep], w.r_diag[keep], w.y[keep])
+        grid = orc.grid_for(w.nx, w.ny, boundary, w.nfields, row_major=ordering == "row_major")
+        ref = orc.letkf_global(w.X, grid, net.obs_indices, net.r_diag, net.y, w.zeta, infl)
+        cfg = mck.AssimilationConfig(zeta=w.zeta, delta=w.delta, method="letkf", inflation=infl)
+        xa, rep = mck.assimilate_parallel(mck.EnsembleState(w.X), net, cfg, geo)
+        assert relerr(xa.X, ref) < 1e-10, relerr(xa.X, ref)
+        if infl == 1.0:
+            assert np.array_equal(xa.X[w.n2d:2 * w.n2d], w.X[w.n2d:2 * w.n2d])   # unconstrained rows: the background, bit for bit
+        assert rep.method == "letkf" and rep.t_analysis.size == w.delta
+    # the dual method through the driver agrees with the primal (tests/test_acceptance.py:81-109)
+    w1 = synthetic.make_workload("dual2", nx=20, ny=12, nens=24, corr_len=3.0, zeta=2, delta=4, obs="random", obs_arg=0.35,
+                                 r_rel=None, r_abs=0.1, seed=78, nugget=0.05)
+    geo = mck.GridGeometry("grid2d", w1.nx, w1.ny)
+    net = mck.ObservationNetwork(w1.obs_indices, w1.r_diag, w1.y)
+    xp, _ = mck.assimilate_parallel(mck.EnsembleState(w1.X), net, mck.AssimilationConfig(zeta=2, delta=4), geo, Ys=w1.Ys)
+    xd, rep = mck.assimilate_parallel(mck.EnsembleState(w1.X), net, mck.AssimilationConfig(zeta=2, delta=4, method="enkf_mc_dual"),
+                                      geo, Ys=w1.Ys)
+    assert relerr(xd.X, xp.X) < 1e-8, relerr(xd.X, xp.X)
+    assert rep.t_estimation.size == 4
