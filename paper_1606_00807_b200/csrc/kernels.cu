@@ -687,7 +687,7 @@ __global__ void __launch_bounds__(256, 1) regress_qr_mma_kernel(const RegressPar
                 const int mb = ob >> 3;
                 const int VP = s_vp[mb];
                 const double *Vblk = Vs + s_voff[mb] - 8 * mb;                 // row r of reflector k: Vblk[k * VP + r]
-                const double *Vb = Vblk + (size_t)g8 * VP + t4;
+                const double *Vb = Vblk + (size_t)g8 * VP + 2 * (g8 >> 2) + t4;
                 double wa0 = 0.0, wa1 = 0.0, wb0 = 0.0, wb1 = 0.0, wc0 = 0.0, wc1 = 0.0, wd0 = 0.0, wd1 = 0.0;
 #pragma unroll
                 for (int mt = 0; mt < NT; ++mt) {
@@ -701,7 +701,7 @@ __global__ void __launch_bounds__(256, 1) regress_qr_mma_kernel(const RegressPar
                 double z0 = 0.0, z1 = 0.0;                                                    // (C^T V T)[g8][2 t4 + {0, 1}]
                 mma_f64(z0, z1, w0, Tb[(2 * t4) * QRM_TP + g8]);
                 mma_f64(z0, z1, w1, Tb[(2 * t4 + 1) * QRM_TP + g8]);
-                const double *V3 = Vblk + (size_t)(2 * t4) * VP + pig;
+                const double *V3 = Vblk + (size_t)(2 * t4) * VP + 2 * (t4 >> 1) + pig;   // reflectors 2 t4, 2 t4 + 1 share the skew
                 z0 = -z0; z1 = -z1;
 #pragma unroll
                 for (int mt = 0; mt < NT; ++mt) {
@@ -730,6 +730,7 @@ __global__ void __launch_bounds__(256, 1) regress_qr_mma_kernel(const RegressPar
             const int VPown = s_vp[m0 & 15];
             double *Vown = Vs + s_voff[m0 & 15] - 8 * m0;                     // this block's reflectors, if stored
             double Trow[8];                              // row g8 of the block's T
+            double vdiag = 0.0;                          // v[j] of this lane's column (lane holding row j), 0 without a reflector
 #pragma unroll
             for (int k = 0; k < 8; ++k) Trow[k] = 0.0;
 #pragma unroll
@@ -782,20 +783,18 @@ __global__ void __launch_bounds__(256, 1) regress_qr_mma_kernel(const RegressPar
                         }
                         Trow[jj] = (g8 < jj) ? -tj * (sA + sB) : (g8 == jj ? tj : 0.0);
                     }
-                    if (stored && g8 == jj) {
-                        double *vdst = Vown + (size_t)jj * VPown + t4;
-#pragma unroll
-                        for (int mt = 1; mt < NT; ++mt)
-                            if (mt > m0) { vdst[8 * mt] = vv[mt][0]; vdst[8 * mt + 4] = vv[mt][1]; }
-                        vdst[8 * m0] = vd[0];
-                        vdst[8 * m0 + 4] = vd[1];
-                    }
-                } else if (stored && g8 == jj) {         // no reflector from this column (p > N): an identity factor
-                    double *vdst = Vown + (size_t)jj * VPown + t4;
-#pragma unroll
-                    for (int mt = 0; mt < NT; ++mt)
-                        if (mt >= m0) { vdst[8 * mt] = 0.0; vdst[8 * mt + 4] = 0.0; }
+                    if (g8 == jj && t4 == (jj & 3)) vdiag = x0 - alpha;       // v[j]: kept for the block's store below
                 }
+            }
+            // ---- the block's reflectors, all eight at once: column g8 of the registers holds reflector g8 below its
+            //      diagonal (later steps of the panel never touch a finished column), v[j] was kept aside, zero above ----
+            if (stored) {
+                double *vdst = Vown + (size_t)g8 * VPown + 2 * (g8 >> 2) + t4;
+#pragma unroll
+                for (int mt = 1; mt < NT; ++mt)
+                    if (mt > m0) { vdst[8 * mt] = c[mt][0]; vdst[8 * mt + 4] = c[mt][1]; }
+                vdst[8 * m0] = t4 > g8 ? dt[0] : (t4 == g8 ? vdiag : 0.0);
+                vdst[8 * m0 + 4] = 4 + t4 > g8 ? dt[1] : (4 + t4 == g8 ? vdiag : 0.0);
             }
             if (stored && t4 == 0) {
                 double *tdst = Ts + (size_t)m0 * 8 * QRM_TP + g8 * QRM_TP;
