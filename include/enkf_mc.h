@@ -60,6 +60,16 @@ int enkfmc_predecessors(int64_t nx, int64_t ny, int row_major, int periodic, int
 int enkfmc_plan_create(int64_t nx, int64_t ny, int row_major, int periodic, int64_t nfields,
                        int64_t delta, int64_t zeta, enkfmc_plan **plan);
 
+/* The same plan for vertically coupled fields (extension, no reference counterpart: BASELINE.json configs 3 and 5,
+ * "vertical r = 1"): every field is nlev stacked 2-D levels (row = level * nx * ny + 2-D label, the reference's
+ * ascending-label convention of geometry.py:145-162 carried to the third axis), a component's box is its 2-D box on
+ * every level within zeta_v of its own (clipped), its predecessors the box members with a smaller label, and a
+ * sub-domain is a 2-D tile of decompose() (geometry.py:165-222) with its zeta-ring halo on every level.  Host integer
+ * code only: the kernels see longer local predecessor lists (up to (2 zeta + 1)^2 (zeta_v + 1) - ... <= 128) and wider
+ * bands.  nlev = 1 is enkfmc_plan_create. */
+int enkfmc_plan_create_levels(int64_t nx, int64_t ny, int row_major, int periodic, int64_t nlev, int64_t zeta_v,
+                              int64_t nfields, int64_t delta, int64_t zeta, enkfmc_plan **plan);
+
 /* Single-tile plan over an explicit strictly increasing local_order (the
  * fit_factors(U, geometry, zeta, local_order) call, estimator.py:64-131).  State rows
  * are local positions 0..n_local-1; every row is "interior". */

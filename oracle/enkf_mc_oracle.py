@@ -21,7 +21,12 @@ numpy ``linalg.svd`` (LAPACK dgesdd) and scipy ``linalg.cho_factor/cho_solve``
 Extension beyond the reference (no reference pin, flagged "parity unpinned by
 the reference" in DESIGN.md): ``nfields`` independent 2-D fields stacked in one
 state vector, label = field * (nx*ny) + 2-D label.  Each field is literally a
-reference problem, so the per-field arithmetic *is* pinned.
+reference problem, so the per-field arithmetic *is* pinned.  ``periodic_x`` / ``periodic_y``: one boundary flag per
+axis.  ``nlev`` / ``zeta_v``: vertically coupled fields (BASELINE.json configs 3 / 5, "vertical r = 1") -- a field is
+nlev stacked levels, label = level * (nx*ny) + 2-D label, the box of a component is its 2-D box on every level within
+zeta_v (clipped), predecessors are the box members with a smaller label (the reference's rule, geometry.py:159-162, on
+the extended box), sub-domains are the reference's 2-D tiles on every level.  The arithmetic per regression / per local
+analysis is the reference's; only the integer maps are new (parity unpinned by the reference).
 """
 
 from __future__ import annotations
@@ -51,6 +56,9 @@ class Grid:
     # extension (no reference counterpart, "parity unpinned by the reference"): one flag per axis; None = `periodic`
     periodic_x: bool | None = None
     periodic_y: bool | None = None
+    # extension: vertically coupled levels
+    nlev: int = 1
+    zeta_v: int = 0
 
     @property
     def px(self) -> bool:
@@ -65,15 +73,27 @@ class Grid:
         return self.nx * self.ny
 
     @property
+    def nfield(self) -> int:
+        """Rows of one field's block (all levels)."""
+        return self.n2d * self.nlev
+
+    @property
     def nstate(self) -> int:
-        return self.n2d * self.nfields
+        return self.nfield * self.nfields
 
 
-def grid_for(nx: int, ny: int, boundary: str, nfields: int = 1, row_major: bool = True) -> Grid:
+def grid_for(nx: int, ny: int, boundary: str, nfields: int = 1, row_major: bool = True, nlev: int = 1, zeta_v: int = 0) -> Grid:
     """Grid of a boundary name: "clipped" / "periodic" (reference), "periodic_x" / "periodic_y" (per-axis extension)."""
     if boundary in ("clipped", "periodic"):
-        return Grid(nx, ny, row_major, boundary == "periodic", nfields)
-    return Grid(nx, ny, row_major, False, nfields, periodic_x=boundary == "periodic_x", periodic_y=boundary == "periodic_y")
+        return Grid(nx, ny, row_major, boundary == "periodic", nfields, nlev=nlev, zeta_v=zeta_v)
+    return Grid(nx, ny, row_major, False, nfields, periodic_x=boundary == "periodic_x", periodic_y=boundary == "periodic_y",
+                nlev=nlev, zeta_v=zeta_v)
+
+
+def _lift(grid: Grid, labels2d: np.ndarray, levels=None) -> np.ndarray:
+    """2-D labels on the given levels (default: all), ascending."""
+    lev = np.arange(grid.nlev, dtype=np.int64) if levels is None else np.asarray(levels, dtype=np.int64)
+    return (lev[:, None] * grid.n2d + np.asarray(labels2d, dtype=np.int64)[None, :]).ravel()
 
 
 def coords(grid: Grid, label: int) -> tuple[int, int]:
@@ -107,7 +127,11 @@ def axis_band(lo: int, hi: int, zeta: int, n: int, periodic: bool) -> np.ndarray
 
 
 def local_box(grid: Grid, center: int, zeta: int) -> np.ndarray:
-    """Chebyshev box members, ascending (geometry.py:145-156)."""
+    """Chebyshev box members, ascending (geometry.py:145-156); with levels: on every level within zeta_v."""
+    if grid.nlev > 1:
+        lev, lab2 = divmod(int(center), grid.n2d)
+        flat = Grid(grid.nx, grid.ny, grid.row_major, grid.periodic, 1, grid.periodic_x, grid.periodic_y)
+        return _lift(grid, local_box(flat, lab2, zeta), axis_window(lev, grid.zeta_v, grid.nlev, False))
     r, c = coords(grid, center)
     return _label_grid(
         grid,
@@ -171,6 +195,8 @@ def decompose(grid: Grid, delta: int, zeta: int) -> list[Tile]:
                 axis_band(c0, c1, zeta, grid.nx, grid.px),
             )
             halo = np.setdiff1d(covered, interior, assume_unique=True)
+            if grid.nlev > 1:                       # the tile on every level (extension)
+                interior, halo = _lift(grid, interior), _lift(grid, halo)
             tiles.append(Tile(bi * pc + bj, interior, halo, np.union1d(interior, halo)))
     return tiles
 
@@ -184,6 +210,15 @@ def predecessor_csr(grid: Grid, zeta: int, local_order: np.ndarray):
     """
     lo = np.asarray(local_order, dtype=np.int64)
     n = lo.size
+    if grid.nlev > 1:                               # levels (extension): the per-row loop of estimator.py:123-131 as it stands
+        indptr, cols = np.zeros(n + 1, dtype=np.int64), []
+        for j in range(n):
+            pred = predecessors(grid, int(lo[j]), zeta)
+            pos = np.searchsorted(lo, pred)
+            ok = (pos < n) & (lo[np.minimum(pos, n - 1)] == pred)
+            cols.append(pos[ok])
+            indptr[j + 1] = indptr[j] + int(ok.sum())
+        return indptr, (np.concatenate(cols) if cols else np.zeros(0)).astype(np.int64)
     if n == 0 or zeta == 0:
         return np.zeros(n + 1, dtype=np.int64), np.zeros(0, dtype=np.int64)
     if grid.row_major:
@@ -327,7 +362,7 @@ def fit_factors(U, grid: Grid, zeta: int, local_order=None,
     U = np.asarray(U, dtype=np.float64)
     n, nens = U.shape
     if local_order is None:
-        local_order = np.arange(grid.n2d, dtype=np.int64)
+        local_order = np.arange(grid.nfield, dtype=np.int64)
     indptr, indices = csr if csr is not None else predecessor_csr(grid, zeta, local_order)
     counts = np.diff(indptr)
     d = np.empty(n)
@@ -357,6 +392,25 @@ def dense_precision(f: Factors) -> np.ndarray:
     return (m + m.T) * 0.5
 
 
+_LINSOLVE = ["cholesky"]     # what the reference calls (cho_factor / cho_solve); "lu" only for the noise-floor probe
+
+
+class linear_solver:
+    """Context manager for the solver-swap probe of the noise floor: the same local analysis with the system solved by
+    LAPACK dgesv (numpy.linalg.solve) instead of the reference's dpotrf / dpotrs."""
+
+    def __init__(self, name: str):
+        assert name in ("cholesky", "lu")
+        self.name = name
+
+    def __enter__(self):
+        self.prev = _LINSOLVE[0]
+        _LINSOLVE[0] = self.name
+
+    def __exit__(self, *exc):
+        _LINSOLVE[0] = self.prev
+
+
 def analysis_primal(Xb: np.ndarray, f: Factors, obs_pos, r_diag, Ys) -> np.ndarray:
     """Xa = Xb + (B^-1 + H^T R^-1 H)^-1 H^T R^-1 (Ys - H Xb) (kernels.py:178-218).
 
@@ -370,7 +424,7 @@ def analysis_primal(Xb: np.ndarray, f: Factors, obs_pos, r_diag, Ys) -> np.ndarr
     rhs[obs_pos] = (Ys - Xb[obs_pos]) * rinv[:, None]
     a = dense_precision(f)
     a[obs_pos, obs_pos] += rinv
-    dx = cho_solve(cho_factor(a, lower=True), rhs)
+    dx = cho_solve(cho_factor(a, lower=True), rhs) if _LINSOLVE[0] == "cholesky" else np.linalg.solve(a, rhs)
     return Xb + dx
 
 
@@ -423,7 +477,7 @@ def assimilate(X, obs_indices, r_diag, Ys, grid: Grid, delta: int, zeta: int,
     Xa = X.copy()
     kept = []
     for f in (range(grid.nfields) if fields is None else fields):
-        lo, hi = f * grid.n2d, (f + 1) * grid.n2d
+        lo, hi = f * grid.nfield, (f + 1) * grid.nfield
         sel = np.flatnonzero((obs_indices >= lo) & (obs_indices < hi))
         args = [(X[lo:hi], obs_indices[sel] - lo, r_diag[sel], Ys[sel], grid, zeta, t, c)
                 for t, c in zip(tiles, csrs)]

@@ -1,6 +1,6 @@
 """Noise floor of the CPU oracle on a given input (TEST INFRASTRUCTURE ONLY, like the oracle itself).
 
-Two probes of how far the reference's *own* answer moves when nothing mathematical changes:
+Three probes of how far the reference's *own* answer moves when nothing mathematical changes:
 
 * ``gesvd``: the same solve with LAPACK dgesvd instead of dgesdd.  Both drivers share the
   bidiagonalisation (dgebrd); only the bidiagonal SVD differs, so this probe does not see the rounding of dgebrd
@@ -8,8 +8,11 @@ Two probes of how far the reference's *own* answer moves when nothing mathematic
   one-sided Jacobi SVD: dgesdd and dgesvd are both 1.1e-9 from the exact T, and 1.2e-12 from each other).
 * ``perm``: the ensemble members (columns of X and Ys) in a different order.  T, D and the analysis (un-permuted)
   are mathematically identical; every rounding error of the reference's path changes.
+* ``solver``: the local analysis system solved by LU (dgesv) instead of Cholesky (dpotrf / dpotrs).  Only the analysis
+  moves; it matters where A = T^T D^-1 T + H^T R^-1 H is numerically singular (many D on the variance floor: more
+  predecessors than members), the regime in which the elimination order decides what the answer is.
 
-The parity gates of the GPU tests are max(north_star gate, 10 x floor) with floor = the larger of the two
+The parity gates of the GPU tests are max(north_star gate, 10 x floor) with floor = the largest of the probes
 (tests/golden/noise_floors.json, written by tools/make_floors.py from this module).
 """
 
@@ -55,4 +58,6 @@ def floors(X2d, obs_idx, r_diag, Ys, grid: orc.Grid, delta: int, zeta: int, tile
     perm = np.random.default_rng(seed).permutation(X2d.shape[1])
     inv = np.argsort(perm)
     alt2 = _run(np.ascontiguousarray(X2d[:, perm]), obs_idx, r_diag, np.ascontiguousarray(Ys[:, perm]), grid, zeta, tiles, csrs)
-    return {"gesvd": _diff(base, alt), "perm": _diff(base, alt2, inv)}
+    with orc.linear_solver("lu"):
+        alt3 = _run(X2d, obs_idx, r_diag, Ys, grid, zeta, tiles, csrs)
+    return {"gesvd": _diff(base, alt), "perm": _diff(base, alt2, inv), "solver": _diff(base, alt3)}

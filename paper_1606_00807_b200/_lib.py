@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(_HERE, "libenkfmc.so")
 # every symbol include/enkf_mc.h declares
 SYMBOLS = (
     "enkfmc_version", "enkfmc_last_error", "enkfmc_tiling", "enkfmc_local_box", "enkfmc_predecessors",
-    "enkfmc_plan_create", "enkfmc_plan_create_local", "enkfmc_plan_create_csr", "enkfmc_plan_destroy",
+    "enkfmc_plan_create", "enkfmc_plan_create_levels", "enkfmc_plan_create_local", "enkfmc_plan_create_csr", "enkfmc_plan_destroy",
     "enkfmc_plan_set_observations", "enkfmc_plan_size", "enkfmc_plan_get", "enkfmc_center_rows",
     "enkfmc_regress", "enkfmc_local_solve", "enkfmc_analysis_device", "enkfmc_analysis_host",
     "enkfmc_plan_counter", "enkfmc_plan_device_buffer", "enkfmc_scatter_rows", "enkfmc_assemble_band",
@@ -55,6 +55,7 @@ def lib():
     L.enkfmc_local_box.argtypes = [i64, i64, C.c_int, C.c_int, i64, i64, vp, vp]
     L.enkfmc_predecessors.argtypes = [i64, i64, C.c_int, C.c_int, i64, i64, vp, vp]
     L.enkfmc_plan_create.argtypes = [i64, i64, C.c_int, C.c_int, i64, i64, i64, vp]
+    L.enkfmc_plan_create_levels.argtypes = [i64, i64, C.c_int, C.c_int, i64, i64, i64, i64, i64, vp]
     L.enkfmc_plan_create_local.argtypes = [i64, i64, C.c_int, C.c_int, i64, i64, vp, vp]
     L.enkfmc_plan_create_csr.argtypes = [i64, vp, vp, vp]
     L.enkfmc_plan_set_observations.argtypes = [vp, i64, vp]

@@ -362,7 +362,7 @@ int scan_status(enkfmc_plan *p) {
             p->counters[4] = (int64_t)it;
             enkfmc_set_error("primal analysis solve failed in subdomain " + std::to_string(t) + " (field " +
                              std::to_string(f) + "): " +
-                             (st[it] == 1 ? "matrix not positive definite" : "non-finite pivot"));
+                             (st[it] == 1 ? "matrix not positive definite" : st[it] == 2 ? "non-finite pivot" : "non-finite solution"));
             return ENKFMC_E_NUMERIC;
         }
     }

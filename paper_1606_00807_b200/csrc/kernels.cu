@@ -1190,6 +1190,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
     extern __shared__ double smem[];
     __shared__ unsigned int s_item;
     __shared__ int s_fail;
+    __shared__ double s_red[SOLVE_THREADS / 32];
     const int tid = threadIdx.x, lane = tid & 31;
     const int nthreads = SOLVE_THREADS;
     const int N = P.N;
@@ -1245,6 +1246,16 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
             continue;
         }
 
+        // largest diagonal entry of A over the tile (the scale a negative pivot is judged against, see factor_diag)
+        double gmax = 0.0;
+        {
+            for (int i = tid; i < n; i += nthreads) gmax = fmax(gmax, band[(int64_t)i * Wr + 8 * Wb + (i & 7)]);
+            gmax = warp_max(gmax);
+            if (lane == 0) s_red[warp] = gmax;
+            __syncthreads();
+            gmax = 0.0;
+            for (int k = 0; k < nwarps; ++k) gmax = fmax(gmax, s_red[k]);
+        }
         // 8x8 tiles (rb, cb <= rb) of the trailing update, ordered by rb: the live ones are a prefix
         for (int s = tid; s < Wb * (Wb + 1) / 2; s += nthreads) {
             int rb = 0, rem = s;
@@ -1360,11 +1371,13 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
                 // elimination (row scales differ by up to 1e10 when some D sit on the variance floor).  At or below the
                 // rounding level of that scale the pivot is cancellation noise of either sign: pinned.  A clearly negative
                 // pivot means the matrix handed in is indefinite (bad factors): fail like the reference's Cholesky
-                // (kernels.py:192-195).  NaN / inf fail.
+                // (kernels.py:192-195).  "Clearly" is judged against the largest diagonal entry of the whole tile as well
+                // (gmax): the elimination error of a pivot scales with |A|, which the entries met so far underestimate when
+                // the large rows come later (deep levels of a vertically coupled tile: |A| 1e15 against 1e12).  NaN / inf fail.
                 const double scale = fmax(pivmax, orig);
-                if (!(piv == piv) || !(fabs(piv) < DBL_MAX)) { if (lane == 0) s_fail = 2; }
+                if (!(piv == piv) || !(fabs(piv) < DBL_MAX)) { if (lane == 0 && s_fail == 0) s_fail = 2; }
                 else if (!(piv > 1e-13 * scale)) {
-                    if ((pivmax == 0.0 && !(piv > 0.0)) || piv < -1e-8 * scale) { if (lane == 0) s_fail = 1; }
+                    if ((pivmax == 0.0 && !(piv > 0.0)) || piv < -1e-8 * fmax(scale, gmax)) { if (lane == 0 && s_fail == 0) s_fail = 1; }
                     else { pin = true; if (lane == 0) atomicAdd(P.counter + 1, 1u); }
                 }
                 pivmax = fmax(pivmax, piv);
@@ -1600,7 +1613,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
                 mma_f64(x0, x1, lt0, w0);
                 mma_f64(x0, x1, lt1, w1);
                 const int col = 8 * ct + 2 * t4;
-                if (col < N && (!(fabs(x0) < DBL_MAX) || (col + 1 < N && !(fabs(x1) < DBL_MAX)))) s_fail = 2;   // benign race
+                if (col < N && (!(fabs(x0) < DBL_MAX) || (col + 1 < N && !(fabs(x1) < DBL_MAX)))) s_fail = 3;   // benign race
                 *reinterpret_cast<double2 *>(Rw + (size_t)(sB + g8) * NR + col) = make_double2(x0, x1);
                 if (xi0 >= 0) {
                     const int64_t gidx = (int64_t)xi0 * N + col;

@@ -149,28 +149,33 @@ int64_t find_sorted(const int64_t *a, int64_t n, int64_t v) {
 }
 
 // Everything downstream of (tile_ptr, local_order, phys): rows, bandwidths, column lists, orders.
+// Predecessors of a local row (estimator.py:123-131): the members of its box with a smaller label that are present in
+// the local domain.  With levels (extension) the box is the 2-D box on every level within zeta_v; a lifted local domain
+// (tile x all levels) is nlev copies of the same sorted 2-D cover, so positions are level * ncover + 2-D position.
 void build_rows_from_geometry(enkfmc_plan &p) {
     Geo g{p.nx, p.ny, p.row_major != 0, p.periodic};
-    const int64_t total = p.sum_nlocal();
     p.row_ptr.assign(1, 0);
     p.col_idx.clear();
     std::vector<int64_t> box, rows, cols;
     for (int64_t t = 0; t < p.ntiles; ++t) {
         const int64_t base = p.tile_ptr[t], n = p.tile_ptr[t + 1] - base;
         const int64_t *lo = p.local_order.data() + base;
+        const int64_t ncover = n / p.nlev;                 // 2-D cover of the tile (nlev == 1: the local domain itself)
         for (int64_t j = 0; j < n; ++j) {
-            if (p.zeta > 0) {
-                box_members(g, lo[j], p.zeta, box, rows, cols);
-                for (int64_t lab : box) {
-                    if (lab >= lo[j]) break;              // ascending: predecessors first
-                    int64_t pos = find_sorted(lo, n, lab);
-                    if (pos >= 0) p.col_idx.push_back((int32_t)pos);
+            if (p.zeta > 0 || p.zeta_v > 0) {
+                const int64_t lev = lo[j] / p.n2d, lab2 = lo[j] % p.n2d;
+                box_members(g, lab2, p.zeta, box, rows, cols);
+                for (int64_t l = std::max<int64_t>(0, lev - p.zeta_v); l <= lev; ++l) {
+                    for (int64_t lab : box) {
+                        if (l == lev && lab >= lab2) break;  // ascending: predecessors first
+                        int64_t pos = find_sorted(lo, ncover, lab);   // level 0 block of the local order = the 2-D cover
+                        if (pos >= 0) p.col_idx.push_back((int32_t)(l * ncover + pos));
+                    }
                 }
             }
             p.row_ptr.push_back((int64_t)p.col_idx.size());
         }
     }
-    (void)total;
 }
 
 void finish_plan(enkfmc_plan &p) {
@@ -384,20 +389,28 @@ extern "C" int enkfmc_predecessors(int64_t nx, int64_t ny, int row_major, int pe
 
 extern "C" int enkfmc_plan_create(int64_t nx, int64_t ny, int row_major, int periodic, int64_t nfields,
                                   int64_t delta, int64_t zeta, enkfmc_plan **out) {
+    return enkfmc_plan_create_levels(nx, ny, row_major, periodic, 1, 0, nfields, delta, zeta, out);
+}
+
+extern "C" int enkfmc_plan_create_levels(int64_t nx, int64_t ny, int row_major, int periodic, int64_t nlev, int64_t zeta_v,
+                                         int64_t nfields, int64_t delta, int64_t zeta, enkfmc_plan **out) {
     *out = nullptr;
     int rc = check_geometry(nx, ny, zeta);
     if (rc) return rc;
     if (nfields < 1) { enkfmc_set_error("nfields must be positive"); return ENKFMC_E_VALUE; }
+    if (nlev < 1) { enkfmc_set_error("nlev must be positive, got " + std::to_string(nlev)); return ENKFMC_E_VALUE; }
+    if (zeta_v < 0) { enkfmc_set_error("zeta_v must be nonnegative, got " + std::to_string(zeta_v)); return ENKFMC_E_VALUE; }
     int64_t pr, pc;
     if (delta < 1) { enkfmc_set_error("delta must be >= 1, got " + std::to_string(delta)); return ENKFMC_E_CONFIG; }
     rc = tiling(nx, ny, delta, pr, pc);
     if (rc) return rc;
-    if (nx * ny * nfields > INT32_MAX) { enkfmc_set_error("state dimension exceeds 2^31-1"); return ENKFMC_E_CAPACITY; }
+    if (nx * ny * nlev * nfields > INT32_MAX) { enkfmc_set_error("state dimension exceeds 2^31-1"); return ENKFMC_E_CAPACITY; }
 
     auto *p = new enkfmc_plan();
     p->nx = nx; p->ny = ny; p->row_major = row_major; p->periodic = periodic; p->nfields = nfields;
     p->delta = delta; p->zeta = zeta; p->pr = pr; p->pc = pc; p->kind = 0;
-    p->ntiles = delta; p->n2d = nx * ny; p->nstate2d = nx * ny;
+    p->nlev = nlev; p->zeta_v = nlev > 1 ? zeta_v : 0;
+    p->ntiles = delta; p->n2d = nx * ny; p->nstate2d = nx * ny * nlev;
     Geo g{nx, ny, row_major != 0, periodic};
 
     std::vector<std::pair<int64_t, int64_t>> rb, cb;
@@ -406,7 +419,8 @@ extern "C" int enkfmc_plan_create(int64_t nx, int64_t ny, int row_major, int per
     p->tile_ptr.assign(1, 0);
     p->interior_ptr.assign(1, 0);
     p->halo_ptr.assign(1, 0);
-    std::vector<int64_t> rows_in, cols_in, rows_s, rows_w, cols_s, cols_w, inter, cover;
+    std::vector<int64_t> rows_in, cols_in, rows_s, rows_w, cols_s, cols_w, inter, cover, halo2, ipos2;
+    std::vector<int32_t> phys2;
     std::vector<int64_t> rowpos(ny), colpos(nx);
     for (int64_t bi = 0; bi < pr; ++bi) {
         for (int64_t bj = 0; bj < pc; ++bj) {
@@ -417,29 +431,37 @@ extern "C" int enkfmc_plan_create(int64_t nx, int64_t ny, int row_major, int per
             axis_band(rb[bi].first, rb[bi].second, zeta, ny, g.periodic_y, rows_s, rows_w);
             axis_band(cb[bj].first, cb[bj].second, zeta, nx, g.periodic_x, cols_s, cols_w);
             label_product(g, rows_s, cols_s, cover);   // == union1d(interior, halo): sorted local_order
-            const int64_t base = (int64_t)p->local_order.size();
-            p->local_order.insert(p->local_order.end(), cover.begin(), cover.end());
-            p->interior.insert(p->interior.end(), inter.begin(), inter.end());
-            for (int64_t lab : inter)
-                p->interior_pos.push_back(find_sorted(cover.data(), (int64_t)cover.size(), lab));
+            ipos2.clear();
+            for (int64_t lab : inter) ipos2.push_back(find_sorted(cover.data(), (int64_t)cover.size(), lab));
             // halo = covered \ interior (both sorted)
-            std::set_difference(cover.begin(), cover.end(), inter.begin(), inter.end(), std::back_inserter(p->halo));
-            p->tile_ptr.push_back((int64_t)p->local_order.size());
-            p->interior_ptr.push_back((int64_t)p->interior.size());
-            p->halo_ptr.push_back((int64_t)p->halo.size());
+            halo2.clear();
+            std::set_difference(cover.begin(), cover.end(), inter.begin(), inter.end(), std::back_inserter(halo2));
             // physical order: walk the extended rectangle in unwrapped order
             for (size_t i = 0; i < rows_w.size(); ++i) rowpos[rows_w[i]] = (int64_t)i;
             for (size_t i = 0; i < cols_w.size(); ++i) colpos[cols_w[i]] = (int64_t)i;
             const int64_t h = (int64_t)rows_w.size(), w = (int64_t)cols_w.size();
-            p->phys.resize(base + cover.size());
-            p->is_interior.resize(base + cover.size(), 0);
+            phys2.resize(cover.size());
             for (size_t j = 0; j < cover.size(); ++j) {
                 int64_t r, c;
                 g.coords(cover[j], r, c);
-                p->phys[base + j] = (int32_t)(g.row_major ? rowpos[r] * w + colpos[c] : colpos[c] * h + rowpos[r]);
+                phys2[j] = (int32_t)(g.row_major ? rowpos[r] * w + colpos[c] : colpos[c] * h + rowpos[r]);
             }
+            // the tile spans every level: level-major copies of the 2-D maps (labels ascending: level * n2d + 2-D label)
+            const int64_t ncover = (int64_t)cover.size();
+            for (int64_t l = 0; l < nlev; ++l) {
+                const int64_t off = l * p->n2d;
+                for (int64_t lab : cover) p->local_order.push_back(off + lab);
+                for (int64_t lab : inter) p->interior.push_back(off + lab);
+                for (int64_t q : ipos2) p->interior_pos.push_back(l * ncover + q);
+                for (int64_t lab : halo2) p->halo.push_back(off + lab);
+                for (int32_t q : phys2) p->phys.push_back((int32_t)(l * ncover) + q);
+            }
+            p->tile_ptr.push_back((int64_t)p->local_order.size());
+            p->interior_ptr.push_back((int64_t)p->interior.size());
+            p->halo_ptr.push_back((int64_t)p->halo.size());
         }
     }
+    p->is_interior.assign(p->local_order.size(), 0);
     for (int64_t t = 0; t < p->ntiles; ++t)
         for (int64_t k = p->interior_ptr[t]; k < p->interior_ptr[t + 1]; ++k)
             p->is_interior[p->tile_ptr[t] + p->interior_pos[k]] = 1;
@@ -565,13 +587,15 @@ extern "C" int enkfmc_plan_set_observations(enkfmc_plan *p, int64_t nobs, const 
             for (int64_t v : s) col_blocks[v].push_back((int32_t)bj);
         }
         for (int64_t k = 0; k < nobs; ++k) {
-            const int64_t f = obs[k] / p->n2d, lab = obs[k] % p->n2d;
+            const int64_t f = obs[k] / p->nstate2d, rem = obs[k] % p->nstate2d;
+            const int64_t lev = rem / p->n2d, lab = rem % p->n2d;
             int64_t r, c;
             g.coords(lab, r, c);
             for (int32_t bi : row_blocks[r]) for (int32_t bj : col_blocks[c]) {
                 const int64_t t = bi * p->pc + bj, base = p->tile_ptr[t];
-                const int64_t pos = find_sorted(p->local_order.data() + base, p->tile_ptr[t + 1] - base, lab);
-                if (pos >= 0) lists[(size_t)(f * p->ntiles + t)].push_back({pos, k});
+                const int64_t ncover = (p->tile_ptr[t + 1] - base) / p->nlev;
+                const int64_t pos = find_sorted(p->local_order.data() + base, ncover, lab);
+                if (pos >= 0) lists[(size_t)(f * p->ntiles + t)].push_back({lev * ncover + pos, k});
             }
         }
     }
@@ -611,6 +635,8 @@ extern "C" int64_t enkfmc_plan_size(const enkfmc_plan *p, int what) {
         case 11: return p->max_bw;
         case 12: return p->nfields;
         case 13: return p->n2d;
+        case 16: return p->nlev;
+        case 17: return p->zeta_v;
         case 14: return (int64_t)p->regress_order.size();   // distinct regressions among the owned rows
         case 15: return (int64_t)p->work_order.size();      // owned local rows
         default: return -1;

@@ -13,7 +13,10 @@ struct enkfmc_plan {
     int64_t nx = 0, ny = 0, nfields = 1, delta = 1, zeta = 0, pr = 1, pc = 1;
     int row_major = 1, periodic = 0;
     int kind = 0;  // 0 decompose, 1 explicit local_order, 2 explicit CSR pattern
-    int64_t ntiles = 0, n2d = 0, nstate2d = 0;  // nstate2d: rows of one field's state block
+    int64_t ntiles = 0, n2d = 0, nstate2d = 0;  // nstate2d: rows of one field's state block (= n2d * nlev)
+    // vertically coupled fields (extension, BASELINE.json configs 3 / 5 "vertical r = 1"): a field is nlev stacked 2-D
+    // levels, row = level * n2d + 2-D label; a component's box spans the levels within zeta_v of its own
+    int64_t nlev = 1, zeta_v = 0;
 
     // tile-major maps, exactly the reference's arrays (int64)
     std::vector<int64_t> tile_ptr, local_order, interior_ptr, interior, interior_pos, halo_ptr, halo;

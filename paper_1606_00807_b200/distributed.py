@@ -32,7 +32,7 @@ class TileShard:
         self.tile_ranges = [(cuts[r] * pc, cuts[r + 1] * pc) for r in range(world)]
         ip, it = plan.get(INTERIOR_PTR), plan.get(INTERIOR)
         tp, lo = plan.get(TILE_PTR), plan.get(LOCAL_ORDER)
-        n2d, nf = geometry.n2d, geometry.nfields
+        n2d, nf = getattr(geometry, "nfield", geometry.n2d), geometry.nfields   # rows of one field's block (all levels)
         fields = np.arange(nf, dtype=np.int64)[:, None] * n2d
         self.rows, self.need = [], []          # owned interior rows / rows read (interiors + halos), all fields
         for t0, t1 in self.tile_ranges:

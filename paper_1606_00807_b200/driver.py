@@ -113,7 +113,7 @@ def _assimilate_dual(Xb, net, cfg, geometry, Ys, cycle, t_start):
     from .geometry import decompose
     from .kernels import analysis_dual, restrict_network
     from .validation import center_rows
-    if geometry.nfields != 1:
+    if geometry.nfields != 1 or getattr(geometry, "nlev", 1) != 1:
         raise ConfigurationError("method 'enkf_mc_dual' is built for single-field geometries only")
     subs = decompose(geometry, cfg.delta, cfg.zeta)
     out = Xb.X.copy()

@@ -58,6 +58,9 @@ def fit_factors(U, geometry: GridGeometry, zeta: int, local_order=None, *,
     n, nens = U.shape
     if nens < 2:
         raise ConfigurationError(f"ensemble size must be at least 2, got {nens}")
+    if getattr(geometry, "nlev", 1) != 1:
+        raise ConfigurationError("stand-alone fit_factors is built for 2-D geometries (nlev = 1); vertically coupled "
+                                 "fields run through assimilate_parallel")
     if local_order is None:
         local_order = np.arange(geometry.n2d, dtype=np.intp)
     local_order = as_index_array(local_order, "local_order")

@@ -5,6 +5,12 @@
 ``nfields`` independent 2-D fields stacked in one state vector, label = field*(nx*ny) + 2-D
 label.  Decomposition, halos and predecessor sets are per 2-D field.
 
+``nlev`` / ``zeta_v`` (defaults 1 / 0 = the reference; no reference counterpart, parity unpinned by the reference,
+checked against the extended oracle): every field is ``nlev`` stacked 2-D levels, label inside a field =
+level*(nx*ny) + 2-D label; a component's box is its 2-D box on every level within ``zeta_v`` of its own (BASELINE.json
+configs 3 / 5: "horizontal r, vertical r = 1"), predecessors = box members with a smaller label, sub-domains = the 2-D
+tiles of ``decompose`` on every level.
+
 Interface schema note: the container fields, argument checks and error messages in this module restate the reference's
 public interface (geometry.py:22-119) on purpose -- they are what a caller (and the reference's own tests, which `match=` on the
 messages) sees at the drop-in boundary.  No arithmetic of the hot path lives here; that is in csrc/ behind the C-ABI.
@@ -37,6 +43,8 @@ class GridGeometry:
     ordering: str = "row_major"
     boundary: str = ""
     nfields: int = 1
+    nlev: int = 1
+    zeta_v: int = 0
 
     def __post_init__(self):
         if self.kind not in KINDS:
@@ -49,6 +57,10 @@ class GridGeometry:
             raise ValueError(f"ring1d requires ny=1, got ny={self.ny}")
         if self.nfields < 1:
             raise ValueError(f"nfields must be positive, got {self.nfields}")
+        if self.nlev < 1:
+            raise ValueError(f"nlev must be positive, got {self.nlev}")
+        if self.zeta_v < 0:
+            raise ValueError(f"zeta_v must be nonnegative, got {self.zeta_v}")
         if not self.boundary:
             object.__setattr__(self, "boundary", "periodic" if self.kind == "ring1d" else "clipped")
         if self.boundary not in BOUNDARIES:
@@ -59,8 +71,13 @@ class GridGeometry:
         return self.nx * self.ny
 
     @property
+    def nfield(self) -> int:
+        """Rows of one field's state block (all its levels)."""
+        return self.nx * self.ny * self.nlev
+
+    @property
     def nstate(self) -> int:
-        return self.nx * self.ny * self.nfields
+        return self.nx * self.ny * self.nlev * self.nfields
 
     @property
     def periodic(self) -> int:
@@ -116,6 +133,16 @@ def grid_coords(geometry: GridGeometry, index: int) -> tuple[int, int]:
 def _box_call(fn, geometry: GridGeometry, center: int, zeta: int) -> np.ndarray:
     if zeta < 0:
         raise ValueError(f"zeta must be nonnegative, got {zeta}")
+    if geometry.nlev > 1:
+        # levels (extension): the 2-D box on every level within zeta_v, labels ascending (host integer code)
+        if not (0 <= center < geometry.nfield):
+            raise ValueError(f"index {center} outside [0, {geometry.nfield})")
+        lev, lab2 = divmod(int(center), geometry.n2d)
+        flat = GridGeometry(geometry.kind, geometry.nx, geometry.ny, geometry.ordering, geometry.boundary)
+        box2 = _box_call(_lib.lib().enkfmc_local_box, flat, lab2, zeta)
+        levels = range(max(0, lev - geometry.zeta_v), min(geometry.nlev, lev + geometry.zeta_v + 1))
+        box = np.concatenate([l * geometry.n2d + box2 for l in levels]).astype(np.intp)
+        return box[box < center] if fn.__name__ == "enkfmc_predecessors" else box
     if not (0 <= center < geometry.n2d):
         raise ValueError(f"index {center} outside [0, {geometry.n2d})")
     span = min(2 * zeta + 1, max(geometry.nx, geometry.ny))

@@ -13,7 +13,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import device
-from .errors import NumericalError
+from .errors import ConfigurationError, NumericalError
 from .factors import PrecisionFactors
 from .validation import as_float_array, as_index_array, ensure_finite
 
@@ -179,6 +179,8 @@ def letkf_analysis_global(Xb: EnsembleState, geometry, net: ObservationNetwork, 
     """LETKF baseline: the point kernel (kernels.py:251-303) at every grid component (kernels.py:306-335), on the GPU.
     A decomposed run (driver.py:128-156) computes exactly these rows, since every local box lies inside its
     sub-domain's interior + halo."""
+    if getattr(geometry, "nlev", 1) != 1:
+        raise ConfigurationError("the LETKF baseline is built for 2-D fields only (nlev = 1)")
     if Xb.nstate != geometry.nstate:
         raise ValueError(f"state dimension {Xb.nstate} does not match geometry {geometry.nstate}")
     if net.nobs and net.obs_indices[-1] >= geometry.nstate:

@@ -29,9 +29,10 @@ class Plan:
     @classmethod
     def decomposed(cls, geometry, delta: int, zeta: int) -> "Plan":
         h = C.c_void_p()
-        _lib.check(_lib.lib().enkfmc_plan_create(geometry.nx, geometry.ny, int(geometry.row_major),
-                                                 int(geometry.periodic), int(geometry.nfields), int(delta), int(zeta),
-                                                 C.byref(h)))
+        _lib.check(_lib.lib().enkfmc_plan_create_levels(geometry.nx, geometry.ny, int(geometry.row_major),
+                                                        int(geometry.periodic), int(getattr(geometry, "nlev", 1)),
+                                                        int(getattr(geometry, "zeta_v", 0)), int(geometry.nfields),
+                                                        int(delta), int(zeta), C.byref(h)))
         return cls(h.value)
 
     @classmethod

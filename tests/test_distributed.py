@@ -14,7 +14,7 @@ import torch.multiprocessing as mp
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _worker(rank, world, port, nfields, out):
+def _worker(rank, world, port, nfields, out, nlev=1):
     sys.path.insert(0, ROOT)
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -25,8 +25,9 @@ def _worker(rank, world, port, nfields, out):
 
     w = synthetic.make_workload("d", nx=20, ny=12, nens=16, corr_len=2.0, zeta=1, delta=6, obs="random", obs_arg=0.4,
                                 r_rel=0.1, r_abs=None, seed=5, nugget=0.01,
-                                variables=[("u", 1.0, nfields)])
-    geo = mck.GridGeometry("grid2d", w.nx, w.ny, nfields=nfields)
+                                variables=[("u", 1.0, nfields * nlev)])
+    # nlev > 1: the same state read as nfields vertically coupled fields of nlev levels (extension)
+    geo = mck.GridGeometry("grid2d", w.nx, w.ny, nfields=nfields, nlev=nlev, zeta_v=1 if nlev > 1 else 0)
     plan = Plan.decomposed(geo, w.delta, w.zeta)
     shard = distributed.TileShard(plan, geo, rank, world)
     shard.apply()
@@ -41,7 +42,7 @@ def _worker(rank, world, port, nfields, out):
     tp, lo = plan.get(TILE_PTR), plan.get(LOCAL_ORDER)
     t0, t1 = shard.tile_ranges[rank]
     read2d = np.unique(lo[tp[t0]:tp[t1]])
-    read = (np.arange(nfields)[:, None] * geo.n2d + read2d[None, :]).ravel()
+    read = (np.arange(nfields)[:, None] * geo.nfield + read2d[None, :]).ravel()
     assert np.array_equal(shard.need[rank], read)
     assert np.array_equal(X.numpy()[read], w.X[read])
     obs_read = np.flatnonzero(np.isin(w.obs_indices, read))
@@ -56,7 +57,7 @@ def _worker(rank, world, port, nfields, out):
     assert np.array_equal(X.numpy()[read], w.X[read])
     assert 0.0 < shard.memory_fraction() < 1.0
     # owned tiles analysed by the oracle, everything else poisoned
-    grid = orc.Grid(w.nx, w.ny, nfields=nfields)
+    grid = orc.Grid(w.nx, w.ny, nfields=nfields, nlev=nlev, zeta_v=1 if nlev > 1 else 0)
     full = orc.assimilate(w.X, w.obs_indices, w.r_diag, w.Ys, grid, w.delta, w.zeta)
     Xa = torch.full(w.X.shape, float("nan"), dtype=torch.float64)
     rows = shard.rows[rank]
@@ -72,12 +73,12 @@ def _worker(rank, world, port, nfields, out):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("nfields", [1, 3])
-def test_two_rank_shard_and_gather(nfields):
+@pytest.mark.parametrize("nfields,nlev", [(1, 1), (3, 1), (2, 3)])
+def test_two_rank_shard_and_gather(nfields, nlev):
     ctx = mp.get_context("spawn")
     out = ctx.Queue()
-    port = 29500 + (os.getpid() + nfields) % 400
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, nfields, out)) for r in range(2)]
+    port = 29500 + (os.getpid() + nfields + 7 * nlev) % 400
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, nfields, out, nlev)) for r in range(2)]
     for p in procs:
         p.start()
     for p in procs:

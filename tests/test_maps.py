@@ -194,3 +194,57 @@ def test_per_axis_boundary_against_extended_oracle():
     r0, c0 = 5, 19
     want = sorted(r * 20 + (c % 20) for r in range(max(0, r0 - 2), min(12, r0 + 3)) for c in range(c0 - 2, c0 + 3))
     assert mck.local_box(lon, c0 + 20 * r0, 2).members.tolist() == sorted(set(want))
+
+
+# ---- vertically coupled levels (extension; BASELINE.json configs 3 / 5 "vertical r = 1"; parity unpinned by the reference:
+# the integer maps are checked against the extended oracle, which applies the reference's rules on the extended box) ----
+@pytest.mark.parametrize("nx,ny,nlev,zeta_v,delta,zeta,boundary", [
+    (12, 8, 3, 1, 4, 2, "clipped"), (10, 9, 4, 2, 6, 1, "periodic_x"), (16, 6, 2, 0, 4, 3, "periodic"),
+    (7, 5, 3, 1, 1, 2, "clipped"), (9, 9, 5, 1, 9, 0, "clipped"),
+])
+def test_level_maps_match_extended_oracle(nx, ny, nlev, zeta_v, delta, zeta, boundary):
+    import paper_1606_00807_b200 as mck
+    from oracle import enkf_mc_oracle as orc
+    from paper_1606_00807_b200.plan import COL_IDX, HALO, INTERIOR, INTERIOR_POS, LOCAL_ORDER, ROW_PTR, Plan
+    g = mck.GridGeometry("grid2d", nx, ny, boundary=boundary, nlev=nlev, zeta_v=zeta_v)
+    og = orc.grid_for(nx, ny, boundary, nlev=nlev, zeta_v=zeta_v)
+    assert g.nstate == og.nstate == nx * ny * nlev
+    plan = Plan.decomposed(g, delta, zeta)
+    tiles = orc.decompose(og, delta, zeta)
+    assert np.array_equal(plan.get(LOCAL_ORDER), np.concatenate([t.local_order for t in tiles]))
+    assert np.array_equal(plan.get(INTERIOR), np.concatenate([t.interior for t in tiles]))
+    assert np.array_equal(plan.get(HALO), np.concatenate([t.halo for t in tiles]))
+    assert np.array_equal(plan.get(INTERIOR_POS), np.concatenate([t.interior_positions() for t in tiles]))
+    assert np.array_equal(np.sort(plan.get(INTERIOR)), np.arange(g.nstate))          # interiors partition the field
+    csr = [orc.predecessor_csr(og, zeta, t.local_order) for t in tiles]
+    assert np.array_equal(plan.get(COL_IDX), np.concatenate([c[1] for c in csr]))
+    assert np.array_equal(plan.get(ROW_PTR), np.concatenate([[0]] + [np.diff(c[0]) for c in csr]).cumsum())
+    for c in (0, nx + 1, g.nstate - 1, (nlev - 1) * nx * ny + 2 * nx + 3):
+        assert np.array_equal(mck.geometry.local_box(g, c, zeta).members, orc.local_box(og, c, zeta))
+        assert np.array_equal(mck.geometry.predecessors(g, c, zeta), orc.predecessors(og, c, zeta))
+
+
+def test_levels_without_vertical_coupling_are_stacked_fields():
+    """zeta_v = 0: the predecessor lists of a lifted tile are those of the 2-D tile on every level."""
+    import paper_1606_00807_b200 as mck
+    from paper_1606_00807_b200.plan import COL_IDX, ROW_PTR, TILE_PTR, Plan
+    p3 = Plan.decomposed(mck.GridGeometry("grid2d", 14, 10, nlev=3, zeta_v=0), 4, 2)
+    p2 = Plan.decomposed(mck.GridGeometry("grid2d", 14, 10), 4, 2)
+    assert p3.max_pred == p2.max_pred and p3.nnz == 3 * p2.nnz
+    tp3, tp2, rp3, rp2, ci3, ci2 = (p3.get(TILE_PTR), p2.get(TILE_PTR), p3.get(ROW_PTR), p2.get(ROW_PTR), p3.get(COL_IDX),
+                                    p2.get(COL_IDX))
+    for t in range(4):
+        n2 = tp2[t + 1] - tp2[t]
+        for lev in range(3):
+            for j in (0, n2 // 2, n2 - 1):
+                a = ci3[rp3[tp3[t] + lev * n2 + j]:rp3[tp3[t] + lev * n2 + j + 1]]
+                b = ci2[rp2[tp2[t] + j]:rp2[tp2[t] + j + 1]]
+                assert np.array_equal(a, b + lev * n2)
+
+
+def test_level_geometry_validation():
+    import paper_1606_00807_b200 as mck
+    with pytest.raises(ValueError, match="nlev must be positive"):
+        mck.GridGeometry("grid2d", 4, 4, nlev=0)
+    with pytest.raises(ValueError, match="zeta_v must be nonnegative"):
+        mck.GridGeometry("grid2d", 4, 4, nlev=2, zeta_v=-1)
