@@ -325,6 +325,8 @@ int do_solve(enkfmc_plan *p, const double *d_X, const double *d_T, const double 
     S.asm_nnzmax = 0;
     for (int64_t t = 0; t < p->ntiles; ++t)
         S.asm_nnzmax = std::max<int>(S.asm_nnzmax, (int)(p->row_ptr[p->tile_ptr[t + 1]] - p->row_ptr[p->tile_ptr[t]]));
+    S.all_mono = 1;
+    for (uint8_t m : p->tile_mono) if (!m) S.all_mono = 0;
     int rc2 = ensure_band(p);
     if (rc2) return rc2;
     S.band = d->band - d->band_off0;          // band_ptr[t] counts from tile 0: biased by the first owned tile's offset
@@ -689,6 +691,8 @@ extern "C" int enkfmc_assemble_band(enkfmc_plan *p, const double *d_T, const dou
     S.nrows_owned = (int64_t)p->work_order.size();
     S.assemble_only = 1; S.f0 = 0; S.f1 = 1; S.band = d_band;
     S.tile_order = d->tile_order; S.tile_mono = d->tile_mono; S.asm_nmax = (int)p->max_nlocal; S.asm_nnzmax = (int)std::min<int64_t>(p->nnz(), 1 << 30);
+    S.all_mono = 1;
+    for (uint8_t m : p->tile_mono) if (!m) S.all_mono = 0;
     {
         cudaError_t e = launch_assemble_band(S, d->sm_count, d->smem_limit, (cudaStream_t)stream);
         if (e == cudaErrorInvalidConfiguration) {

@@ -1167,6 +1167,96 @@ __global__ void __launch_bounds__(ASMT_THREADS) assemble_band_tile_kernel(const 
     }
 }
 
+// Tensor-core form of K3a: A = T~^T D^-1 T~ as a banded SYRK of 8 x 8 tiles, one CTA per (field, tile).  For tiles whose
+// physical order is the local order (every clipped tile) T~ is lower triangular with its entries inside the band, so
+//     A[I, K] = sum_{J = I}^{K + Wb} T~[J, I]^T D_J^-1 T~[J, K]        (8 x 8 blocks, K <= I <= K + Wb).
+// Block rows of T~ are scattered from the CSR values into a ring of Wb + 2 dense 8 x Wr slots in shared memory (zeros where
+// the pattern has no entry); block row I of A then takes (Wb + 1)(Wb + 2) / 2 tile products of two mma.m8n8k4 each: warp d
+// accumulates tile (I, I - d) over its J in ascending order (two interleaved accumulator chains, added at the end: a fixed
+// order, results are deterministic), while the warps with the short chains scatter block row I + Wb + 1 into the free slot --
+// one barrier per block row.  Same band layout as the gather forms; the sums run over the same terms in the same order of
+// rows j, grouped four at a time by the tensor-core product.
+#define ASMM_THREADS 512
+__host__ __device__ inline int asmm_pitch(int Wr) { int v = Wr + 4; while (v % 16 != 4) ++v; return v; }   // fragment loads t4 * pitch + g8: conflict-free
+__host__ __device__ inline size_t asmm_smem_bytes(int bmax) {
+    const int Wr = 8 * (solve_wb(bmax) + 1);
+    return ((size_t)(Wr + 8) * asmm_pitch(Wr) + (size_t)(Wr + 8)) * sizeof(double);
+}
+
+__global__ void __launch_bounds__(ASMM_THREADS) assemble_band_mma_kernel(const SolveParams P) {
+    extern __shared__ double smem[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = ASMM_THREADS / 32;
+    const int g8 = lane >> 2, t4 = lane & 3;
+    const int nf = P.f1 - P.f0;
+    const int t = P.tile_order[blockIdx.x / nf];
+    const int fl = (int)(blockIdx.x % nf), f = P.f0 + fl;
+    if (!P.assemble_only && P.tile_nobs[(int64_t)f * P.ntiles + t] == 0) return;
+    const int64_t base = P.tile_ptr[t];
+    const int n = (int)(P.tile_ptr[t + 1] - base), nb = (n + 7) >> 3;
+    const int Wb = solve_wb(P.bw[t]), Wr = 8 * (Wb + 1), pitch = asmm_pitch(Wr), nslot = Wb + 2;
+    double *ring = smem;                                   // [nslot][8][pitch]
+    double *dinv = ring + (size_t)nslot * 8 * pitch;       // [nslot][8]
+    const double *Tf = P.T + (int64_t)f * P.tstride;
+    const double *Df = P.D + (int64_t)f * P.dstride + base;
+    double *band = P.band + (int64_t)fl * P.band_stride + P.band_ptr[t];
+
+    // row jr of block row J into its ring slot (one warp): zeros, then the row's entries at column - 8 (J - Wb)
+    auto load_row = [&](int J, int jr) {
+        const int sl = J % nslot, j = 8 * J + jr;
+        double *S = ring + ((size_t)sl * 8 + jr) * pitch;
+        for (int e = lane; e < Wr; e += 32) S[e] = 0.0;
+        __syncwarp();
+        double dv = 0.0;
+        if (j < n) {
+            const int c0 = 8 * (J - Wb);
+            const int64_t q0 = P.row_ptr[base + j];
+            const int cnt = (int)(P.row_ptr[base + j + 1] - q0);
+            for (int m = lane - 1; m < cnt; m += 32) {
+                if (m < 0) S[j - c0] = 1.0;
+                else S[P.col_idx[q0 + m] - c0] = Tf[q0 + m];
+            }
+            dv = 1.0 / Df[j];
+        }
+        if (lane == 0) dinv[sl * 8 + jr] = dv;
+    };
+    for (int idx = warp; idx < 8 * (Wb + 1); idx += nwarps)
+        if ((idx >> 3) < nb) load_row(idx >> 3, idx & 7);
+    __syncthreads();
+
+    for (int I = 0; I < nb; ++I) {
+        for (int d = warp; d <= Wb; d += nwarps) {
+            const int K = I - d;
+            double p0 = 0.0, p1 = 0.0, q0 = 0.0, q1 = 0.0;
+            if (K >= 0) {
+                const int Jend = (I + Wb - d < nb - 1) ? I + Wb - d : nb - 1;
+                for (int J = I; J <= Jend; ++J) {
+                    const int sl = J % nslot;
+                    const double *S = ring + ((size_t)sl * 8 + t4) * pitch + g8;
+                    const int oi = 8 * (I - J + Wb), ok = 8 * (K - J + Wb);
+                    const double a0 = S[oi] * dinv[sl * 8 + t4], a1 = S[(size_t)4 * pitch + oi] * dinv[sl * 8 + 4 + t4];
+                    const double b0 = S[ok], b1 = S[(size_t)4 * pitch + ok];
+                    if ((J - I) & 1) { mma_f64(q0, q1, a0, b0); mma_f64(q0, q1, a1, b1); }
+                    else { mma_f64(p0, p1, a0, b0); mma_f64(p0, p1, a1, b1); }
+                }
+            }
+            double v0 = p0 + q0, v1 = p1 + q1;              // A[8 I + g8, 8 K + 2 t4 + {0, 1}]
+            const int i = 8 * I + g8;
+            if (d == 0) {
+                if (2 * t4 > g8) v0 = 0.0;                   // row form keeps the lower triangle of the diagonal block
+                if (2 * t4 + 1 > g8) v1 = 0.0;
+                if (!P.assemble_only && i < n && (g8 >> 1) == t4) {
+                    const int sl = P.obs_slot[(int64_t)f * P.nloc + base + i];
+                    if (sl >= 0) { const double ri = 1.0 / P.rdiag[sl]; if (g8 & 1) v1 += ri; else v0 += ri; }
+                }
+            }
+            if (i < n) *reinterpret_cast<double2 *>(band + (int64_t)i * Wr + 8 * (Wb - d) + 2 * t4) = make_double2(v0, v1);
+        }
+        // block row I + Wb + 1 goes into the slot that is free during this step (the warps with the short chains do it)
+        if (warp >= nwarps - 8 && I + Wb + 1 < nb) load_row(I + Wb + 1, warp - (nwarps - 8));
+        __syncthreads();
+    }
+}
+
 __host__ __device__ inline size_t solve_strip_doubles(int Wb) { return (((4 * (size_t)Wb * (Wb + 1) * 2 + 7) / 8 + 1) & ~(size_t)1); }
 __host__ __device__ inline size_t solve_rowsrc_doubles(int rows) { return ((3 * (size_t)rows * 4 + 15) / 16) * 2; }
 
@@ -1693,6 +1783,14 @@ cudaError_t launch_assemble_band(const SolveParams &p, int sm_count, size_t smem
     const size_t tile_smem = asm_tile_smem_bytes(p.asm_nmax, p.asm_nnzmax, p.bmax);
     // (ENKFMC_K3A=rows forces the warp-per-row form that large tiles fall back to: tests compare the two)
     const char *k3a_sel = getenv("ENKFMC_K3A");
+    // tensor-core form: every tile in its local order and a ring that fits (ENKFMC_K3A=tile / rows force the gather forms)
+    if (p.all_mono && !k3a_sel && asmm_smem_bytes(p.bmax) + 2048 <= smem_limit) {
+        const size_t smem = asmm_smem_bytes(p.bmax);
+        cudaError_t e = cudaFuncSetAttribute(assemble_band_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        assemble_band_mma_kernel<<<(unsigned)((int64_t)p.ntiles_owned * (p.f1 - p.f0)), ASMM_THREADS, smem, s>>>(p);
+        return cudaGetLastError();
+    }
     if (p.asm_nmax > 0 && p.asm_nmax < 65536 && p.asm_nnzmax < 65536 && tile_smem + 2048 <= smem_limit &&   // 1 KB is reserved per CTA
         !(k3a_sel && k3a_sel[0] == 'r')) {
         cudaError_t e = cudaFuncSetAttribute(assemble_band_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

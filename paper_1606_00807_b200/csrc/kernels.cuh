@@ -60,6 +60,7 @@ struct SolveParams {
     const int32_t *work_order; // owned local rows
     int64_t nrows_owned;
     int asm_nmax, asm_nnzmax;  // largest tile (rows, T entries): shared-memory staging of the tile-cooperative K3a
+    int all_mono;              // every tile's physical order is its local order: the tensor-core form of K3a applies
 };
 
 struct LetkfParams {

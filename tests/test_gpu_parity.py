@@ -158,8 +158,9 @@ def test_dense_precision_and_apply(mck):
 
 
 def test_assembly_forms_agree(mck, monkeypatch):
-    """K3a has a tile-cooperative form (tile staged in shared memory) and a warp-per-row form for tiles that do
-    not fit: the same band to rounding, and the same analysis through either."""
+    """K3a has three forms: the tensor-core banded SYRK (tiles in their local order), the tile-cooperative gather (tile
+    staged in shared memory) and the warp-per-row gather for tiles that fit neither: the same band to rounding, and the
+    same analysis through each."""
     import scipy.sparse as sp
     from paper_1606_00807_b200 import synthetic
     rng = np.random.default_rng(11)
@@ -167,18 +168,33 @@ def test_assembly_forms_agree(mck, monkeypatch):
     low = np.tril(rng.standard_normal((n, n)), -1) * (rng.random((n, n)) < 0.2)
     f = mck.PrecisionFactors(sp.csr_matrix(low), rng.random(n) + 0.5)
     monkeypatch.delenv("ENKFMC_K3A", raising=False)
+    a_mma = f.dense_precision()
+    monkeypatch.setenv("ENKFMC_K3A", "tile")
     a_tile = f.dense_precision()
     monkeypatch.setenv("ENKFMC_K3A", "rows")
     a_rows = f.dense_precision()
     assert np.allclose(a_tile, a_rows, rtol=1e-14, atol=1e-14)
+    assert np.allclose(a_mma, a_rows, rtol=1e-13, atol=1e-13)
     w = synthetic.config("cfg2", nugget=0.01)
     geo = mck.GridGeometry("grid2d", w.nx, w.ny)
     net = mck.ObservationNetwork(w.obs_indices, w.r_diag, w.y)
     cfg = mck.AssimilationConfig(zeta=w.zeta, delta=w.delta)
     x_rows, _ = mck.assimilate_parallel(mck.EnsembleState(w.X), net, cfg, geo, Ys=w.Ys)
-    monkeypatch.delenv("ENKFMC_K3A", raising=False)
+    monkeypatch.setenv("ENKFMC_K3A", "tile")
     x_tile, _ = mck.assimilate_parallel(mck.EnsembleState(w.X), net, cfg, geo, Ys=w.Ys)
+    monkeypatch.delenv("ENKFMC_K3A", raising=False)
+    x_mma, _ = mck.assimilate_parallel(mck.EnsembleState(w.X), net, cfg, geo, Ys=w.Ys)
     assert relerr(x_rows.X, x_tile.X) < 1e-11
+    assert relerr(x_rows.X, x_mma.X) < 1e-11
+    # a periodic tiling has tiles whose band order is not the local order: those plans keep the gather forms
+    wp = synthetic.config("cfg1", boundary="periodic", nugget=0.01)
+    geo_p = mck.GridGeometry("grid2d", wp.nx, wp.ny, boundary="periodic")
+    net_p = mck.ObservationNetwork(wp.obs_indices, wp.r_diag, wp.y)
+    cfg_p = mck.AssimilationConfig(zeta=wp.zeta, delta=wp.delta)
+    x_def, _ = mck.assimilate_parallel(mck.EnsembleState(wp.X), net_p, cfg_p, geo_p, Ys=wp.Ys)
+    monkeypatch.setenv("ENKFMC_K3A", "rows")
+    x_r, _ = mck.assimilate_parallel(mck.EnsembleState(wp.X), net_p, cfg_p, geo_p, Ys=wp.Ys)
+    assert relerr(x_def.X, x_r.X) < 1e-5      # the oracle's own noise floor on this input is 3.8e-6 (tests/golden/noise_floors.json)
 
 
 def test_analysis_edge_cases(mck):
