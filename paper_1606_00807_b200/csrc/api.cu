@@ -56,7 +56,7 @@ struct DeviceState {
     double *dX = nullptr, *dXa = nullptr, *dR = nullptr, *dYs = nullptr;
     int64_t stage_nens = 0, stage_nobs = -1;
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
-    cudaStream_t stream = nullptr, copy_stream = nullptr;
+    cudaStream_t stream = nullptr, copy_stream = nullptr, down_stream = nullptr;   // kernels, uploads, downloads
     std::vector<cudaEvent_t> hev;    // events of the pipelined host path
 };
 
@@ -124,6 +124,7 @@ int init_device(enkfmc_plan *p) {
     for (auto &ev : d->ev) CK(cudaEventCreate(&ev));
     CK(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&d->copy_stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&d->down_stream, cudaStreamNonBlocking));
     return ENKFMC_OK;
 }
 
@@ -388,6 +389,7 @@ void enkfmc_device_release(enkfmc_plan *p) {
     for (auto &ev : d->ev) if (ev) cudaEventDestroy(ev);
     for (auto &ev : d->hev) cudaEventDestroy(ev);
     if (d->copy_stream) cudaStreamDestroy(d->copy_stream);
+    if (d->down_stream) cudaStreamDestroy(d->down_stream);
     for (auto &ev : d->prof) cudaEventDestroy(ev);
     if (d->stream) cudaStreamDestroy(d->stream);
     delete d;
@@ -561,7 +563,7 @@ extern "C" int enkfmc_analysis_host(enkfmc_plan *p, const double *X, const doubl
     }
     // Pipelined over groups of fields: the copy stream uploads group g + 1 and downloads the analysis of group
     // g - 1 while the compute stream works on group g (fields are independent: PAPER.md:201).
-    cudaStream_t s = d->stream, cs = d->copy_stream;
+    cudaStream_t s = d->stream, cs = d->copy_stream, ds = d->down_stream;
     // tiles outside the owned range are never written: start every analysis from a clean status array
     CK(cudaMemsetAsync(d->status, 0, std::max<size_t>(1, (size_t)p->ntiles * p->nfields) * sizeof(int32_t), s));
     // Five groups for a dozen fields or more, the first and the last small (the kernels start after a short upload and
@@ -591,7 +593,10 @@ extern "C" int enkfmc_analysis_host(enkfmc_plan *p, const double *X, const doubl
     auto EV = [&](int g, int k) { return d->hev[2 + 8 * (size_t)g + k]; };   // 0,1 X up; 7 Ys up; 2,3,4 compute; 5,6 down
     const size_t rowbytes = (size_t)nens * sizeof(double);
     auto fcut = [&](int g) { return cuts[(size_t)g]; };
-    for (int g = 0; g < ngroups; ++g) {
+    // Issue order: upload g + 1 and download g - 1 are queued right after the kernels of group g.  With page-locked host
+    // arrays every call returns at once and the order is immaterial; with ordinary (pageable) arrays a copy blocks the host
+    // while it is staged, and this order lets the staging of the neighbouring groups run while the device computes group g.
+    auto upload_group = [&](int g) -> int {
         const size_t r0 = (size_t)fcut(g) * p->nstate2d, r1 = (size_t)fcut(g + 1) * p->nstate2d;
         CK(cudaEventRecord(EV(g, 0), cs));
         CK(cudaMemcpyAsync(d->dX + r0 * nens, X + r0 * nens, (r1 - r0) * rowbytes, cudaMemcpyHostToDevice, cs));
@@ -605,7 +610,18 @@ extern "C" int enkfmc_analysis_host(enkfmc_plan *p, const double *X, const doubl
             CK(cudaMemcpyAsync(d->dYs + o0 * nens, Ys + o0 * nens, (size_t)(o1 - o0) * rowbytes, cudaMemcpyHostToDevice, cs));
         CK(cudaEventRecord(EV(g, 7), cs));
         if (g == ngroups - 1) CK(cudaEventRecord(evY1, cs));
-    }
+        return ENKFMC_OK;
+    };
+    auto download_group = [&](int g) -> int {
+        const size_t r0 = (size_t)fcut(g) * p->nstate2d, r1 = (size_t)fcut(g + 1) * p->nstate2d;
+        CK(cudaStreamWaitEvent(ds, EV(g, 4), 0));
+        CK(cudaEventRecord(EV(g, 5), ds));
+        CK(cudaMemcpyAsync(Xa + r0 * nens, d->dXa + r0 * nens, (r1 - r0) * rowbytes, cudaMemcpyDeviceToHost, ds));
+        CK(cudaEventRecord(EV(g, 6), ds));
+        return ENKFMC_OK;
+    };
+    auto drain = [&]() { cudaStreamSynchronize(cs); cudaStreamSynchronize(ds); cudaStreamSynchronize(s); };
+    if ((rc = upload_group(0))) { drain(); return rc; }
     for (int g = 0; g < ngroups; ++g) {
         const int64_t f0 = fcut(g), f1 = fcut(g + 1);
         const size_t r0 = (size_t)f0 * p->nstate2d, r1 = (size_t)f1 * p->nstate2d;
@@ -613,18 +629,18 @@ extern "C" int enkfmc_analysis_host(enkfmc_plan *p, const double *X, const doubl
         CK(cudaEventRecord(EV(g, 2), s));
         CK(launch_center_rows(d->dX + r0 * nens, d->U + r0 * nens, (int64_t)(r1 - r0), (int)nens, s));
         p->counters[0] += 1;
-        if ((rc = do_regress(p, d->U, nens, rank_tol, floor_, d->T, d->D, d->flags, s, nullptr, f0, f1, true))) { cudaStreamSynchronize(cs); cudaStreamSynchronize(s); return rc; }
+        if ((rc = do_regress(p, d->U, nens, rank_tol, floor_, d->T, d->D, d->flags, s, nullptr, f0, f1, true))) { drain(); return rc; }
         CK(cudaEventRecord(EV(g, 3), s));
         CK(cudaStreamWaitEvent(s, EV(g, 7), 0));
         if (p->tile_begin != 0 || p->tile_end != p->ntiles)   // a rank's share: rows it does not own come back as the background
             CK(cudaMemcpyAsync(d->dXa + r0 * nens, d->dX + r0 * nens, (r1 - r0) * rowbytes, cudaMemcpyDeviceToDevice, s));
-        if ((rc = do_solve(p, d->dX, d->T, d->D, d->dR, d->dYs, nens, d->dXa, d->status, s, f0, f1, true))) { cudaStreamSynchronize(cs); cudaStreamSynchronize(s); return rc; }
+        if ((rc = do_solve(p, d->dX, d->T, d->D, d->dR, d->dYs, nens, d->dXa, d->status, s, f0, f1, true))) { drain(); return rc; }
         CK(cudaEventRecord(EV(g, 4), s));
-        CK(cudaStreamWaitEvent(cs, EV(g, 4), 0));
-        CK(cudaEventRecord(EV(g, 5), cs));
-        CK(cudaMemcpyAsync(Xa + r0 * nens, d->dXa + r0 * nens, (r1 - r0) * rowbytes, cudaMemcpyDeviceToHost, cs));
-        CK(cudaEventRecord(EV(g, 6), cs));
+        if (g + 1 < ngroups && (rc = upload_group(g + 1))) { drain(); return rc; }
+        if (g >= 1 && (rc = download_group(g - 1))) { drain(); return rc; }
     }
+    if ((rc = download_group(ngroups - 1))) { drain(); return rc; }
+    CK(cudaStreamSynchronize(ds));
     CK(cudaStreamSynchronize(cs));
     CK(cudaStreamSynchronize(s));
     if (timings_ms) {   // busy time of each stage, summed over the groups (the stages overlap in wall-clock time)

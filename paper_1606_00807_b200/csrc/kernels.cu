@@ -1223,7 +1223,32 @@ __global__ void __launch_bounds__(ASMM_THREADS) assemble_band_mma_kernel(const S
         if ((idx >> 3) < nb) load_row(idx >> 3, idx & 7);
     __syncthreads();
 
+    // The warps with the short chains (the last eight) fill the slot that is free during a step with block row I + Wb + 1,
+    // one row each.  The row's values travel through registers: its CSR range is read one step ahead and the values / columns
+    // at the top of the step, so that both global latencies pass under the tile products; the slot is written at the end.
+    const bool loader = warp >= nwarps - 8;
+    const int ljr = warp - (nwarps - 8);
+    int64_t nq0 = 0;
+    int ncnt = -1;                                          // CSR range of this warp's row of the next block row (-1: none)
+    auto peek_row = [&](int J) {
+        const int j = 8 * J + ljr;
+        ncnt = -1;
+        if (J < nb && j < n) { nq0 = P.row_ptr[base + j]; ncnt = (int)(P.row_ptr[base + j + 1] - nq0); }
+    };
+    if (loader) peek_row(Wb + 1);
     for (int I = 0; I < nb; ++I) {
+        const int Jn = I + Wb + 1;
+        double tv0 = 0.0, tv1 = 0.0, dvn = 0.0;
+        int tc0 = 0, tc1 = 0;
+        const int64_t q0c = nq0;
+        const int cntc = ncnt;
+        if (loader && cntc >= 0) {
+            const int m0 = lane - 1, m1 = lane + 31;
+            if (m0 >= 0 && m0 < cntc) { tv0 = Tf[q0c + m0]; tc0 = P.col_idx[q0c + m0]; }
+            if (m1 < cntc) { tv1 = Tf[q0c + m1]; tc1 = P.col_idx[q0c + m1]; }
+            dvn = 1.0 / Df[8 * Jn + ljr];
+            peek_row(Jn + 1);
+        }
         for (int d = warp; d <= Wb; d += nwarps) {
             const int K = I - d;
             double p0 = 0.0, p1 = 0.0, q0 = 0.0, q1 = 0.0;
@@ -1251,8 +1276,19 @@ __global__ void __launch_bounds__(ASMM_THREADS) assemble_band_mma_kernel(const S
             }
             if (i < n) *reinterpret_cast<double2 *>(band + (int64_t)i * Wr + 8 * (Wb - d) + 2 * t4) = make_double2(v0, v1);
         }
-        // block row I + Wb + 1 goes into the slot that is free during this step (the warps with the short chains do it)
-        if (warp >= nwarps - 8 && I + Wb + 1 < nb) load_row(I + Wb + 1, warp - (nwarps - 8));
+        if (loader && Jn < nb) {
+            const int sl = Jn % nslot, j = 8 * Jn + ljr, c0 = 8 * (Jn - Wb);
+            double *S = ring + ((size_t)sl * 8 + ljr) * pitch;
+            for (int e = lane; e < Wr; e += 32) S[e] = 0.0;
+            __syncwarp();
+            if (cntc >= 0) {
+                if (lane == 0) S[j - c0] = 1.0;
+                else if (lane - 1 < cntc) S[tc0 - c0] = tv0;
+                if (lane + 31 < cntc) S[tc1 - c0] = tv1;
+                for (int m = lane + 63; m < cntc; m += 32) S[P.col_idx[q0c + m] - c0] = Tf[q0c + m];   // (more than 63 predecessors)
+            }
+            if (lane == 0) dinv[sl * 8 + ljr] = dvn;
+        }
         __syncthreads();
     }
 }
