@@ -23,7 +23,7 @@ st, step = plain["stage_ms"], plain["ms_per_step"]
 json.dump(plain, open(os.path.join(P, f"{TAG}_bench_cfg3.json"), "w"), indent=1)
 
 MAIN = ("center_rows_kernel", "regress_qr_mma_kernel", "regress_clean_kernel", "regress_trunc_kernel", "replicate_rows_kernel",
-        "assemble_band_tile_kernel", "local_solve_kernel")
+        "assemble_band_mma_kernel", "assemble_band_tile_kernel", "local_solve_kernel")
 
 
 def short(name):
@@ -53,11 +53,11 @@ out = [f"ncu --metrics gpu__time_duration.sum --clock-control none -c 400, `pyth
        f"({step:.2f} ms/step; K2a {st['regress_qr']:.2f}, K2b {st['regress_solve']:.2f}, K3 {st['local_solve']:.2f}, K0 {st['center']:.2f} ms).", "",
        "| kernel | avg ms per step (ncu) | share of step (ncu) | share of step (CUDA events, no ncu) |", "|---|---|---|---|"]
 k2b = sum(avg.get(k, 0.0) for k in ("regress_clean_kernel", "regress_trunc_kernel", "replicate_rows_kernel"))
-k3 = sum(avg.get(k, 0.0) for k in ("assemble_band_tile_kernel", "local_solve_kernel"))
+k3 = sum(avg.get(k, 0.0) for k in ("assemble_band_mma_kernel", "assemble_band_tile_kernel", "local_solve_kernel"))
 for k, a in avg.items():
     if k in ev:
         es = f"{100 * ev[k] / step:.1f}%"
-    elif k in ("assemble_band_tile_kernel", "local_solve_kernel"):
+    elif k in ("assemble_band_mma_kernel", "assemble_band_tile_kernel", "local_solve_kernel"):
         es = f"K3a+K3b: {100 * st['local_solve'] / step:.1f}%"
     else:
         es = f"K2b (clean + trunc + replicate): {100 * st['regress_solve'] / step:.1f}%"
@@ -111,7 +111,7 @@ with open(os.path.join(P, f"{TAG}_ncu_full_bench_launch.csv"), "w") as f:   # re
 out = ["Functions and source lines with the most instructions / stall samples (ncu --set full --import-source on, one full-size launch of each",
        "kernel, cfg3 29 fields; `tools/ncu_lines.py` joins the SASS-level counters with nvdisasm line info; code inlined from CUDA headers keeps",
        "the header's name).", ""]
-for k in ("regress_qr_mma", "regress_clean", "regress_trunc", "local_solve", "assemble_band_tile"):
+for k in ("regress_qr_mma", "regress_clean", "regress_trunc", "local_solve", "assemble_band_mma"):
     txt = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_lines.py"), rep, k, "16"], capture_output=True, text=True).stdout
     out += ["## " + k, "", "```", txt.strip(), "```", ""]
 open(os.path.join(P, f"{TAG}_hot_lines_bench_cfg3.md"), "w").write("\n".join(out))
