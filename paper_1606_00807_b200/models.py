@@ -71,7 +71,8 @@ def propagate_device(model: ModelHandle, dX, dTmp, window=None):
     g = model.geometry
     src, dst = dX, dTmp
     for _ in range(steps):
-        _lib.check(_lib.lib().enkfmc_advdiff_step(src.data_ptr(), dst.data_ptr(), g.nx, g.ny, int(g.row_major), g.nfields,
+        _lib.check(_lib.lib().enkfmc_advdiff_step(src.data_ptr(), dst.data_ptr(), g.nx, g.ny, int(g.row_major),
+                                                  g.nfields * getattr(g, "nlev", 1),   # every level is advected as a 2-D field
                                                   src.shape[1], model.velocity[0], model.velocity[1], model.dt,
                                                   model.diffusivity, device.stream_ptr()))
         src, dst = dst, src
