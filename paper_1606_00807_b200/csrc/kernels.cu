@@ -1236,6 +1236,7 @@ __global__ void __launch_bounds__(ASMM_THREADS) assemble_band_mma_kernel(const S
         if (J < nb && j < n) { nq0 = P.row_ptr[base + j]; ncnt = (int)(P.row_ptr[base + j + 1] - nq0); }
     };
     if (loader) peek_row(Wb + 1);
+    int sI = 0;                                             // ring slot of block row I
     for (int I = 0; I < nb; ++I) {
         const int Jn = I + Wb + 1;
         double tv0 = 0.0, tv1 = 0.0, dvn = 0.0;
@@ -1254,14 +1255,17 @@ __global__ void __launch_bounds__(ASMM_THREADS) assemble_band_mma_kernel(const S
             double p0 = 0.0, p1 = 0.0, q0 = 0.0, q1 = 0.0;
             if (K >= 0) {
                 const int Jend = (I + Wb - d < nb - 1) ? I + Wb - d : nb - 1;
+                // slot of block row J walks the ring from the slot of row I; the tile columns move left by 8 per block row
+                int sl = sI, oi = 8 * Wb + g8, ok = 8 * (Wb - d) + g8;
                 for (int J = I; J <= Jend; ++J) {
-                    const int sl = J % nslot;
-                    const double *S = ring + ((size_t)sl * 8 + t4) * pitch + g8;
-                    const int oi = 8 * (I - J + Wb), ok = 8 * (K - J + Wb);
-                    const double a0 = S[oi] * dinv[sl * 8 + t4], a1 = S[(size_t)4 * pitch + oi] * dinv[sl * 8 + 4 + t4];
+                    const double *S = ring + ((size_t)sl * 8 + t4) * pitch;
+                    const double *dv = dinv + sl * 8 + t4;
+                    const double a0 = S[oi] * dv[0], a1 = S[(size_t)4 * pitch + oi] * dv[4];
                     const double b0 = S[ok], b1 = S[(size_t)4 * pitch + ok];
                     if ((J - I) & 1) { mma_f64(q0, q1, a0, b0); mma_f64(q0, q1, a1, b1); }
                     else { mma_f64(p0, p1, a0, b0); mma_f64(p0, p1, a1, b1); }
+                    sl = sl + 1 == nslot ? 0 : sl + 1;
+                    oi -= 8; ok -= 8;
                 }
             }
             double v0 = p0 + q0, v1 = p1 + q1;              // A[8 I + g8, 8 K + 2 t4 + {0, 1}]
@@ -1277,7 +1281,8 @@ __global__ void __launch_bounds__(ASMM_THREADS) assemble_band_mma_kernel(const S
             if (i < n) *reinterpret_cast<double2 *>(band + (int64_t)i * Wr + 8 * (Wb - d) + 2 * t4) = make_double2(v0, v1);
         }
         if (loader && Jn < nb) {
-            const int sl = Jn % nslot, j = 8 * Jn + ljr, c0 = 8 * (Jn - Wb);
+            const int sl = sI == 0 ? nslot - 1 : sI - 1;     // slot of row I + Wb + 1 = slot of row I - 1 (Wb + 2 slots)
+            const int j = 8 * Jn + ljr, c0 = 8 * (Jn - Wb);
             double *S = ring + ((size_t)sl * 8 + ljr) * pitch;
             for (int e = lane; e < Wr; e += 32) S[e] = 0.0;
             __syncwarp();
@@ -1290,6 +1295,7 @@ __global__ void __launch_bounds__(ASMM_THREADS) assemble_band_mma_kernel(const S
             if (lane == 0) dinv[sl * 8 + ljr] = dvn;
         }
         __syncthreads();
+        sI = sI + 1 == nslot ? 0 : sI + 1;
     }
 }
 

@@ -468,8 +468,8 @@ __device__ __noinline__ int jacobi_solve(double *W, int ld, int K, int p, double
 }
 
 // offset of column j inside a packed R with K rows: sum_{i<j} min(i+1, K)
-__device__ __forceinline__ int64_t packed_col_offset(int j, int K) {
-    return j <= K ? (int64_t)j * (j + 1) / 2 : (int64_t)K * (K + 1) / 2 + (int64_t)(j - K) * K;
+__device__ __forceinline__ int packed_col_offset(int j, int K) {     // (j, K <= 256: 32-bit arithmetic)
+    return j <= K ? (j * (j + 1)) >> 1 : ((K * (K + 1)) >> 1) + (j - K) * K;
 }
 
 // Packed block -> dense [R | c] with p rows (rows >= K and the strict lower part are zero); p <= 32 PS.
