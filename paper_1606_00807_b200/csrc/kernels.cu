@@ -1492,11 +1492,14 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
             double a[8], v[8];
 #pragma unroll
             for (int c = 0; c < 8; ++c) { a[c] = (c <= r) ? Dg[(size_t)r * pitch + c] : 0.0; v[c] = (c == r) ? 1.0 : 0.0; }
-            const double d0 = Aw[(size_t)(sJ + r) * pitch + Wr];          // A_rr before any elimination
+            double og[8];                                                // A_cc before any elimination (uniform loads: kept out of the chain)
+#pragma unroll
+            for (int c = 0; c < 8; ++c) og[c] = Aw[(size_t)(sJ + c) * pitch + Wr];
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
                 double piv = __shfl_sync(FULL, a[c], c);
-                const double orig = __shfl_sync(FULL, d0, c);
+                double inv = rsqrt(piv);                                 // issued before the pivot test: replaced below in the rare cases
+                const double orig = og[c];
                 // A = T~^T D^-1 T~ + H^T R^-1 H is positive (semi-)definite by construction.
                 bool pin = false;
                 // The scale a pivot is judged against: the largest pivot so far, or the row's own diagonal before
@@ -1507,15 +1510,15 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
                 // (gmax): the elimination error of a pivot scales with |A|, which the entries met so far underestimate when
                 // the large rows come later (deep levels of a vertically coupled tile: |A| 1e15 against 1e12).  NaN / inf fail.
                 const double scale = fmax(pivmax, orig);
-                if (!(piv == piv) || !(fabs(piv) < DBL_MAX)) { if (lane == 0 && s_fail == 0) s_fail = 2; }
-                else if (!(piv > 1e-13 * scale)) {
-                    if ((pivmax == 0.0 && !(piv > 0.0)) || piv < -1e-8 * fmax(scale, gmax)) { if (lane == 0 && s_fail == 0) s_fail = 1; }
+                if (!(piv > 1e-13 * scale) || !(piv < DBL_MAX)) {        // rare and warp-uniform: NaN / inf, noise-level or negative pivot
+                    if (!(piv == piv) || !(fabs(piv) < DBL_MAX)) { if (lane == 0 && s_fail == 0) s_fail = 2; }
+                    else if ((pivmax == 0.0 && !(piv > 0.0)) || piv < -1e-8 * fmax(scale, gmax)) { if (lane == 0 && s_fail == 0) s_fail = 1; }
                     else { pin = true; if (lane == 0) atomicAdd(P.counter + 1, 1u); }
+                    // a pinned variable gets the pivot +infinity: column of L zero, unit diagonal, zero increment -- no
+                    // element growth, unlike a tiny positive pivot
+                    if (pin) inv = 0.0;
                 }
                 pivmax = fmax(pivmax, piv);
-                // a pinned variable gets the pivot +infinity: column of L zero, unit diagonal, zero increment -- no
-                // element growth, unlike a tiny positive pivot
-                const double inv = pin ? 0.0 : rsqrt(piv);
                 a[c] = (r == c) ? (pin ? 1.0 : piv * inv) : a[c] * inv;   // column c of L
 #pragma unroll
                 for (int k = 0; k <= c; ++k) if (r == c) v[k] *= inv; // row c of L^-1 is final
