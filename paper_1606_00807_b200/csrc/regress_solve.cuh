@@ -594,13 +594,19 @@ __global__ void __launch_bounds__(512, 1) regress_clean_kernel(const RegressPara
             double dmin = DBL_MAX, dmax = 0.0, fro2 = 0.0;
             unpack_rc<PS>(in, W, ld, p, K, lane, &fro2);
             __syncwarp();
+            int jmin = 0;                                // column of the smallest pivot (smallest index among ties)
             for (int j = lane; j < K; j += 32) {
                 const double v = W[(size_t)j * ld + j];
                 rinv[j] = 1.0 / v;
-                dmin = fmin(dmin, fabs(v));
+                if (fabs(v) < dmin) { dmin = fabs(v); jmin = j; }
                 dmax = fmax(dmax, fabs(v));
             }
-            dmin = warp_min(dmin);
+            {
+                const double mine = dmin;
+                dmin = warp_min(dmin);
+                const unsigned who = __ballot_sync(FULL, mine == dmin);
+                jmin = __shfl_sync(FULL, jmin, __ffs(who) - 1);
+            }
             dmax = warp_max(dmax);
             e2 = in[packed_col_offset(p, K) + K];
             __syncwarp();
@@ -615,14 +621,14 @@ __global__ void __launch_bounds__(512, 1) regress_clean_kernel(const RegressPara
                     // converges to a value s_1 that is provably below the threshold and the rest of the spectrum is provably
                     // above it -- sum_{i>=2} 1/s_i^2 = |X|_F^2 - 1/s_1^2 bounds s_2 from below -- the row is finished here
                     // with the single pair deflated; anything else goes to the block kernel.
+                    // Start: column jmin of X = R^-1 (the certificate left X in W), i.e. half an inverse-iteration step from the
+                    // unit vector of the smallest pivot -- the direction in which R is nearly singular is already amplified by
+                    // 1 / s_1 in it.  (X[r, c] for r < c sits at W[r ld + c], the diagonal in rinv, zero below.)
                     Vec<PS> z, yt;
-                    const unsigned seed = (unsigned)P.state_row[q] * 7919u + (unsigned)p * 104729u;
 #pragma unroll
                     for (int t = 0; t < PS; ++t) {
                         const int e = lane + 32 * t;
-                        unsigned h = (unsigned)(e + 1) * 2654435761u ^ (seed * 40503u + 0x9e3779b9u);
-                        h ^= h >> 15; h *= 2246822519u; h ^= h >> 13; h *= 3266489917u; h ^= h >> 16;
-                        z.v[t] = e < p ? (double)(h >> 8) * (1.0 / 8388608.0) - 1.0 : 0.0;
+                        z.v[t] = e < jmin ? W[(size_t)e * ld + jmin] : (e == jmin ? rinv[jmin] : 0.0);
                     }
                     {
                         const double inv = rsqrt(vdot<PS>(z, z));
