@@ -39,6 +39,7 @@
 
 #define JACOBI_MAX_SWEEPS 30
 #define TRUNC_MAX_SWEEPS 16
+#define REG_PROBE_TOL 1e-10    // K2b-1 probe: predicted distance of the iterate to the singular vector at which it stops
 
 __host__ __device__ inline int trunc_zp(int pmax) { return 8 * ((pmax + 7) / 8) + 4; }   // block pitch: = 4 mod 8
 __host__ __device__ inline size_t regress_clean_ws_doubles(int pmax) {
@@ -656,8 +657,11 @@ __global__ void __launch_bounds__(512, 1) regress_clean_kernel(const RegressPara
                         dz = sqrt(warp_sum(dz));
                         if ((dz < 1e-6 && dz > 0.9 * dz_old) || dz < 1e-12) conv = true;          // at the rounding floor
                         // linear convergence with ratio q = dz / dz_old: the iterate just computed is within dz q / (1 - q) of
-                        // the limit -- stop once that is at the 5e-14 level
-                        else if (it >= 2 && dz < 0.25 * dz_old && dz * dz < 4e-14 * dz_old) conv = true;
+                        // the limit -- stop once that is at the 1e-10 level.  The vector enters T to first order, so this is
+                        // a relative 1e-10 in T: a tenth of the north_star gate and a tenth of the distance of the reference's
+                        // own LAPACK answer from the exact one on these inputs (1.1e-9, oracle/noise_floor.py); measured T / D /
+                        // Xa errors against the oracle are unchanged from the 5e-14 level used before.
+                        else if (it >= 2 && dz < 0.25 * dz_old && dz * dz < REG_PROBE_TOL * dz_old) conv = true;
                         else if (it >= 3 && dz > 0.3 * dz_old) break;                                // close values: a block is the better tool
                         dz_old = dz;
                     }
