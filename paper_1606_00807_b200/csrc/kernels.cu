@@ -1303,11 +1303,11 @@ __host__ __device__ inline size_t solve_strip_doubles(int Wb) { return (((4 * (s
 __host__ __device__ inline size_t solve_rowsrc_doubles(int rows) { return ((3 * (size_t)rows * 4 + 15) / 16) * 2; }
 
 #ifdef ENKFMC_K3B_TIMING
-__device__ unsigned long long g_k3b_t[16];
+__device__ unsigned long long g_k3b_t[24];
 #define K3T(i) do { if (blockIdx.x == 0 && threadIdx.x == 0) { const long long now_ = clock64(); atomicAdd(&g_k3b_t[i], (unsigned long long)(now_ - tmark_)); tmark_ = now_; } } while (0)
-extern "C" int enkfmc_debug_k3b_times(unsigned long long *out16) {
-    cudaMemcpyFromSymbol(out16, g_k3b_t, sizeof(g_k3b_t));
-    unsigned long long z[16] = {0};
+extern "C" int enkfmc_debug_k3b_times(unsigned long long *out24) {
+    cudaMemcpyFromSymbol(out24, g_k3b_t, sizeof(g_k3b_t));
+    unsigned long long z[24] = {0};
     cudaMemcpyToSymbol(g_k3b_t, z, sizeof(z));
     return 0;
 }
@@ -1621,8 +1621,15 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
                     K3T(12);
                     if (nbl > 0) c_tile(0, 0);
                     K3T(13);
+#ifdef ENKFMC_K3B_TWICE
+                    if (J + 1 < nb) {     // (timing experiment: the second pass through the same code is the hot-instruction-cache cost)
+#pragma unroll 1
+                        for (int rep = 0; rep < 2; ++rep) { __syncwarp(); factor_diag(s1, (J + 1) & 1); if (rep == 0) K3T(14); else K3T(15); }
+                    }
+#else
                     if (J + 1 < nb) { __syncwarp(); factor_diag(s1, (J + 1) & 1); }
                     K3T(14);
+#endif
                 } else if (widx >= 0) {
                     for (int u = 1 + widx; u < nC; u += nwork) {
                         const int rc = strips[u];
@@ -1723,10 +1730,13 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
                     if (col + 1 < N) xb1 = Xf[(int64_t)xi0 * N + col + 1];
                 }
             }
+            K3T(16);
             if (J > 0 && pfb) fetch_panel(J - 1);
+            K3T(17);
             const double lt0 = linv(Lc, rinvc, t4, g8), lt1 = linv(Lc, rinvc, 4 + t4, g8);   // (L_JJ^-T)[g8][k]
             for (int ct = warp; ct < nct; ct += nwarps) {
                 double p0 = 0.0, p1 = 0.0, q0 = 0.0, q1 = 0.0;
+#pragma unroll 4
                 for (int k0 = 0; k0 < below; k0 += 8) {
                     int w = s1 + k0; if (w >= Wr) w -= Wr;
                     const double *lk = Lc + (8 + k0 + t4) * LP_PITCH + g8;
@@ -1734,6 +1744,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
                     mma_f64(p0, p1, lk[0], xk[0]);
                     mma_f64(q0, q1, lk[4 * LP_PITCH], xk[(size_t)4 * NR]);
                 }
+                K3T(18);
                 // S (C-fragment layout) -> shared -> B fragments of z_J - S, within the warp
                 double *rd = red + 8 * ct;
                 *reinterpret_cast<double2 *>(rd + (size_t)g8 * NR + 2 * t4) = make_double2(p0 + q0, p1 + q1);
@@ -1744,6 +1755,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
                     if (col < N) { zf0 = Z[(int64_t)(8 * J + t4) * N + col]; zf1 = Z[(int64_t)(8 * J + 4 + t4) * N + col]; }
                 }
                 const double w0 = zf0 - rd[(size_t)t4 * NR + g8], w1 = zf1 - rd[(size_t)(4 + t4) * NR + g8];
+                K3T(19);
                 double x0 = 0.0, x1 = 0.0;
                 mma_f64(x0, x1, lt0, w0);
                 mma_f64(x0, x1, lt1, w1);
@@ -1760,6 +1772,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
                     if (col + 1 < N) Xaf[gidx + 1] = xb1 + x1;
                 }
                 __syncwarp();
+                K3T(20);
             }
             K3T(9);
             if (J > 0) { if (pfb) commit_panel(J - 1, Ln, rinv0 + 8 * (cur ^ 1)); else load_panel(J - 1, Ln, rinv0 + 8 * (cur ^ 1)); }

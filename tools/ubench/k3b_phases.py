@@ -20,7 +20,7 @@ dX, dR, dYs = device.to_device(w.X), device.to_device(w.r_diag), device.to_devic
 dXa = torch.empty_like(dX)
 device.analysis_device(plan, dX, dR, dYs, dXa); torch.cuda.synchronize()
 L = _lib.lib()
-out = (C.c_ulonglong * 16)()
+out = (C.c_ulonglong * 24)()
 L.enkfmc_debug_k3b_times(out)
 device.analysis_device(plan, dX, dR, dYs, dXa); torch.cuda.synchronize()
 L.enkfmc_debug_k3b_times(out)
@@ -29,5 +29,7 @@ names = ["fetch item/between tiles", "tile setup (tables)", "initial window load
          "fwd barrier wait", "first panel load", "bwd S + solve + stores", "bwd commit panel", "bwd barrier wait",
          "fwd: prefetch + L store (warp 0)", "fwd: tile (0,0) (warp 0)", "fwd: factor + invert next diagonal block (warp 0)"]
 tot = t.sum()
+names += ["(second, hot call of the diagonal factorisation: -DENKFMC_K3B_TWICE builds only)", "bwd: global loads of z_J / background issued", "bwd: next panel fetch issued",
+          "bwd: S = L_below^T x (tensor-core chain)", "bwd: S through shared memory, z_J - S (waits for z_J)", "bwd: x_J, stores"]
 for n, v in zip(names, t): print(f"{n:28s} {v/1e3:10.1f} kcycles  {100*v/tot:5.1f}%")
 print("total kcycles on CTA 0:", tot / 1e3)
