@@ -897,7 +897,7 @@ __global__ void __launch_bounds__(256, 1) regress_trunc_kernel(const RegressPara
                 const double marg = warp_max(est < 2.0 * thr_hi ? est : 0.0);         // largest estimate near / below the threshold
                 if (marg > 0.0) {
                     const double lr = 2.0 * log(marg / top);                          // log of the contraction per sweep (< 0)
-                    int n = lr < -2.5 ? (int)ceil(-29.9 / lr) : TRUNC_MAX_SWEEPS;     // 1e-13 after n sweeps
+                    int n = lr < -2.5 ? (int)ceil(-23.0 / lr) : TRUNC_MAX_SWEEPS;     // 1e-10 after n sweeps
                     if (n > TRUNC_MAX_SWEEPS) n = TRUNC_MAX_SWEEPS;
                     if (n > need) need = n;
                 }
