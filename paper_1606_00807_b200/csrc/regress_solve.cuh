@@ -671,16 +671,24 @@ __global__ void __launch_bounds__(512, 1) regress_clean_kernel(const RegressPara
                         const double ny = sqrt(vdot<PS>(yt, yt));
                         sv = 1.0 / ny;
                         double smax_lo = dmax;
+                        bool pw_used = false;
                         if (!(sv < P.rank_tol * smax_lo * (1.0 - 1e-3))) {       // sharpen the lower bound of s_max: two power steps
+                            pw_used = true;
                             Vec<PS> v;
                             const double v0 = rsqrt((double)p);
 #pragma unroll
                             for (int t = 0; t < PS; ++t) v.v[t] = (lane + 32 * t < p) ? v0 : 0.0;
+                            // every half step gives a lower bound (|R v| <= sqrt |R^T R v| <= s_max for unit v); on smooth
+                            // ensembles the first one, |R 1| / sqrt(p), is already within a few per cent: stop as soon as the
+                            // bound settles the question
                             for (int pw = 0; pw < 2; ++pw) {
                                 const Vec<PS> y = mul_upper<PS>(v, W, ld, p, lane);
+                                smax_lo = fmax(smax_lo, sqrt(vdot<PS>(y, y)));
+                                if (sv < P.rank_tol * smax_lo * (1.0 - 1e-3)) break;
                                 v = mul_upper_t<PS>(y, W, ld, p, lane);
                                 const double nv = sqrt(vdot<PS>(v, v));
                                 smax_lo = fmax(smax_lo, sqrt(nv));
+                                if (sv < P.rank_tol * smax_lo * (1.0 - 1e-3)) break;
                                 const double inv = 1.0 / nv;
 #pragma unroll
                                 for (int t = 0; t < PS; ++t) v.v[t] *= inv;
@@ -717,7 +725,7 @@ __global__ void __launch_bounds__(512, 1) regress_clean_kernel(const RegressPara
                             if (lane == 0) {
                                 const double d = (e2 + rest2) / denom;
                                 P.D[(int64_t)f * P.dstride + q] = fmax(d, P.variance_floor);
-                                if (P.flags) P.flags[(int64_t)f * P.dstride + q] = 2 | 32 | (d < P.variance_floor ? 8 : 0) | ((nsteps < 255 ? nsteps : 255) << 8);
+                                if (P.flags) P.flags[(int64_t)f * P.dstride + q] = 2 | 32 | (pw_used ? 64 : 0) | (d < P.variance_floor ? 8 : 0) | ((nsteps < 255 ? nsteps : 255) << 8);
                             }
                             __syncwarp();
                             continue;

@@ -51,3 +51,5 @@ if fb.any():
     print("Jacobi sweeps per fallback row: mean %.1f, histogram" % ((flags[fb] >> 16) & 63).mean(), np.bincount((flags[fb] >> 16) & 63, minlength=31)[:31])
 fl = plan.work(w.nens)
 print("algorithmic GF regress/solve:", fl[2] / 1e9, fl[1] / 1e9, " -> TF/s", fl[2] / ((ms[1] + ms[2]) / n) / 1e9, fl[1] / (ms[3] / n) / 1e9)
+single = ((flags & 32) > 0) & ((flags & 16) == 0) & ((flags & 1) == 0)
+print("K2b-1 single-pair rows: %d, of which the s_max bound had to be sharpened by power steps: %d" % (int(single.sum()), int((single & ((flags & 64) > 0)).sum())))
