@@ -39,6 +39,7 @@
 
 #define JACOBI_MAX_SWEEPS 30
 #define TRUNC_MAX_SWEEPS 16
+#define UNPACK_COLS 8          // columns of the packed R fetched together by unpack_rc
 #define REG_PROBE_TOL 1e-10    // K2b-1 probe: predicted distance of the iterate to the singular vector at which it stops
 
 __host__ __device__ inline int trunc_zp(int pmax) { return 8 * ((pmax + 7) / 8) + 4; }   // block pitch: = 4 mod 8
@@ -78,21 +79,32 @@ __device__ __noinline__ double inverse_norm2_mma(double *W, const double *rinv, 
     const int t4 = lane & 3, m = lane >> 2;
     const int nbk = (p + 7) >> 3;
     double f2 = 0.0;
-    // diagonal blocks, four at a time: lanes 8 g .. 8 g + 7 own the columns of block jb0 + g (back-substitution per column)
+    // diagonal blocks, four at a time: lanes 8 g .. 8 g + 7 own the columns of block jb0 + g.  Column c of X_jj by
+    // back-substitution held in registers (x[i] = 0 below the diagonal, so every lane runs the same unrolled sums):
+    // x_c = 1 / r_cc, x_k = -(sum_{i > k} r_ki x_i) / r_kk.  The block of R is read with block-uniform addresses.
     for (int jb0 = 0; jb0 < nbk; jb0 += 4) {
         const int j = jb0 + (lane >> 3), l8 = lane & 7;
         const int c = 8 * j + l8;
         const bool act = c < p;
-        const double rc = act ? rinv[c] : 0.0;
-        f2 += rc * rc;
-        for (int kk = 6; kk >= 0; --kk) {
-            if (act && l8 > kk) {
-                const int k = 8 * j + kk;
-                double acc = W[(size_t)c * ld + k] * rc;                        // R[k,c] X[c,c]
-                for (int i = k + 1; i < c; ++i) acc += W[(size_t)i * ld + k] * W[(size_t)i * ld + c];   // R[k,i] X[i,c]
-                const double x = -rinv[k] * acc;
-                W[(size_t)k * ld + c] = x;
-                f2 += x * x;
+        const int j8 = 8 * (j < nbk ? j : nbk - 1);              // (lanes beyond the last block read a valid one; nothing is stored)
+        double x[8];
+#pragma unroll
+        for (int kk = 7; kk >= 0; --kk) {
+            const int k = j8 + kk;
+            const double rk = k < p ? rinv[k] : 0.0;
+            double acc = 0.0;
+#pragma unroll
+            for (int i = kk + 1; i < 8; ++i) {
+                const int ci = j8 + i;
+                acc = fma(ci < p ? W[(size_t)ci * ld + k] : 0.0, x[i], acc);        // R[k, ci] X[ci, c]
+            }
+            x[kk] = kk == l8 ? rk : (kk < l8 ? -rk * acc : 0.0);
+        }
+        if (act) {
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+                if (kk < l8) W[(size_t)(j8 + kk) * ld + c] = x[kk];                  // X[k, c] at (row c, column k)
+                if (kk <= l8) f2 = fma(x[kk], x[kk], f2);
             }
         }
     }
@@ -479,10 +491,10 @@ template <int PS>
 __device__ __forceinline__ void unpack_rc(const double *in, double *W, int ld, int p, int K, int lane,
                                           double *fro2 = nullptr) {
     double f2 = 0.0;
-    for (int j0 = 0; j0 <= p; j0 += 4) {               // four columns in flight: the loads are latency-bound
-        double v[4][PS];
+    for (int j0 = 0; j0 <= p; j0 += UNPACK_COLS) {     // several columns in flight: the loads are latency-bound (DRAM: K2a's output is far larger than L2)
+        double v[UNPACK_COLS][PS];
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
+        for (int b = 0; b < UNPACK_COLS; ++b) {
             const int j = j0 + b <= p ? j0 + b : p;
             const int h = j < p ? (j + 1 < K ? j + 1 : K) : K;
             const double *src = in + packed_col_offset(j, K);
@@ -490,7 +502,7 @@ __device__ __forceinline__ void unpack_rc(const double *in, double *W, int ld, i
             for (int t = 0; t < PS; ++t) { const int i = lane + 32 * t; v[b][t] = i < h ? src[i] : 0.0; }
         }
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
+        for (int b = 0; b < UNPACK_COLS; ++b) {
             const int j = j0 + b;
             if (j > p) break;
             double *col = W + (size_t)j * ld;
