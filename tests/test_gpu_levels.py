@@ -183,3 +183,16 @@ def test_run_filter_with_coupled_levels():
         x = mck.EnsembleState(advdiff_host(xa.X, model.steps_per_window), role="background")
     assert np.array_equal(res.final.X, x.X)
     assert not np.array_equal(res.analyses[0].X, w.X)
+
+
+def test_too_many_coupled_predecessors_are_refused():
+    """Config 5 as worded (horizontal radius 5, vertical radius 1) has 60 + 121 = 181 predecessors: beyond the 128 the regression
+    kernels hold; the analysis is refused with CapacityError instead of running something else."""
+    import paper_1606_00807_b200 as mck
+    from paper_1606_00807_b200 import synthetic
+    w = synthetic.make_workload("cap", nx=40, ny=24, nens=24, corr_len=3.0, zeta=5, delta=4, obs="random", obs_arg=0.3,
+                                r_rel=0.1, r_abs=None, seed=33, nugget=0.02, variables=[("a", 1.0, 2)])
+    geo = mck.GridGeometry("grid2d", w.nx, w.ny, nlev=2, zeta_v=1)
+    net = mck.ObservationNetwork(w.obs_indices, w.r_diag, w.y)
+    with pytest.raises(mck.CapacityError, match="predecessor"):
+        mck.assimilate_parallel(mck.EnsembleState(w.X), net, mck.AssimilationConfig(zeta=w.zeta, delta=w.delta), geo, Ys=w.Ys)
