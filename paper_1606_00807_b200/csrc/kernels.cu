@@ -1588,6 +1588,9 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
             }
             __syncthreads();
             K3T(4);
+            // (e) block row J of the window (A rows and right-hand sides) was consumed by (b): the next block row goes into its slot
+            // now, which also ends the life of the prefetch registers before the serial factorisation below
+            if (more) { if (pf) commit_block_row(sJ, s1); else load_block_row(J + Wb + 1); }
             // L block -> global (overwrites the A rows of block J, already consumed)
             for (int e = tid; e < (8 + below) * 8; e += nthreads)
                 band[(int64_t)8 * J * Wr + e] = Lp[(e >> 3) * LP_PITCH + (e & 7)];
@@ -1655,7 +1658,6 @@ __global__ void __launch_bounds__(SOLVE_THREADS) local_solve_kernel(const SolveP
                 }
             }
             K3T(5);
-            if (more) { if (pf) commit_block_row(sJ, s1); else load_block_row(J + Wb + 1); }
             K3T(6);
             __syncthreads();
             K3T(7);
