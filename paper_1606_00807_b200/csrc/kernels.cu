@@ -1169,8 +1169,8 @@ __global__ void __launch_bounds__(ASMT_THREADS) assemble_band_tile_kernel(const 
 
 // Tensor-core form of K3a: A = T~^T D^-1 T~ as a banded SYRK of 8 x 8 tiles, one CTA per (field, tile).  For tiles whose
 // physical order is the local order (every clipped tile) T~ is lower triangular with its entries inside the band, so
-//     A[I, K] = sum_{J = I}^{K + Wb} T~[J, I]^T D_J^-1 T~[J, K]        (8 x 8 blocks, K <= I <= K + Wb).
-// Block rows of T~ are scattered from the CSR values into a ring of Wb + 2 dense 8 x Wr slots in shared memory (zeros where
+//     A[I, K] = sum_{J = I}^{K + Wb} C[J, I]^T C[J, K],  C = D^-1/2 T~   (8 x 8 blocks, K <= I <= K + Wb).
+// Block rows of C are scattered from the CSR values into a ring of Wb + 2 dense 8 x Wr slots in shared memory (zeros where
 // the pattern has no entry); block row I of A then takes (Wb + 1)(Wb + 2) / 2 tile products of two mma.m8n8k4 each: warp d
 // accumulates tile (I, I - d) over its J in ascending order (two interleaved accumulator chains, added at the end: a fixed
 // order, results are deterministic), while the warps with the short chains scatter block row I + Wb + 1 into the free slot --
@@ -1180,7 +1180,7 @@ __global__ void __launch_bounds__(ASMT_THREADS) assemble_band_tile_kernel(const 
 __host__ __device__ inline int asmm_pitch(int Wr) { int v = Wr + 4; while (v % 16 != 4) ++v; return v; }   // fragment loads t4 * pitch + g8: conflict-free
 __host__ __device__ inline size_t asmm_smem_bytes(int bmax) {
     const int Wr = 8 * (solve_wb(bmax) + 1);
-    return ((size_t)(Wr + 8) * asmm_pitch(Wr) + (size_t)(Wr + 8)) * sizeof(double);
+    return (size_t)(Wr + 8) * asmm_pitch(Wr) * sizeof(double);
 }
 
 __global__ void __launch_bounds__(ASMM_THREADS) assemble_band_mma_kernel(const SolveParams P) {
@@ -1195,7 +1195,6 @@ __global__ void __launch_bounds__(ASMM_THREADS) assemble_band_mma_kernel(const S
     const int n = (int)(P.tile_ptr[t + 1] - base), nb = (n + 7) >> 3;
     const int Wb = solve_wb(P.bw[t]), Wr = 8 * (Wb + 1), pitch = asmm_pitch(Wr), nslot = Wb + 2;
     double *ring = smem;                                   // [nslot][8][pitch]
-    double *dinv = ring + (size_t)nslot * 8 * pitch;       // [nslot][8]
     const double *Tf = P.T + (int64_t)f * P.tstride;
     const double *Df = P.D + (int64_t)f * P.dstride + base;
     double *band = P.band + (int64_t)fl * P.band_stride + P.band_ptr[t];
@@ -1206,18 +1205,16 @@ __global__ void __launch_bounds__(ASMM_THREADS) assemble_band_mma_kernel(const S
         double *S = ring + ((size_t)sl * 8 + jr) * pitch;
         for (int e = lane; e < Wr; e += 32) S[e] = 0.0;
         __syncwarp();
-        double dv = 0.0;
         if (j < n) {
             const int c0 = 8 * (J - Wb);
             const int64_t q0 = P.row_ptr[base + j];
             const int cnt = (int)(P.row_ptr[base + j + 1] - q0);
+            const double sc = rsqrt(Df[j]);              // row j of D^-1/2 T~ (factors.py:140-143 forms the same matrix)
             for (int m = lane - 1; m < cnt; m += 32) {
-                if (m < 0) S[j - c0] = 1.0;
-                else S[P.col_idx[q0 + m] - c0] = Tf[q0 + m];
+                if (m < 0) S[j - c0] = sc;
+                else S[P.col_idx[q0 + m] - c0] = Tf[q0 + m] * sc;
             }
-            dv = 1.0 / Df[j];
         }
-        if (lane == 0) dinv[sl * 8 + jr] = dv;
     };
     for (int idx = warp; idx < 8 * (Wb + 1); idx += nwarps)
         if ((idx >> 3) < nb) load_row(idx >> 3, idx & 7);
@@ -1247,7 +1244,7 @@ __global__ void __launch_bounds__(ASMM_THREADS) assemble_band_mma_kernel(const S
             const int m0 = lane - 1, m1 = lane + 31;
             if (m0 >= 0 && m0 < cntc) { tv0 = Tf[q0c + m0]; tc0 = P.col_idx[q0c + m0]; }
             if (m1 < cntc) { tv1 = Tf[q0c + m1]; tc1 = P.col_idx[q0c + m1]; }
-            dvn = 1.0 / Df[8 * Jn + ljr];
+            dvn = rsqrt(Df[8 * Jn + ljr]);
             peek_row(Jn + 1);
         }
         for (int d = warp; d <= Wb; d += nwarps) {
@@ -1259,8 +1256,7 @@ __global__ void __launch_bounds__(ASMM_THREADS) assemble_band_mma_kernel(const S
                 int sl = sI, oi = 8 * Wb + g8, ok = 8 * (Wb - d) + g8;
                 for (int J = I; J <= Jend; ++J) {
                     const double *S = ring + ((size_t)sl * 8 + t4) * pitch;
-                    const double *dv = dinv + sl * 8 + t4;
-                    const double a0 = S[oi] * dv[0], a1 = S[(size_t)4 * pitch + oi] * dv[4];
+                    const double a0 = S[oi], a1 = S[(size_t)4 * pitch + oi];
                     const double b0 = S[ok], b1 = S[(size_t)4 * pitch + ok];
                     if ((J - I) & 1) { mma_f64(q0, q1, a0, b0); mma_f64(q0, q1, a1, b1); }
                     else { mma_f64(p0, p1, a0, b0); mma_f64(p0, p1, a1, b1); }
@@ -1287,12 +1283,11 @@ __global__ void __launch_bounds__(ASMM_THREADS) assemble_band_mma_kernel(const S
             for (int e = lane; e < Wr; e += 32) S[e] = 0.0;
             __syncwarp();
             if (cntc >= 0) {
-                if (lane == 0) S[j - c0] = 1.0;
-                else if (lane - 1 < cntc) S[tc0 - c0] = tv0;
-                if (lane + 31 < cntc) S[tc1 - c0] = tv1;
-                for (int m = lane + 63; m < cntc; m += 32) S[P.col_idx[q0c + m] - c0] = Tf[q0c + m];   // (more than 63 predecessors)
+                if (lane == 0) S[j - c0] = dvn;
+                else if (lane - 1 < cntc) S[tc0 - c0] = tv0 * dvn;
+                if (lane + 31 < cntc) S[tc1 - c0] = tv1 * dvn;
+                for (int m = lane + 63; m < cntc; m += 32) S[P.col_idx[q0c + m] - c0] = Tf[q0c + m] * dvn;   // (more than 63 predecessors)
             }
-            if (lane == 0) dinv[sl * 8 + ljr] = dvn;
         }
         __syncthreads();
         sI = sI + 1 == nslot ? 0 : sI + 1;
