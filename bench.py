@@ -387,7 +387,7 @@ def run_b200(args, rank, world, local_rank):
                            "(EnsembleState, ObservationNetwork, AssimilationConfig, GridGeometry, Ys=)",
                     "inputs": "page-locked host arrays"},
             "e2e_pageable": {"value": nstate / t_e2e_pageable, "unit": UNIT, "ms_per_step": t_e2e_pageable * 1e3,
-                             "inputs": "ordinary (pageable) numpy arrays: a staged copy blocks the host, so the upload of group g + 1 is issued right after the kernels of group g and is staged while they run"},
+                             "inputs": "ordinary (pageable) numpy arrays: a staged copy blocks the host, so the fields go in 12 groups and the upload of group g + 1 is issued right after the kernels of group g and is staged while they run"},
             "gpu_launches": int(launches),
             "clocks": summarize_clocks(samples),
             "parity_vs_cpu_sample": parity, "parity_gate": parity_gate, "clamped_pivots": int(clamped),
