@@ -44,8 +44,8 @@
 
 __host__ __device__ inline int trunc_zp(int pmax) { return 8 * ((pmax + 7) / 8) + 4; }   // block pitch: = 4 mod 8
 __host__ __device__ inline size_t regress_clean_ws_doubles(int pmax) {
-    // R | c (pitch pmax|1, pmax+1 columns) | rinv | aux | mma staging
-    const size_t d = (size_t)(pmax | 1) * (pmax + 1) + (size_t)2 * pmax + 64;
+    // R | c (pitch pmax|1, pmax+1 columns) | rinv | mma staging
+    const size_t d = (size_t)(pmax | 1) * (pmax + 1) + (size_t)pmax + 64;
     return (d + 1) & ~(size_t)1;
 }
 __host__ __device__ inline size_t regress_trunc_ws_doubles(int pmax, int bmax) {
@@ -583,8 +583,7 @@ __global__ void __launch_bounds__(512, 1) regress_clean_kernel(const RegressPara
     const int N = P.N, pmax = P.pmax, ld = pmax | 1;
     double *W = smem + (size_t)(threadIdx.x >> 5) * regress_clean_ws_doubles(pmax);
     double *rinv = W + (size_t)ld * (pmax + 1);
-    double *aux = rinv + pmax;
-    double *stage = aux + pmax;
+    double *stage = rinv + pmax;
     const double denom = (double)(N - 1);
     const unsigned nf = (unsigned)(P.f1 - P.f0);
 
